@@ -1,0 +1,210 @@
+/*
+ * aim.h -- C ABI of the B200-native AIM-accelerated EFIE matvec / GMRES
+ * (hot path of Patel, Triverio, Hum, arXiv 1712.02443, §V "Acceleration with
+ * AIM"; operator readings D1-D17 in SURVEY.md §8(c) and
+ * DESIGN.md).
+ *
+ * The operator (eq. Gouter1, reading D1):
+ *
+ *   Z_eq = Z_corr + j k eta0 ( sum_{psi=x,y,z} P_psi^T H P_psi - k^-2 P_phi^T H P_phi )
+ *
+ *   P_psi   projection onto an AIM grid of spacing h, stencil order M,
+ *           (M+1)^3 nodes per RWG (step (i); D2, D3, D4)
+ *   H       Toeplitz convolution with G(R) = exp(-jkR)/(4 pi R), G(0) = 0
+ *           (step (ii), eq. AIM_step2; D6, D11, D12)
+ *   P^T     interpolation (step (iii))
+ *   Z_corr  near-field precorrection on pairs ||c_m - c_n|| <= near_radius
+ *           (D5, D8, D9)
+ *
+ * Conventions for every entry point:
+ *   - Complex numbers are interleaved (re, im) float64 pairs (complex128).
+ *   - Vectors x, y, V, J have layout [N][nrhs] with the RHS index fastest.
+ *   - "device" pointers are CUDA device pointers on the device that was
+ *     current when the plan was created; "host" pointers are ordinary host
+ *     memory (pinned or pageable).
+ *   - The caller owns every buffer it passes.  The library never frees them
+ *     and keeps no pointer to them after the call returns.  The plan owns all
+ *     device memory it allocates until aim_plan_destroy().
+ *   - Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
+ *     default stream).  Stream-ordered entry points are asynchronous.
+ *   - Every function returns an aim_status.  On a negative status a
+ *     thread-local message is available from aim_last_error(); outputs are
+ *     unspecified.  AIM_NOT_CONVERGED (=1) is a flag, not an error.
+ *   - No entry point falls back to a CPU implementation: if the CUDA device
+ *     or a kernel launch fails the call returns AIM_E_CUDA.
+ */
+#ifndef AIM_H
+#define AIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aim_plan aim_plan; /* opaque */
+
+typedef enum aim_status {
+    AIM_OK = 0,
+    AIM_NOT_CONVERGED = 1, /* aim_gmres: tolerance not reached in max_iters   */
+    AIM_E_ARG = -1,        /* bad scalar argument / NULL pointer / nrhs < 1    */
+    AIM_E_MESH = -2,       /* mesh topology error                 */
+    AIM_E_GRID = -3,       /* grid or index space exceeds 32-bit addressing    */
+    AIM_E_NOMEM = -4,      /* device allocation failed                         */
+    AIM_E_CUDA = -5,       /* CUDA runtime / launch error                      */
+    AIM_E_NCCL = -6        /* reserved for the slab-decomposed multi-GPU path  */
+} aim_status;
+
+enum { AIM_C128 = 0, AIM_C64 = 1 };
+
+typedef struct aim_info {
+    int64_t n_rwg;          /* N                                                */
+    int64_t n_tri;
+    int32_t M;              /* stencil order (BASELINE.json's "order M")        */
+    int32_t S;              /* (M+1)^3 nodes per stencil                        */
+    int32_t grid_origin[3]; /* lattice index of grid node (0,0,0)  (D4)         */
+    int32_t grid_dims[3];   /* Nx, Ny, Nz (unpadded grid)                       */
+    int32_t fft_dims[3];    /* Px, Py, Pz >= 2 Na - 1 (D11)                     */
+    int64_t n_nodes;        /* Nx Ny Nz                                         */
+    int64_t nnz_proj;       /* N S projection entries                           */
+    int64_t nnz_near;       /* near-field (precorrected) entries                */
+    double k, h, near_radius;
+    int64_t device_bytes;   /* device memory owned by the plan (workspaces incl.) */
+    double plan_seconds;    /* wall time of aim_plan_create                     */
+} aim_info;
+
+/*
+ * aim_plan_create -- build the AIM operator for a closed triangle mesh.
+ *
+ * vertices   host  float64 [nv][3]   vertex coordinates (lambda = 1 units)
+ * triangles  host  int32   [nt][3]   vertex indices
+ * rwg_edges  host  int32   [N][4]    {va, vb, t_plus, t_minus}: the RWG on the
+ *            edge (va, vb) shared by triangles t_plus and t_minus; current
+ *            flows from t_plus into t_minus:
+ *              Lambda = l/(2A+) (r - p+) on t+,  l/(2A-) (p- - r) on t-
+ *            ("RWG basis function").
+ * k          wavenumber > 0 (k = 2 pi for lambda = 1)
+ * h          AIM grid spacing > 0 (lattice h Z^3 anchored at the origin, D4)
+ * M          stencil order in [1, 6] ("N_O")
+ * near_radius  >= 0; pairs with ||c_m - c_n|| <= near_radius (1 + 1e-9) are
+ *            treated exactly (D5)
+ * precision  AIM_C128 (AIM_C64 is reserved; returns AIM_E_ARG in this build)
+ * dist       must be NULL (single-GPU plan); multi-GPU runs shard RHS across
+ *            independent plans, see DESIGN.md "Multi-GPU"
+ * out        receives the plan
+ *
+ * Errors: AIM_E_ARG (k <= 0, h <= 0, M outside [1,6], near_radius < 0,
+ * NULL pointers, N < 1), AIM_E_MESH (index out of range, t+ == t-, triangle
+ * not containing va and vb, zero-area triangle), AIM_E_GRID (padded grid
+ * > 2^31 points or nnz > 2^31 - 1), AIM_E_NOMEM, AIM_E_CUDA.
+ * Synchronous.  Uses the current CUDA device.
+ */
+int aim_plan_create(const double* vertices, int64_t nv,
+                    const int32_t* triangles, int64_t nt,
+                    const int32_t* rwg_edges, int64_t n_rwg,
+                    double k, double h, int32_t M, double near_radius,
+                    int32_t precision, const void* dist, aim_plan** out);
+
+/* Release every device buffer of the plan.  NULL is accepted. */
+int aim_plan_destroy(aim_plan* plan);
+
+/* Fill *info.  Host call, no device work. */
+int aim_plan_info(const aim_plan* plan, aim_info* info);
+
+/*
+ * aim_matvec -- y := Z_eq x for nrhs right-hand sides (PAPER.md:539-559,
+ * steps (i)-(iii) plus the precorrected near field).
+ * x, y: device complex128 [N][nrhs], must not overlap.  nrhs >= 1.
+ * Stream-ordered on `stream`; workspaces for this nrhs are allocated on the
+ * first call (synchronously) and reused afterwards.
+ */
+int aim_matvec(aim_plan* plan, const void* x, void* y, int32_t nrhs, void* stream);
+
+/*
+ * aim_matvec_host -- the same product with HOST buffers: copies x to the
+ * device, runs aim_matvec, copies y back, and synchronises (end-to-end path).
+ */
+int aim_matvec_host(aim_plan* plan, const void* x_host, void* y_host, int32_t nrhs);
+
+/*
+ * aim_gmres -- solve Z_eq J = V by restarted GMRES(restart) from J0 = 0
+ * (reading D15: CGS2 Arnoldi, complex Givens rotations,
+ * stop when ||V - Z J|| / ||V|| <= tol, the true residual being recomputed
+ * at the end of each cycle).
+ * V, J: device complex128 [N].  max_iters <= 0 means 20000.
+ * fixed_iters > 0 runs exactly that many inner iterations and returns the
+ * iterate (parity protocol "at equal iteration counts"); 0 = off.
+ * iters, rel_res: host outputs (may be NULL).  Synchronous.
+ * Returns AIM_OK, or AIM_NOT_CONVERGED with J = the last iterate.
+ */
+int aim_gmres(aim_plan* plan, const void* V, void* J, int32_t restart, double tol,
+              int32_t max_iters, int32_t fixed_iters, int32_t* iters, double* rel_res);
+
+/*
+ * aim_planewave_rhs -- V_m = <Lambda_m, E_inc>, E_inc(r) = E0 pol exp(-j k khat.r)
+ * (PAPER.md:455-459 with the sign convention of D1; D14), 7-point rule.
+ * khat, pol: host float64[3]; V: device complex128 [N].  Stream-ordered.
+ */
+int aim_planewave_rhs(aim_plan* plan, const double* khat, const double* pol,
+                      double E0_re, double E0_im, void* V, void* stream);
+
+/* ---- stage entry points (composition and per-stage parity) -------------- */
+/* Grid arrays have layout [4][Nx][Ny][Nz][nrhs], components (x, y, z, phi). */
+
+/* Q := P x   (step (i)).  x device [N][nrhs]. */
+int aim_project(aim_plan* plan, const void* x, void* Q, int32_t nrhs, void* stream);
+
+/* Phi := H Q (step (ii)), zero-padded FFT convolution.  Q is not modified;
+ * Q and Phi may alias. */
+int aim_convolve(aim_plan* plan, const void* Q, void* Phi, int32_t nrhs, void* stream);
+
+/* y := j k eta0 [sum_xyz P^T Phi - k^-2 P_phi^T Phi_phi] (step (iii))
+ *      + (add_near ? Z_corr x : 0).   With Phi == NULL only the near part. */
+int aim_interpolate(aim_plan* plan, const void* Phi, const void* x, void* y,
+                    int32_t nrhs, int32_t add_near, void* stream);
+
+/* ---- plan export (host copies, for parity tests) ------------------------ */
+enum {
+    AIM_EXPORT_BASES = 0,      /* int32   [N][3]   absolute stencil base s_n     */
+    AIM_EXPORT_WEIGHTS = 1,    /* float64 [N][S][4] projection weights          */
+    AIM_EXPORT_NEAR_ROWPTR = 2,/* int64   [N+1]                                 */
+    AIM_EXPORT_NEAR_COL = 3,   /* int32   [nnz_near] (ascending within a row)   */
+    AIM_EXPORT_NEAR_VAL = 4,   /* complex128 [nnz_near] Z_corr                  */
+    AIM_EXPORT_GREEN = 5,      /* complex128 [(Px/2+1)(Py/2+1)(Pz/2+1)] spectrum */
+    AIM_EXPORT_PROJ_ROWPTR = 6,/* int32   [Nx Ny Nz + 1]                        */
+    AIM_EXPORT_PROJ_ENT = 7    /* int32   [N S] entries n*S + u                  */
+};
+/* Copy table `what` into host memory `dst` of `bytes` bytes (must be exact). */
+int aim_plan_export(const aim_plan* plan, int32_t what, void* dst, int64_t bytes);
+
+/* ---- live stage timing (bench accounting) ------------------------------- */
+/* Stage ids of one aim_matvec, in launch order. */
+enum {
+    AIM_STAGE_PROJECT = 0,   /* H1 projection gather                         */
+    AIM_STAGE_FFT_X = 1,     /* H2 x forward pass (zero-pad fused)           */
+    AIM_STAGE_FFT_Y = 2,     /* H2 y forward pass (zero-pad fused)           */
+    AIM_STAGE_FFT_Z = 3,     /* H2-H4 z turnaround: fwd, x spectrum, inv     */
+    AIM_STAGE_IFFT_Y = 4,    /* H4 y inverse pass (pruned)                   */
+    AIM_STAGE_IFFT_X = 5,    /* H4 x inverse pass (pruned)                   */
+    AIM_STAGE_INTERP_NEAR = 6, /* H5+H6 interpolation + near SpMV            */
+    AIM_NUM_STAGES = 7
+};
+/* enable != 0: every subsequent aim_matvec records CUDA events around each
+ * stage on its stream; enable == 0 stops and discards.  Host call. */
+int aim_profile(aim_plan* plan, int32_t enable);
+/* Synchronise on the recorded events and write the summed milliseconds per
+ * stage into ms[AIM_NUM_STAGES] and the number of profiled matvecs into *count;
+ * resets the accumulators. */
+int aim_profile_read(aim_plan* plan, double* ms, int64_t* count);
+
+/* Thread-local message for the last non-OK status ("" if none). */
+const char* aim_last_error(void);
+
+/* Number of kernel launches issued by this thread since the last reset
+ * (bench accounting of "gpu_launches"). */
+int64_t aim_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AIM_H */

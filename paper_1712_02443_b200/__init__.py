@@ -1,0 +1,7 @@
+"""B200-native AIM-accelerated EFIE matvec + GMRES (arXiv 1712.02443, §V).
+
+Thin Python binding over the C ABI in include/aim.h (libaim_b200.so, built
+in-tree for sm_100a).  PyTorch is used for device memory and streams only;
+every step of the operator runs in the library's CUDA kernels.
+"""
+from .api import AimPlan, AimError, launch_count, EXPORT  # noqa: F401

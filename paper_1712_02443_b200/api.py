@@ -1,0 +1,194 @@
+"""Python binding with the C-ABI names (argument marshalling only).
+
+Tensors passed in must be contiguous complex128 CUDA tensors on the plan's
+device; results are allocated with torch.  The current torch CUDA stream is
+passed to the stream-ordered entry points.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+STATUS = {0: "AIM_OK", 1: "AIM_NOT_CONVERGED", -1: "AIM_E_ARG", -2: "AIM_E_MESH", -3: "AIM_E_GRID",
+          -4: "AIM_E_NOMEM", -5: "AIM_E_CUDA", -6: "AIM_E_NCCL"}
+EXPORT = {"bases": 0, "weights": 1, "near_rowptr": 2, "near_col": 3, "near_val": 4, "green": 5,
+          "proj_rowptr": 6, "proj_ent": 7}
+
+
+class AimError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st):
+    if st < 0:
+        raise AimError(st, _lib.load().aim_last_error().decode())
+    return st
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(_lib.load().aim_launch_count(1 if reset else 0))
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev_ptr(t, n, nrhs):
+    torch = _torch()
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128 and t.is_contiguous()):
+        raise TypeError("expected a contiguous complex128 CUDA tensor")
+    if t.numel() != n * nrhs:
+        raise ValueError(f"expected {n * nrhs} elements, got {t.numel()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class AimPlan:
+    """aim_plan_create(...) wrapper; owns the plan until close()."""
+
+    def __init__(self, vertices, triangles, rwg, k, h, M, near_radius, precision=0):
+        lib = _lib.load()
+        self._v = np.ascontiguousarray(vertices, dtype=np.float64)
+        self._t = np.ascontiguousarray(triangles, dtype=np.int32)
+        self._r = np.ascontiguousarray(rwg, dtype=np.int32)
+        out = ctypes.c_void_p()
+        _check(lib.aim_plan_create(self._v.ctypes.data, self._v.shape[0], self._t.ctypes.data, self._t.shape[0],
+                                   self._r.ctypes.data, self._r.shape[0], float(k), float(h), int(M),
+                                   float(near_radius), int(precision), None, ctypes.byref(out)))
+        self._p = out
+        self.N = int(self._r.shape[0])
+        self.info = self.plan_info()
+
+    @classmethod
+    def from_mesh(cls, mesh, k, h, M, near_radius):
+        return cls(mesh.vertices, mesh.triangles, mesh.rwg, k, h, M, near_radius)
+
+    def close(self):
+        if getattr(self, "_p", None):
+            _lib.load().aim_plan_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def plan_info(self) -> dict:
+        inf = _lib.AimInfo()
+        _check(_lib.load().aim_plan_info(self._p, ctypes.byref(inf)))
+        d = {f: getattr(inf, f) for f, _ in _lib.AimInfo._fields_}
+        for f in ("grid_origin", "grid_dims", "fft_dims"):
+            d[f] = tuple(d[f])
+        return d
+
+    @property
+    def grid_dims(self):
+        return self.info["grid_dims"]
+
+    # ---- hot path
+    def matvec(self, x, y=None):
+        torch = _torch()
+        nrhs = 1 if x.dim() == 1 else x.shape[1]
+        if y is None:
+            y = torch.empty_like(x)
+        _check(_lib.load().aim_matvec(self._p, _dev_ptr(x, self.N, nrhs), _dev_ptr(y, self.N, nrhs), nrhs,
+                                      _stream()))
+        return y
+
+    def matvec_host(self, x: np.ndarray, y: np.ndarray | None = None) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        nrhs = 1 if x.ndim == 1 else x.shape[1]
+        if y is None:
+            y = np.empty_like(x)
+        _check(_lib.load().aim_matvec_host(self._p, x.ctypes.data, y.ctypes.data, nrhs))
+        return y
+
+    def gmres(self, V, restart=50, tol=1e-4, max_iters=0, fixed_iters=0):
+        torch = _torch()
+        J = torch.empty_like(V)
+        it = ctypes.c_int32()
+        rr = ctypes.c_double()
+        torch.cuda.current_stream().synchronize()
+        st = _check(_lib.load().aim_gmres(self._p, _dev_ptr(V, self.N, 1), _dev_ptr(J, self.N, 1), int(restart),
+                                          float(tol), int(max_iters), int(fixed_iters), ctypes.byref(it),
+                                          ctypes.byref(rr)))
+        return J, int(it.value), float(rr.value), STATUS[st]
+
+    def planewave_rhs(self, khat=(0.0, 0.0, -1.0), pol=(1.0, 0.0, 0.0), E0=1.0 + 0j):
+        torch = _torch()
+        V = torch.empty(self.N, dtype=torch.complex128, device="cuda")
+        kh = np.ascontiguousarray(khat, dtype=np.float64)
+        po = np.ascontiguousarray(pol, dtype=np.float64)
+        _check(_lib.load().aim_planewave_rhs(self._p, kh.ctypes.data, po.ctypes.data, float(np.real(E0)),
+                                             float(np.imag(E0)), _dev_ptr(V, self.N, 1), _stream()))
+        return V
+
+    # ---- stages
+    def grid_numel(self, nrhs=1):
+        Nx, Ny, Nz = self.grid_dims
+        return 4 * Nx * Ny * Nz * nrhs
+
+    def project(self, x):
+        torch = _torch()
+        nrhs = 1 if x.dim() == 1 else x.shape[1]
+        Q = torch.empty(self.grid_numel(nrhs), dtype=torch.complex128, device=x.device)
+        _check(_lib.load().aim_project(self._p, _dev_ptr(x, self.N, nrhs), ctypes.c_void_p(Q.data_ptr()), nrhs,
+                                       _stream()))
+        return Q.view(4, *self.grid_dims, nrhs)
+
+    def convolve(self, Q):
+        torch = _torch()
+        nrhs = Q.shape[-1]
+        Phi = torch.empty_like(Q)
+        _check(_lib.load().aim_convolve(self._p, ctypes.c_void_p(Q.data_ptr()), ctypes.c_void_p(Phi.data_ptr()),
+                                        nrhs, _stream()))
+        return Phi
+
+    def interpolate(self, Phi, x=None, add_near=False):
+        torch = _torch()
+        nrhs = Phi.shape[-1] if Phi is not None else (1 if x.dim() == 1 else x.shape[1])
+        y = torch.empty((self.N, nrhs), dtype=torch.complex128, device="cuda")
+        _check(_lib.load().aim_interpolate(self._p, ctypes.c_void_p(Phi.data_ptr()) if Phi is not None else None,
+                                           ctypes.c_void_p(x.data_ptr()) if x is not None else None,
+                                           ctypes.c_void_p(y.data_ptr()), nrhs, 1 if add_near else 0, _stream()))
+        return y
+
+    # ---- live stage timing
+    STAGES = ("project", "fft_x", "fft_y", "fft_z_turn", "ifft_y", "ifft_x", "interp_near")
+
+    def profile(self, enable: bool):
+        _check(_lib.load().aim_profile(self._p, 1 if enable else 0))
+
+    def profile_read(self):
+        ms = (ctypes.c_double * 7)()
+        cnt = ctypes.c_int64()
+        _check(_lib.load().aim_profile_read(self._p, ms, ctypes.byref(cnt)))
+        return dict(zip(self.STAGES, list(ms))), int(cnt.value)
+
+    # ---- export
+    def export(self, what: str) -> np.ndarray:
+        inf = self.info
+        N, S = inf["n_rwg"], inf["S"]
+        Px, Py, Pz = inf["fft_dims"]
+        shapes = {
+            "bases": (np.int32, (N, 3)), "weights": (np.float64, (N, S, 4)),
+            "near_rowptr": (np.int64, (N + 1,)), "near_col": (np.int32, (inf["nnz_near"],)),
+            "near_val": (np.complex128, (inf["nnz_near"],)),
+            "green": (np.complex128, (Px // 2 + 1, Py // 2 + 1, Pz // 2 + 1)),
+            "proj_rowptr": (np.int32, (inf["n_nodes"] + 1,)), "proj_ent": (np.int32, (inf["nnz_proj"],)),
+        }
+        dt, sh = shapes[what]
+        out = np.empty(sh, dtype=dt)
+        _check(_lib.load().aim_plan_export(self._p, EXPORT[what], out.ctypes.data, out.nbytes))
+        return out

@@ -1,0 +1,411 @@
+// C ABI of the AIM library (include/aim.h) and the host part of plan
+// construction (setup steps S0-S1 of SURVEY.md §8(a)):
+//   S0 RWG geometry and the 7-point Radon/Dunavant rule (D7)
+//      on every triangle;
+//   S1 stencil bases s_n = floor(c_n/h - (M-1)/2 + 1e-7) (D3), grid box (D4)
+//      and 7-smooth FFT sizes P_a >= 2 N_a - 1 (D11).
+// Device-side setup (S2-S4) is in k_plan.cu; the per-matvec kernels are in
+// k_matvec.cu / k_fft.cu and GMRES in k_gmres.cu.
+#include <math.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "aim_internal.cuh"
+
+namespace aim {
+
+static thread_local std::string g_err;
+static thread_local long long g_launches = 0;
+
+void note_launch(const char* name) {
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(AIM_E_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+}
+
+static int fail(int status, const std::string& msg) {
+    g_err = msg;
+    return status;
+}
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        g_err.clear();
+        return f();
+    } catch (const Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(AIM_E_NOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(AIM_E_CUDA, e.what());
+    }
+}
+
+// 7-point degree-5 rule (Radon; Dunavant's 7-point rule), D7
+static void dunavant7(double bary[7][3], double w[7]) {
+    const double s15 = sqrt(15.0);
+    const double a1 = (6.0 - s15) / 21.0, a2 = (6.0 + s15) / 21.0;
+    const double w1 = (155.0 - s15) / 1200.0, w2 = (155.0 + s15) / 1200.0;
+    bary[0][0] = bary[0][1] = bary[0][2] = 1.0 / 3.0;
+    w[0] = 9.0 / 40.0;
+    const double as[2] = {a1, a2}, ws[2] = {w1, w2};
+    for (int g = 0; g < 2; ++g) {
+        const double a = as[g], b = 1.0 - 2.0 * a;
+        for (int q = 0; q < 3; ++q) {
+            for (int c = 0; c < 3; ++c) bary[1 + 3 * g + q][c] = (c == q) ? b : a;
+            w[1 + 3 * g + q] = ws[g];
+        }
+    }
+}
+
+template <class T>
+static T* upload(aim_plan* p, const std::vector<T>& h) {
+    T* d = p->alloc<T>(h.size());
+    AIM_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return d;
+}
+
+static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, const int32_t* E, int64_t N, double k,
+                   double h, int M, double r, aim_plan* p) {
+    const auto t0 = std::chrono::steady_clock::now();
+    AIM_CUDA(cudaGetDevice(&p->device));
+    AIM_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->N = N; p->nt = nt; p->nv = nv; p->k = k; p->h = h; p->M = M; p->r = r;
+    p->S = (M + 1) * (M + 1) * (M + 1);
+
+    // ---- S0: triangle geometry + quadrature
+    double bary[7][3], bw[7];
+    dunavant7(bary, bw);
+    std::vector<double> qp(nt * 21), qw(nt * 7), cor(nt * 9), area(nt);
+    std::vector<int32_t> tv(nt * 3);
+    for (int64_t t = 0; t < nt; ++t) {
+        const double* P[3];
+        for (int c = 0; c < 3; ++c) {
+            const int32_t vi = T[3 * t + c];
+            if (vi < 0 || vi >= nv) throw Error(AIM_E_MESH, "triangle vertex index out of range");
+            P[c] = V + 3 * (int64_t)vi;
+            tv[3 * t + c] = vi;
+            for (int d = 0; d < 3; ++d) cor[9 * t + 3 * c + d] = P[c][d];
+        }
+        const double e1[3] = {P[1][0] - P[0][0], P[1][1] - P[0][1], P[1][2] - P[0][2]};
+        const double e2[3] = {P[2][0] - P[0][0], P[2][1] - P[0][1], P[2][2] - P[0][2]};
+        const double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+        area[t] = 0.5 * sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+        if (!(area[t] > 0)) throw Error(AIM_E_MESH, "degenerate triangle " + std::to_string(t));
+        for (int q = 0; q < 7; ++q) {
+            for (int d = 0; d < 3; ++d)
+                qp[21 * t + 3 * q + d] = bary[q][0] * P[0][d] + bary[q][1] * P[1][d] + bary[q][2] * P[2][d];
+            qw[7 * t + q] = bw[q] * area[t];
+        }
+    }
+    // ---- S0: RWG geometry; Lambda = alpha (r - p), alpha = +l/(2A+) on t+, -l/(2A-) on t-
+    std::vector<int32_t> rt(2 * N), base(3 * N), node0(N);
+    std::vector<double> ra(2 * N), rp(6 * N), rc(3 * N);
+    for (int64_t n = 0; n < N; ++n) {
+        const int32_t va = E[4 * n], vb = E[4 * n + 1], tp = E[4 * n + 2], tm = E[4 * n + 3];
+        if (va < 0 || va >= nv || vb < 0 || vb >= nv || va == vb)
+            throw Error(AIM_E_MESH, "rwg edge vertex invalid at row " + std::to_string(n));
+        if (tp < 0 || tp >= nt || tm < 0 || tm >= nt) throw Error(AIM_E_MESH, "rwg triangle index out of range");
+        if (tp == tm) throw Error(AIM_E_MESH, "t+ == t- at row " + std::to_string(n));
+        const double l = sqrt((V[3 * vb] - V[3 * va]) * (V[3 * vb] - V[3 * va]) +
+                              (V[3 * vb + 1] - V[3 * va + 1]) * (V[3 * vb + 1] - V[3 * va + 1]) +
+                              (V[3 * vb + 2] - V[3 * va + 2]) * (V[3 * vb + 2] - V[3 * va + 2]));
+        const int32_t tri[2] = {tp, tm};
+        double cen[3] = {0, 0, 0};
+        for (int side = 0; side < 2; ++side) {
+            const int32_t t = tri[side];
+            int hasa = 0, hasb = 0, fv = -1;
+            for (int c = 0; c < 3; ++c) {
+                const int32_t v = T[3 * t + c];
+                if (v == va) hasa = 1;
+                else if (v == vb) hasb = 1;
+                else fv = v;
+            }
+            if (!hasa || !hasb || fv < 0) throw Error(AIM_E_MESH, "rwg edge not in its triangle at row " + std::to_string(n));
+            rt[2 * n + side] = t;
+            ra[2 * n + side] = (side == 0 ? 1.0 : -1.0) * l / (2.0 * area[t]);
+            for (int d = 0; d < 3; ++d) {
+                rp[6 * n + 3 * side + d] = V[3 * fv + d];
+                cen[d] += (V[3 * T[3 * t] + d] + V[3 * T[3 * t + 1] + d] + V[3 * T[3 * t + 2] + d]) / 3.0;
+            }
+        }
+        for (int d = 0; d < 3; ++d) rc[3 * n + d] = 0.5 * cen[d];
+    }
+    // ---- S1: stencils (D3) and grid box (D4)
+    long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX}, hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+    for (int64_t n = 0; n < N; ++n)
+        for (int d = 0; d < 3; ++d) {
+            const double s = floor(rc[3 * n + d] / h - (M - 1) / 2.0 + 1e-7);
+            if (!(fabs(s) < 1e9)) throw Error(AIM_E_GRID, "stencil index exceeds addressable grid");
+            const long long si = (long long)s;
+            base[3 * n + d] = (int32_t)si;
+            lo[d] = std::min(lo[d], si);
+            hi[d] = std::max(hi[d], si);
+        }
+    long long ng = 1, npad = 1;
+    for (int d = 0; d < 3; ++d) {
+        const long long nd = hi[d] + M + 1 - lo[d];
+        if (nd > (1 << 20)) throw Error(AIM_E_GRID, "grid extent exceeds addressable grid");
+        p->origin[d] = (int)lo[d];
+        p->dims[d] = (int)nd;
+        p->pads[d] = smooth_size_at_least((int)(2 * nd - 1));
+        ng *= nd;
+        npad *= p->pads[d];
+    }
+    if (npad > 2147483647LL || ng > 2147483647LL) throw Error(AIM_E_GRID, "padded grid exceeds 2^31 points");
+    if ((long long)N * p->S > 2147483647LL) throw Error(AIM_E_GRID, "projection nnz exceeds 2^31-1");
+    p->Ng = ng;
+    for (int64_t n = 0; n < N; ++n)
+        node0[n] = (int32_t)(((long long)(base[3 * n] - lo[0]) * p->dims[1] + (base[3 * n + 1] - lo[1])) * p->dims[2] +
+                             (base[3 * n + 2] - lo[2]));
+
+    // ---- uploads
+    p->tri_qp = upload(p, qp);
+    p->tri_qw = upload(p, qw);
+    p->tri_cor = upload(p, cor);
+    p->tri_v = upload(p, tv);
+    p->rwg_t = upload(p, rt);
+    p->rwg_a = upload(p, ra);
+    p->rwg_p = upload(p, rp);
+    p->rwg_c = upload(p, rc);
+    p->base = upload(p, base);
+    p->node0 = upload(p, node0);
+    for (int d = 0; d < 3; ++d) make_fft_axis(p->pads[d], p->ax[d]);
+
+    // ---- device setup S2-S4
+    cudaStream_t s = p->stream;
+    build_weights(p, s);
+    build_projection_csr(p, node0, s);
+    build_green_spectrum(p, s);
+    build_near_list(p, s);
+    build_near_values(p, s);
+    AIM_CUDA(cudaStreamSynchronize(s));
+    p->plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+static void destroy(aim_plan* p) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();
+    for (auto& a : p->allocs) cudaFree(a.first);
+    for (int d = 0; d < 3; ++d)
+        if (p->ax[d].tw) cudaFree(p->ax[d].tw);
+    for (auto e : p->ev_pool) cudaEventDestroy(e);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    cudaSetDevice(cur);
+    delete p;
+}
+
+}  // namespace aim
+
+using namespace aim;
+
+extern "C" {
+
+int aim_plan_create(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt,
+                    const int32_t* rwg_edges, int64_t n_rwg, double k, double h, int32_t M, double near_radius,
+                    int32_t precision, const void* dist, aim_plan** out) {
+    if (!out) return fail(AIM_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!vertices || !triangles || !rwg_edges) return fail(AIM_E_ARG, "NULL mesh pointer");
+    if (nv < 3 || nt < 2 || n_rwg < 1) return fail(AIM_E_ARG, "empty mesh");
+    if (!(k > 0) || !(h > 0) || M < 1 || M > 6 || !(near_radius >= 0))
+        return fail(AIM_E_ARG, "k, h > 0, M in [1,6], near_radius >= 0 required");
+    if (precision != AIM_C128) return fail(AIM_E_ARG, "only AIM_C128 is implemented");
+    if (dist) return fail(AIM_E_ARG, "dist must be NULL (single-GPU plan)");
+    aim_plan* p = new aim_plan();
+    const int st = guarded([&] {
+        create(vertices, nv, triangles, nt, rwg_edges, n_rwg, k, h, M, near_radius, p);
+        return AIM_OK;
+    });
+    if (st != AIM_OK) {
+        const std::string msg = g_err;
+        destroy(p);
+        g_err = msg;
+        return st;
+    }
+    *out = p;
+    return AIM_OK;
+}
+
+int aim_plan_destroy(aim_plan* plan) {
+    return guarded([&] {
+        destroy(plan);
+        return AIM_OK;
+    });
+}
+
+int aim_plan_info(const aim_plan* p, aim_info* info) {
+    if (!p || !info) return fail(AIM_E_ARG, "NULL argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n_rwg = p->N;
+    info->n_tri = p->nt;
+    info->M = p->M;
+    info->S = p->S;
+    for (int d = 0; d < 3; ++d) {
+        info->grid_origin[d] = p->origin[d];
+        info->grid_dims[d] = p->dims[d];
+        info->fft_dims[d] = p->pads[d];
+    }
+    info->n_nodes = p->Ng;
+    info->nnz_proj = p->nnzP;
+    info->nnz_near = p->nnzN;
+    info->k = p->k;
+    info->h = p->h;
+    info->near_radius = p->r;
+    info->device_bytes = p->device_bytes;
+    info->plan_seconds = p->plan_seconds;
+    return AIM_OK;
+}
+
+int aim_matvec(aim_plan* p, const void* x, void* y, int32_t nrhs, void* stream) {
+    if (!p || !x || !y || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
+    if (x == y) return fail(AIM_E_ARG, "x and y must not overlap");
+    return guarded([&] {
+        matvec(p, (const double2*)x, (double2*)y, nrhs, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_matvec_host(aim_plan* p, const void* xh, void* yh, int32_t nrhs) {
+    if (!p || !xh || !yh || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        const size_t bytes = sizeof(double2) * (size_t)p->N * nrhs;
+        if (p->hs_nrhs < nrhs) {
+            p->release(p->hx);
+            p->release(p->hy);
+            p->hx = p->alloc<double2>((size_t)p->N * nrhs);
+            p->hy = p->alloc<double2>((size_t)p->N * nrhs);
+            p->hs_nrhs = nrhs;
+        }
+        cudaStream_t s = p->stream;
+        AIM_CUDA(cudaMemcpyAsync(p->hx, xh, bytes, cudaMemcpyHostToDevice, s));
+        matvec(p, p->hx, p->hy, nrhs, s);
+        AIM_CUDA(cudaMemcpyAsync(yh, p->hy, bytes, cudaMemcpyDeviceToHost, s));
+        AIM_CUDA(cudaStreamSynchronize(s));
+        return AIM_OK;
+    });
+}
+
+int aim_gmres(aim_plan* p, const void* V, void* J, int32_t restart, double tol, int32_t max_iters,
+              int32_t fixed_iters, int32_t* iters, double* rel_res) {
+    if (!p || !V || !J || restart < 1 || !(tol >= 0)) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        int it = 0;
+        double rr = 0;
+        const int st = gmres(p, (const double2*)V, (double2*)J, restart, tol, max_iters, fixed_iters, &it, &rr);
+        if (iters) *iters = it;
+        if (rel_res) *rel_res = rr;
+        return st;
+    });
+}
+
+int aim_planewave_rhs(aim_plan* p, const double* khat, const double* pol, double E0_re, double E0_im, void* V,
+                      void* stream) {
+    if (!p || !khat || !pol || !V) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        launch_planewave(p, khat, pol, make_double2(E0_re, E0_im), (double2*)V, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_project(aim_plan* p, const void* x, void* Q, int32_t nrhs, void* stream) {
+    if (!p || !x || !Q || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        launch_project(p, (const double2*)x, (double2*)Q, nrhs, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_convolve(aim_plan* p, const void* Q, void* Phi, int32_t nrhs, void* stream) {
+    if (!p || !Q || !Phi || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        ensure_workspace(p, nrhs);
+        convolve(p, (const double2*)Q, (double2*)Phi, nrhs, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_interpolate(aim_plan* p, const void* Phi, const void* x, void* y, int32_t nrhs, int32_t add_near,
+                    void* stream) {
+    if (!p || !y || nrhs < 1 || (add_near && !x) || (!Phi && !add_near)) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        launch_interp_near(p, (const double2*)Phi, (const double2*)x, (double2*)y, nrhs, Phi != nullptr,
+                           add_near != 0, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_plan_export(const aim_plan* p, int32_t what, void* dst, int64_t bytes) {
+    if (!p || !dst) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        const void* src = nullptr;
+        int64_t need = 0;
+        switch (what) {
+            case AIM_EXPORT_BASES: src = p->base; need = 12 * p->N; break;
+            case AIM_EXPORT_WEIGHTS: src = p->W; need = 32 * p->N * p->S; break;
+            case AIM_EXPORT_NEAR_ROWPTR: src = p->nrow; need = 8 * (p->N + 1); break;
+            case AIM_EXPORT_NEAR_COL: src = p->ncol; need = 4 * p->nnzN; break;
+            case AIM_EXPORT_NEAR_VAL: src = p->nval; need = 16 * p->nnzN; break;
+            case AIM_EXPORT_GREEN:
+                src = p->spec;
+                need = 16LL * (p->pads[0] / 2 + 1) * (p->pads[1] / 2 + 1) * (p->pads[2] / 2 + 1);
+                break;
+            case AIM_EXPORT_PROJ_ROWPTR: src = p->prow; need = 4 * (p->Ng + 1); break;
+            case AIM_EXPORT_PROJ_ENT: src = p->pent; need = 4 * p->nnzP; break;
+            default: throw Error(AIM_E_ARG, "unknown export id");
+        }
+        if (need != bytes) throw Error(AIM_E_ARG, "export size mismatch: need " + std::to_string(need));
+        AIM_CUDA(cudaDeviceSynchronize());
+        if (need) AIM_CUDA(cudaMemcpy(dst, src, need, cudaMemcpyDeviceToHost));
+        return AIM_OK;
+    });
+}
+
+int aim_profile(aim_plan* p, int32_t enable) {
+    if (!p) return fail(AIM_E_ARG, "NULL plan");
+    return guarded([&] {
+        p->prof = enable ? 1 : 0;
+        p->ev_used = 0;
+        p->prof_count = 0;
+        return AIM_OK;
+    });
+}
+
+int aim_profile_read(aim_plan* p, double* ms, int64_t* count) {
+    if (!p || !ms || !count) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        for (int i = 0; i < AIM_NUM_STAGES; ++i) ms[i] = 0.0;
+        const size_t per = AIM_NUM_STAGES + 1;
+        if (p->ev_used % per) throw Error(AIM_E_ARG, "profiling events out of step");
+        if (p->ev_used) AIM_CUDA(cudaEventSynchronize(p->ev_pool[p->ev_used - 1]));
+        for (size_t b = 0; b < p->ev_used; b += per)
+            for (int i = 0; i < AIM_NUM_STAGES; ++i) {
+                float t = 0.f;
+                AIM_CUDA(cudaEventElapsedTime(&t, p->ev_pool[b + i], p->ev_pool[b + i + 1]));
+                ms[i] += t;
+            }
+        *count = p->prof_count;
+        p->ev_used = 0;
+        p->prof_count = 0;
+        return AIM_OK;
+    });
+}
+
+const char* aim_last_error(void) { return g_err.c_str(); }
+
+int64_t aim_launch_count(int32_t reset) {
+    const long long v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+
+}  // extern "C"

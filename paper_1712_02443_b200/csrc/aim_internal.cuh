@@ -1,0 +1,179 @@
+// Internal declarations of the AIM library (plan layout, launch helpers).
+// See include/aim.h for the public contract and DESIGN.md for the design.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/aim.h"
+
+namespace aim {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define AIM_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            throw ::aim::Error(e_ == cudaErrorMemoryAllocation ? AIM_E_NOMEM : AIM_E_CUDA, \
+                               std::string(#call) + ": " + cudaGetErrorString(e_));      \
+        }                                                                               \
+    } while (0)
+
+void note_launch(const char* name);  // counts launches, checks launch errors
+
+// eta0 = mu0 c with mu0 = 4 pi 1e-7 (reading D1; one fixed value).
+constexpr double kPi = 3.14159265358979323846;
+inline double eta0() { return 4.0e-7 * kPi * 299792458.0; }
+
+// ------------------------------------------------------------ FFT pass plan
+constexpr int kMaxStages = 12;
+
+struct FftAxis {
+    int P = 1;                       // transform length
+    int nst = 0;                     // number of Stockham stages
+    int radix[kMaxStages] = {0};     // radices, product == P
+    double2* tw = nullptr;           // device twiddles exp(-2 pi i e / P), e in [0,P)
+};
+
+// One batched 1-D pass over a tensor viewed as [outer][L][inner].
+struct FftPass {
+    const double2* in;
+    double2* out;
+    long long outer;     // number of outer slices
+    int Lin;             // input length along the axis (zero-padded to P)
+    int Lout;            // output length along the axis (pruned from P)
+    long long inner;     // element stride of the axis
+    int TO, TI;          // tile: TO outer x TI inner lines per CTA
+    int mode;            // 0 forward, 1 inverse, 2 turnaround (fwd, x spectrum, inv)
+    FftAxis ax;
+    // turnaround only: spectrum octant and the (kx, ky) decoding of `outer`
+    const double2* spec;
+    int Px, Py;          // outer = (c Px + kx) Py + ky
+    int PyH, PzH;        // octant extents Py/2+1, Pz/2+1
+};
+
+void launch_fft_pass(const FftPass& p, cudaStream_t s);
+void make_fft_axis(int P, FftAxis& ax);    // factorisation + device twiddles
+int smooth_size_at_least(int n);           // smallest 2^a 3^b 5^c 7^d >= n
+
+// -------------------------------------------------------------------- plan
+}  // namespace aim
+
+struct aim_plan {
+    int device = 0;
+    int64_t N = 0, nt = 0, nv = 0;
+    double k = 0, h = 0, r = 0;
+    int M = 0, S = 0;
+    int origin[3] = {0, 0, 0};
+    int dims[3] = {0, 0, 0};     // Nx Ny Nz
+    int pads[3] = {0, 0, 0};     // Px Py Pz
+    int64_t Ng = 0;
+    int64_t nnzP = 0, nnzN = 0;
+    double plan_seconds = 0;
+
+    // geometry (device)
+    double* tri_qp = nullptr;     // [nt][7][3]
+    double* tri_qw = nullptr;     // [nt][7]   weight x area
+    double* tri_cor = nullptr;    // [nt][3][3]
+    int32_t* tri_v = nullptr;     // [nt][3]
+    int32_t* rwg_t = nullptr;     // [N][2]   t+, t-
+    double* rwg_a = nullptr;      // [N][2]   alpha = +-l/(2A)
+    double* rwg_p = nullptr;      // [N][2][3] free vertices
+    double* rwg_c = nullptr;      // [N][3]   centre
+    int32_t* base = nullptr;      // [N][3]   absolute stencil base
+    int32_t* node0 = nullptr;     // [N]      grid index of the base node
+
+    // operator tables (device)
+    double* W = nullptr;          // [N][S][4] weights (x, y, z, phi)
+    int32_t* prow = nullptr;      // [Ng+1]
+    int32_t* pent = nullptr;      // [nnzP]  n*S + u
+    int64_t* nrow = nullptr;      // [N+1]
+    int32_t* ncol = nullptr;      // [nnzN]
+    double2* nval = nullptr;      // [nnzN]
+    double2* spec = nullptr;      // [(Px/2+1)(Py/2+1)(Pz/2+1)]
+    aim::FftAxis ax[3];
+
+    // workspaces (device), sized for ws_nrhs
+    int ws_nrhs = 0;
+    double2* Q = nullptr;         // [4][Nx][Ny][Nz][R]   (also Phi)
+    double2* W1 = nullptr;        // [4][Px][Ny][Nz][R]
+    double2* W2 = nullptr;        // [4][Px][Py][Nz][R]
+    // GMRES workspace
+    int gm_restart = 0;
+    double2* gm_V = nullptr;      // [(restart+1)][N]
+    double2* gm_w = nullptr;      // [N]
+    double2* gm_part = nullptr;   // partial sums
+    // host staging for aim_matvec_host
+    int hs_nrhs = 0;
+    double2* hx = nullptr;
+    double2* hy = nullptr;
+
+    // live stage timing (aim_profile): 8 events per profiled matvec
+    int prof = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    int64_t prof_count = 0;
+
+    int64_t device_bytes = 0;
+    std::vector<std::pair<void*, size_t>> allocs;
+    cudaStream_t stream = nullptr;  // plan-private stream for synchronous calls
+
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        if (count == 0) count = 1;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess)
+            throw aim::Error(AIM_E_NOMEM, std::string("cudaMalloc ") + std::to_string(count * sizeof(T)) +
+                                              " bytes: " + cudaGetErrorString(e));
+        allocs.emplace_back(p, count * sizeof(T));
+        device_bytes += (int64_t)(count * sizeof(T));
+        return (T*)p;
+    }
+    void release(void* p) {
+        if (!p) return;
+        for (size_t i = 0; i < allocs.size(); ++i)
+            if (allocs[i].first == p) {
+                device_bytes -= (int64_t)allocs[i].second;
+                allocs.erase(allocs.begin() + i);
+                break;
+            }
+        cudaFree(p);
+    }
+};
+
+namespace aim {
+
+// ---- plan-building launches (k_plan.cu)
+void build_weights(aim_plan* p, cudaStream_t s);
+void build_projection_csr(aim_plan* p, const std::vector<int32_t>& node0_host, cudaStream_t s);
+void build_near_list(aim_plan* p, cudaStream_t s);
+void build_near_values(aim_plan* p, cudaStream_t s);
+void build_green_spectrum(aim_plan* p, cudaStream_t s);
+
+// ---- matvec launches (k_matvec.cu)
+void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s);
+void launch_interp_near(const aim_plan* p, const double2* Phi, const double2* x, double2* y, int R,
+                        bool far, bool near, cudaStream_t s);
+void launch_planewave(const aim_plan* p, const double* khat, const double* pol, double2 E0, double2* V,
+                      cudaStream_t s);
+void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s);
+void ensure_workspace(aim_plan* p, int R);
+void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
+void prof_mark(aim_plan* p, cudaStream_t s);  // records a stage-boundary event when profiling
+
+// ---- GMRES (k_gmres.cu)
+int gmres(aim_plan* p, const double2* V, double2* J, int restart, double tol, int max_iters, int fixed_iters,
+          int* iters, double* rel_res);
+
+}  // namespace aim

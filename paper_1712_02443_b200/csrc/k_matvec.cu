@@ -1,0 +1,279 @@
+// Per-matvec kernels of y = Z_eq x:
+//   H1 projection  Q^psi[u,r] = sum_{n in col(u)} w^psi_{n,u} x[n,r]
+//      deterministic gather over the grid-node-sorted CSR, warp per node,
+//      lanes over (entry group, rhs), fixed-order shuffle reduction;
+//   H2-H4 convolution Phi = H Q by five Stockham passes (k_fft.cu):
+//      x fwd (pad) -> y fwd (pad) -> z turnaround (pad, x G^, prune) ->
+//      y inv (prune) -> x inv (prune)
+//   H5+H6 interpolation y = j k eta0 [sum_xyz P^T Phi - k^-2 P_phi^T Phi_phi]
+//       fused with the precorrected near-field SpMV
+//      y += Z_corr x: warp per RWG row, one y write.
+#include <math.h>
+
+#include <algorithm>
+
+#include "aim_internal.cuh"
+
+namespace aim {
+
+static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
+    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+// ------------------------------------------------------------ H1 projection
+template <int M, int RC>
+__global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict__ prow,
+                                                      const int32_t* __restrict__ pent,
+                                                      const double* __restrict__ W, const double2* __restrict__ x,
+                                                      long long Ng, int R, double2* __restrict__ Q) {
+    constexpr int S = (M + 1) * (M + 1) * (M + 1);
+    constexpr int G = 32 / RC;
+    const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (g >= Ng) return;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / RC, r = lane % RC;
+    const int e0 = prow[g], e1 = prow[g + 1];
+    for (int r0 = 0; r0 < R; r0 += RC) {
+        const int rr = r0 + r;
+        const bool act = rr < R;
+        double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
+        for (int e = e0 + grp; e < e1; e += G) {
+            const int ent = __ldg(&pent[e]);
+            const int n = ent / S;
+            const double2 w01 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (long long)ent);
+            const double2 w23 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (long long)ent + 1);
+            const double2 xv = act ? __ldg(&x[(long long)n * R + rr]) : make_double2(0, 0);
+            a0.x = fma(w01.x, xv.x, a0.x); a0.y = fma(w01.x, xv.y, a0.y);
+            a1.x = fma(w01.y, xv.x, a1.x); a1.y = fma(w01.y, xv.y, a1.y);
+            a2.x = fma(w23.x, xv.x, a2.x); a2.y = fma(w23.x, xv.y, a2.y);
+            a3.x = fma(w23.y, xv.x, a3.x); a3.y = fma(w23.y, xv.y, a3.y);
+        }
+#pragma unroll
+        for (int off = RC; off < 32; off <<= 1) {
+            double2 t;
+            t = shfl_xor2(a0, off); a0.x += t.x; a0.y += t.y;
+            t = shfl_xor2(a1, off); a1.x += t.x; a1.y += t.y;
+            t = shfl_xor2(a2, off); a2.x += t.x; a2.y += t.y;
+            t = shfl_xor2(a3, off); a3.x += t.x; a3.y += t.y;
+        }
+        if (RC == 1) {
+            if (lane < 4) {
+                const double2 v = lane == 0 ? a0 : lane == 1 ? a1 : lane == 2 ? a2 : a3;
+                Q[((long long)lane * Ng + g) * R + rr] = v;
+            }
+        } else if (grp == 0 && act) {
+            Q[(0 * Ng + g) * R + rr] = a0;
+            Q[(1 * Ng + g) * R + rr] = a1;
+            Q[(2 * Ng + g) * R + rr] = a2;
+            Q[(3 * Ng + g) * R + rr] = a3;
+        }
+    }
+}
+
+static int rhs_chunk(int R) {
+    int rc = 1;
+    while (rc < R && rc < 32) rc <<= 1;
+    return rc;
+}
+
+void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s) {
+    const int rc = rhs_chunk(R);
+    const unsigned grid = nblk(p->Ng * 32, 256);
+#define PJ(MM, RR) \
+    if (p->M == MM && rc == RR) { project_kernel<MM, RR><<<grid, 256, 0, s>>>(p->prow, p->pent, p->W, x, p->Ng, R, Q); note_launch("project"); return; }
+#define PJM(MM) PJ(MM, 1) PJ(MM, 2) PJ(MM, 4) PJ(MM, 8) PJ(MM, 16) PJ(MM, 32)
+    PJM(1) PJM(2) PJM(3) PJM(4) PJM(5) PJM(6)
+#undef PJM
+#undef PJ
+    throw Error(AIM_E_ARG, "unsupported M");
+}
+
+// ------------------------------------------------ H5 + H6 interp + near
+template <int M, int RC>
+__global__ void __launch_bounds__(256) interp_near_kernel(const double2* __restrict__ Phi,
+                                                          const double* __restrict__ W,
+                                                          const int32_t* __restrict__ node0, long long Ng, int Ny,
+                                                          int Nz, const int64_t* __restrict__ rowp,
+                                                          const int32_t* __restrict__ col,
+                                                          const double2* __restrict__ val,
+                                                          const double2* __restrict__ x, long long N, int R,
+                                                          double keta, double ik2, int do_far, int do_near,
+                                                          double2* __restrict__ y) {
+    constexpr int M1 = M + 1, S = M1 * M1 * M1;
+    constexpr int G = 32 / RC;
+    const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (m >= N) return;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / RC, r = lane % RC;
+    const long long g0 = do_far ? node0[m] : 0;
+    const long long e0 = rowp[m], e1 = rowp[m + 1];
+    for (int r0 = 0; r0 < R; r0 += RC) {
+        const int rr = r0 + r;
+        const bool act = rr < R;
+        double2 aA = make_double2(0, 0), aP = aA, aN = aA;
+        if (do_far) {
+            for (int u = grp; u < S; u += G) {
+                const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
+                const long long g = g0 + ((long long)ui * Ny + uj) * Nz + uk;
+                const double2 w01 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u));
+                const double2 w23 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u) + 1);
+                if (act) {
+                    const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
+                    const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
+                    const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
+                    const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
+                    aA.x = fma(w01.x, f0.x, aA.x); aA.y = fma(w01.x, f0.y, aA.y);
+                    aA.x = fma(w01.y, f1.x, aA.x); aA.y = fma(w01.y, f1.y, aA.y);
+                    aA.x = fma(w23.x, f2.x, aA.x); aA.y = fma(w23.x, f2.y, aA.y);
+                    aP.x = fma(w23.y, f3.x, aP.x); aP.y = fma(w23.y, f3.y, aP.y);
+                }
+            }
+        }
+        if (do_near) {
+            for (long long e = e0 + grp; e < e1; e += G) {
+                const double2 z = __ldg(&val[e]);
+                const int n = __ldg(&col[e]);
+                if (act) {
+                    const double2 xv = __ldg(&x[(long long)n * R + rr]);
+                    aN.x = fma(z.x, xv.x, aN.x); aN.x = fma(-z.y, xv.y, aN.x);
+                    aN.y = fma(z.x, xv.y, aN.y); aN.y = fma(z.y, xv.x, aN.y);
+                }
+            }
+        }
+        // far = j k eta0 (aA - aP / k^2)
+        double2 f = make_double2(aA.x - aP.x * ik2, aA.y - aP.y * ik2);
+        double2 tot = make_double2(aN.x - keta * f.y, aN.y + keta * f.x);
+#pragma unroll
+        for (int off = RC; off < 32; off <<= 1) {
+            const double2 t = shfl_xor2(tot, off);
+            tot.x += t.x; tot.y += t.y;
+        }
+        if (grp == 0 && act) y[m * R + rr] = tot;
+    }
+}
+
+void launch_interp_near(const aim_plan* p, const double2* Phi, const double2* x, double2* y, int R, bool far,
+                        bool near, cudaStream_t s) {
+    const int rc = rhs_chunk(R);
+    const unsigned grid = nblk(p->N * 32, 256);
+    const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
+#define IN(MM, RR)                                                                                              \
+    if (p->M == MM && rc == RR) {                                                                               \
+        interp_near_kernel<MM, RR><<<grid, 256, 0, s>>>(Phi, p->W, p->node0, p->Ng, p->dims[1], p->dims[2],     \
+                                                        p->nrow, p->ncol, p->nval, x, p->N, R, keta, ik2, far,  \
+                                                        near, y);                                               \
+        note_launch("interp_near");                                                                             \
+        return;                                                                                                 \
+    }
+#define INM(MM) IN(MM, 1) IN(MM, 2) IN(MM, 4) IN(MM, 8) IN(MM, 16) IN(MM, 32)
+    INM(1) INM(2) INM(3) INM(4) INM(5) INM(6)
+#undef INM
+#undef IN
+    throw Error(AIM_E_ARG, "unsupported M");
+}
+
+// ------------------------------------------------------------ plane wave
+__global__ void planewave_kernel(const double* __restrict__ qp, const double* __restrict__ qw,
+                                 const int32_t* __restrict__ rt, const double* __restrict__ ra,
+                                 const double* __restrict__ rp, long long N, double k, double kx, double ky,
+                                 double kz, double px, double py, double pz, double2 E0, double2* __restrict__ V) {
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    double2 acc = make_double2(0, 0);
+    for (int side = 0; side < 2; ++side) {
+        const int t = rt[2 * n + side];
+        const double a = ra[2 * n + side];
+        const double* p = rp + 6 * n + 3 * side;
+        for (int q = 0; q < 7; ++q) {
+            const double* r = qp + (7 * t + q) * 3;
+            const double lp = a * ((r[0] - p[0]) * px + (r[1] - p[1]) * py + (r[2] - p[2]) * pz);
+            double s, c;
+            sincos(k * (kx * r[0] + ky * r[1] + kz * r[2]), &s, &c);  // exp(-j k khat.r) = c - j s
+            const double f = qw[7 * t + q] * lp;
+            acc.x += f * c;
+            acc.y -= f * s;
+        }
+    }
+    V[n] = make_double2(E0.x * acc.x - E0.y * acc.y, E0.x * acc.y + E0.y * acc.x);
+}
+
+void launch_planewave(const aim_plan* p, const double* khat, const double* pol, double2 E0, double2* V,
+                      cudaStream_t s) {
+    planewave_kernel<<<nblk(p->N, 256), 256, 0, s>>>(p->tri_qp, p->tri_qw, p->rwg_t, p->rwg_a, p->rwg_p, p->N,
+                                                      p->k, khat[0], khat[1], khat[2], pol[0], pol[1], pol[2], E0,
+                                                      V);
+    note_launch("planewave");
+}
+
+// ------------------------------------------------------- H2-H4 convolution
+void ensure_workspace(aim_plan* p, int R) {
+    if (p->ws_nrhs >= R) return;
+    AIM_CUDA(cudaDeviceSynchronize());
+    p->release(p->Q);
+    p->release(p->W1);
+    p->release(p->W2);
+    const long long Nx = p->dims[0], Ny = p->dims[1], Nz = p->dims[2];
+    const long long Px = p->pads[0], Py = p->pads[1];
+    p->Q = p->alloc<double2>(4 * Nx * Ny * Nz * R);
+    p->W1 = p->alloc<double2>(4 * Px * Ny * Nz * R);
+    p->W2 = p->alloc<double2>(4 * Px * Py * Nz * R);
+    p->ws_nrhs = R;
+}
+
+void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s) {
+    const long long Nx = p->dims[0], Ny = p->dims[1], Nz = p->dims[2];
+    const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2];
+    FftPass f{};
+    // A: x forward, [4][Nx -> Px][Ny Nz R]
+    f.in = Q; f.out = p->W1; f.outer = 4; f.Lin = (int)Nx; f.Lout = Px; f.inner = Ny * Nz * R;
+    f.mode = 0; f.ax = p->ax[0]; f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    prof_mark(p, s);
+    // B1: y forward, [4 Px][Ny -> Py][Nz R]
+    f.in = p->W1; f.out = p->W2; f.outer = 4LL * Px; f.Lin = (int)Ny; f.Lout = Py; f.inner = Nz * R;
+    f.mode = 0; f.ax = p->ax[1]; f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    prof_mark(p, s);
+    // B2: z turnaround in place, [4 Px Py][Nz -> Pz -> Nz][R]
+    f.in = p->W2; f.out = p->W2; f.outer = 4LL * Px * Py; f.Lin = (int)Nz; f.Lout = (int)Nz; f.inner = R;
+    f.mode = 2; f.ax = p->ax[2]; f.TO = f.TI = 0;
+    f.spec = p->spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
+    launch_fft_pass(f, s);
+    prof_mark(p, s);
+    // B3: y inverse, [4 Px][Py -> Ny][Nz R]
+    f.in = p->W2; f.out = p->W1; f.outer = 4LL * Px; f.Lin = Py; f.Lout = (int)Ny; f.inner = Nz * R;
+    f.mode = 1; f.ax = p->ax[1]; f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    prof_mark(p, s);
+    // C: x inverse, [4][Px -> Nx][Ny Nz R]
+    f.in = p->W1; f.out = Phi; f.outer = 4; f.Lin = Px; f.Lout = (int)Nx; f.inner = Ny * Nz * R;
+    f.mode = 1; f.ax = p->ax[0]; f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    prof_mark(p, s);
+}
+
+void prof_mark(aim_plan* p, cudaStream_t s) {
+    if (!p->prof) return;
+    if (p->ev_used == p->ev_pool.size()) {
+        cudaEvent_t e;
+        AIM_CUDA(cudaEventCreate(&e));
+        p->ev_pool.push_back(e);
+    }
+    AIM_CUDA(cudaEventRecord(p->ev_pool[p->ev_used++], s));
+}
+
+void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
+    ensure_workspace(p, R);
+    const int prof = p->prof;   // stages of one matvec are profiled together
+    prof_mark(p, s);
+    launch_project(p, x, p->Q, R, s);
+    prof_mark(p, s);
+    convolve(p, p->Q, p->Q, R, s);
+    launch_interp_near(p, p->Q, x, y, R, true, true, s);
+    prof_mark(p, s);
+    if (prof) p->prof_count++;
+}
+
+}  // namespace aim

@@ -1,0 +1,612 @@
+// Plan construction on the device (setup steps S2-S4 of SURVEY.md §8(a)):
+//   S2 projection weights (tensor Lagrange moment matching, D2) and the
+//      grid-node-sorted projection CSR (deterministic, no atomics);
+//   S3 Green's-function spectrum (sampled min-image kernel, forward FFT via
+//      the same Stockham passes as the matvec, octant storage, D11/D12);
+//   S4 near list (cell list, ||c_m - c_n|| <= r(1+1e-9), D5), exact Galerkin
+//      EFIE entries with singularity subtraction (D8), symmetrisation (D9) and
+//      precorrection Z_corr = Z_ex_sym - Z_grid.
+#include <math.h>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "aim_internal.cuh"
+
+namespace aim {
+
+static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------ S2 weights
+// L_i(t) = prod_{j != i} (t - j)/(i - j) on nodes 0..M
+template <int M>
+__device__ __forceinline__ double lagr(double t, int i) {
+    double num = 1.0, den = 1.0;
+#pragma unroll
+    for (int j = 0; j <= M; ++j)
+        if (j != i) {
+            num *= (t - j);
+            den *= (double)(i - j);
+        }
+    return num / den;
+}
+
+template <int M>
+__global__ void weights_kernel(const double* __restrict__ qp, const double* __restrict__ qw,
+                               const int32_t* __restrict__ rt, const double* __restrict__ ra,
+                               const double* __restrict__ rp, const int32_t* __restrict__ base, double h,
+                               long long N, double* __restrict__ W) {
+    constexpr int M1 = M + 1, S = M1 * M1 * M1;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= N * S) return;
+    const long long n = idx / S;
+    const int u = (int)(idx % S);
+    const int i = u / (M1 * M1), j = (u / M1) % M1, kk = u % M1;
+    const double bx = base[3 * n], by = base[3 * n + 1], bz = base[3 * n + 2];
+    double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    for (int side = 0; side < 2; ++side) {
+        const int t = rt[2 * n + side];
+        const double a = ra[2 * n + side];
+        const double px = rp[6 * n + 3 * side], py = rp[6 * n + 3 * side + 1], pz = rp[6 * n + 3 * side + 2];
+        for (int q = 0; q < 7; ++q) {
+            const double x = qp[(7 * t + q) * 3], y = qp[(7 * t + q) * 3 + 1], z = qp[(7 * t + q) * 3 + 2];
+            const double L = lagr<M>(x / h - bx, i) * lagr<M>(y / h - by, j) * lagr<M>(z / h - bz, kk);
+            const double f = qw[7 * t + q] * L;
+            acc0 += f * a * (x - px);
+            acc1 += f * a * (y - py);
+            acc2 += f * a * (z - pz);
+            acc3 += f * 2.0 * a;
+        }
+    }
+    double2* o = reinterpret_cast<double2*>(W + 4 * idx);
+    o[0] = make_double2(acc0, acc1);
+    o[1] = make_double2(acc2, acc3);
+}
+
+void build_weights(aim_plan* p, cudaStream_t s) {
+    p->W = p->alloc<double>((size_t)p->N * p->S * 4);
+    const long long tot = p->N * p->S;
+    switch (p->M) {
+#define W_CASE(MM) \
+    case MM: weights_kernel<MM><<<nblk(tot, 256), 256, 0, s>>>(p->tri_qp, p->tri_qw, p->rwg_t, p->rwg_a, p->rwg_p, p->base, p->h, p->N, p->W); break;
+        W_CASE(1) W_CASE(2) W_CASE(3) W_CASE(4) W_CASE(5) W_CASE(6)
+#undef W_CASE
+    }
+    note_launch("weights");
+}
+
+// ------------------------------------------------- S2 projection CSR (nodes)
+// Entries of node g: for u (ascending), for n in bucket(g - o_u) (ascending):
+// ent = n*S + u.  bucket(b) = RWGs whose stencil base node is b.
+__global__ void proj_count_kernel(const int32_t* __restrict__ bptr, int Nx, int Ny, int Nz, int M,
+                                  int32_t* __restrict__ cnt) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long Ng = (long long)Nx * Ny * Nz;
+    if (g >= Ng) return;
+    const int x = (int)(g / ((long long)Ny * Nz)), y = (int)((g / Nz) % Ny), z = (int)(g % Nz);
+    int c = 0;
+    for (int i = 0; i <= M; ++i)
+        for (int j = 0; j <= M; ++j)
+            for (int k = 0; k <= M; ++k) {
+                const int bx = x - i, by = y - j, bz = z - k;
+                if (bx < 0 || by < 0 || bz < 0) continue;
+                const long long b = ((long long)bx * Ny + by) * Nz + bz;
+                c += bptr[b + 1] - bptr[b];
+            }
+    cnt[g] = c;
+}
+
+__global__ void proj_fill_kernel(const int32_t* __restrict__ bptr, const int32_t* __restrict__ bids, int Nx,
+                                 int Ny, int Nz, int M, const int32_t* __restrict__ prow,
+                                 int32_t* __restrict__ pent) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long Ng = (long long)Nx * Ny * Nz;
+    if (g >= Ng) return;
+    const int M1 = M + 1, S = M1 * M1 * M1;
+    const int x = (int)(g / ((long long)Ny * Nz)), y = (int)((g / Nz) % Ny), z = (int)(g % Nz);
+    int pos = prow[g];
+    for (int i = 0; i <= M; ++i)
+        for (int j = 0; j <= M; ++j)
+            for (int k = 0; k <= M; ++k) {
+                const int bx = x - i, by = y - j, bz = z - k;
+                if (bx < 0 || by < 0 || bz < 0) continue;
+                const long long b = ((long long)bx * Ny + by) * Nz + bz;
+                const int u = (i * M1 + j) * M1 + k;
+                for (int e = bptr[b]; e < bptr[b + 1]; ++e) pent[pos++] = bids[e] * S + u;
+            }
+}
+
+void build_projection_csr(aim_plan* p, const std::vector<int32_t>& node0, cudaStream_t s) {
+    const long long Ng = p->Ng;
+    // counting sort of RWGs by base node (stable: ascending n inside a bucket)
+    std::vector<int32_t> bptr(Ng + 1, 0), bids(p->N);
+    for (long long n = 0; n < p->N; ++n) bptr[node0[n] + 1]++;
+    for (long long g = 0; g < Ng; ++g) bptr[g + 1] += bptr[g];
+    {
+        std::vector<int32_t> fill(bptr.begin(), bptr.end() - 1);
+        for (long long n = 0; n < p->N; ++n) bids[fill[node0[n]]++] = (int32_t)n;
+    }
+    int32_t* d_bptr = nullptr;
+    int32_t* d_bids = nullptr;
+    int32_t* d_cnt = nullptr;
+    AIM_CUDA(cudaMalloc(&d_bptr, sizeof(int32_t) * (Ng + 1)));
+    AIM_CUDA(cudaMalloc(&d_bids, sizeof(int32_t) * std::max<long long>(1, p->N)));
+    AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int32_t) * Ng));
+    AIM_CUDA(cudaMemcpyAsync(d_bptr, bptr.data(), sizeof(int32_t) * (Ng + 1), cudaMemcpyHostToDevice, s));
+    AIM_CUDA(cudaMemcpyAsync(d_bids, bids.data(), sizeof(int32_t) * p->N, cudaMemcpyHostToDevice, s));
+    proj_count_kernel<<<nblk(Ng, 256), 256, 0, s>>>(d_bptr, p->dims[0], p->dims[1], p->dims[2], p->M, d_cnt);
+    note_launch("proj_count");
+    std::vector<int32_t> cnt(Ng);
+    AIM_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int32_t) * Ng, cudaMemcpyDeviceToHost, s));
+    AIM_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> prow(Ng + 1, 0);
+    long long acc = 0;
+    for (long long g = 0; g < Ng; ++g) {
+        prow[g] = (int32_t)acc;
+        acc += cnt[g];
+    }
+    prow[Ng] = (int32_t)acc;
+    if (acc != p->N * p->S) throw Error(AIM_E_GRID, "projection CSR count mismatch");
+    p->nnzP = acc;
+    p->prow = p->alloc<int32_t>(Ng + 1);
+    p->pent = p->alloc<int32_t>(acc);
+    AIM_CUDA(cudaMemcpyAsync(p->prow, prow.data(), sizeof(int32_t) * (Ng + 1), cudaMemcpyHostToDevice, s));
+    proj_fill_kernel<<<nblk(Ng, 256), 256, 0, s>>>(d_bptr, d_bids, p->dims[0], p->dims[1], p->dims[2], p->M,
+                                                   p->prow, p->pent);
+    note_launch("proj_fill");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_bptr);
+    cudaFree(d_bids);
+    cudaFree(d_cnt);
+}
+
+// ------------------------------------------------------------- S4 near list
+struct CellGrid {
+    double lo[3];
+    double csz;
+    int nc[3];
+    int32_t* cptr;  // [ncells+1]
+    int32_t* cids;  // [N]
+};
+
+__device__ __forceinline__ bool near_pair(const double* c, long long m, long long n, double lim) {
+    const double dx = __dsub_rn(c[3 * m], c[3 * n]);
+    const double dy = __dsub_rn(c[3 * m + 1], c[3 * n + 1]);
+    const double dz = __dsub_rn(c[3 * m + 2], c[3 * n + 2]);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return __dsqrt_rn(d2) <= lim;
+}
+
+__device__ __forceinline__ int cell_of(double v, double lo, double csz, int nc) {
+    int c = (int)floor((v - lo) / csz);
+    return min(max(c, 0), nc - 1);
+}
+
+template <bool FILL>
+__global__ void near_scan_kernel(const double* __restrict__ cen, long long N, CellGrid cg, double lim,
+                                 const int64_t* __restrict__ rowp, int32_t* __restrict__ out_cnt,
+                                 int32_t* __restrict__ out_col) {
+    const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= N) return;
+    int cx = cell_of(cen[3 * m], cg.lo[0], cg.csz, cg.nc[0]);
+    int cy = cell_of(cen[3 * m + 1], cg.lo[1], cg.csz, cg.nc[1]);
+    int cz = cell_of(cen[3 * m + 2], cg.lo[2], cg.csz, cg.nc[2]);
+    long long pos = FILL ? rowp[m] : 0;
+    int cnt = 0;
+    for (int ax = max(cx - 1, 0); ax <= min(cx + 1, cg.nc[0] - 1); ++ax)
+        for (int ay = max(cy - 1, 0); ay <= min(cy + 1, cg.nc[1] - 1); ++ay)
+            for (int az = max(cz - 1, 0); az <= min(cz + 1, cg.nc[2] - 1); ++az) {
+                const long long cell = ((long long)ax * cg.nc[1] + ay) * cg.nc[2] + az;
+                for (int e = cg.cptr[cell]; e < cg.cptr[cell + 1]; ++e) {
+                    const int n = cg.cids[e];
+                    if (near_pair(cen, m, n, lim)) {
+                        if (FILL) out_col[pos++] = n;
+                        else ++cnt;
+                    }
+                }
+            }
+    if (!FILL) out_cnt[m] = cnt;
+}
+
+// warp per row: rank sort (columns are distinct) tmp -> col
+__global__ void near_sort_kernel(const int64_t* __restrict__ rowp, long long N, const int32_t* __restrict__ tmp,
+                                 int32_t* __restrict__ col) {
+    const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (m >= N) return;
+    const long long a = rowp[m], b = rowp[m + 1];
+    for (long long e = a + lane; e < b; e += 32) {
+        const int v = tmp[e];
+        int rank = 0;
+        for (long long f = a; f < b; ++f) rank += (tmp[f] < v);
+        col[a + rank] = v;
+    }
+}
+
+void build_near_list(aim_plan* p, cudaStream_t s) {
+    const long long N = p->N;
+    std::vector<double> cen(3 * N);
+    AIM_CUDA(cudaMemcpy(cen.data(), p->rwg_c, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost));
+    const double lim = p->r * (1.0 + 1e-9);
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = 1e300;
+        hi[a] = -1e300;
+    }
+    for (long long n = 0; n < N; ++n)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], cen[3 * n + a]);
+            hi[a] = std::max(hi[a], cen[3 * n + a]);
+        }
+    double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-30});
+    CellGrid cg;
+    cg.csz = std::max(lim * 1.01, ext / 256.0);
+    long long ncells = 1;
+    for (int a = 0; a < 3; ++a) {
+        cg.lo[a] = lo[a];
+        cg.nc[a] = (int)std::floor((hi[a] - lo[a]) / cg.csz) + 1;
+        ncells *= cg.nc[a];
+    }
+    std::vector<int32_t> cell(N), cptr(ncells + 1, 0), cids(N);
+    for (long long n = 0; n < N; ++n) {
+        int c[3];
+        for (int a = 0; a < 3; ++a)
+            c[a] = std::min(std::max((int)std::floor((cen[3 * n + a] - cg.lo[a]) / cg.csz), 0), cg.nc[a] - 1);
+        cell[n] = (int32_t)(((long long)c[0] * cg.nc[1] + c[1]) * cg.nc[2] + c[2]);
+        cptr[cell[n] + 1]++;
+    }
+    for (long long c = 0; c < ncells; ++c) cptr[c + 1] += cptr[c];
+    {
+        std::vector<int32_t> f(cptr.begin(), cptr.end() - 1);
+        for (long long n = 0; n < N; ++n) cids[f[cell[n]]++] = (int32_t)n;
+    }
+    AIM_CUDA(cudaMalloc(&cg.cptr, sizeof(int32_t) * (ncells + 1)));
+    AIM_CUDA(cudaMalloc(&cg.cids, sizeof(int32_t) * N));
+    AIM_CUDA(cudaMemcpy(cg.cptr, cptr.data(), sizeof(int32_t) * (ncells + 1), cudaMemcpyHostToDevice));
+    AIM_CUDA(cudaMemcpy(cg.cids, cids.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    int32_t* d_cnt = nullptr;
+    AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int32_t) * N));
+    near_scan_kernel<false><<<nblk(N, 256), 256, 0, s>>>(p->rwg_c, N, cg, lim, nullptr, d_cnt, nullptr);
+    note_launch("near_count");
+    std::vector<int32_t> cnt(N);
+    AIM_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+    AIM_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> rowp(N + 1, 0);
+    for (long long m = 0; m < N; ++m) rowp[m + 1] = rowp[m] + cnt[m];
+    const long long nnz = rowp[N];
+    if (nnz > 2147483647LL) throw Error(AIM_E_GRID, "near-field nnz exceeds 2^31-1");
+    p->nnzN = nnz;
+    p->nrow = p->alloc<int64_t>(N + 1);
+    p->ncol = p->alloc<int32_t>(nnz);
+    AIM_CUDA(cudaMemcpyAsync(p->nrow, rowp.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
+    int32_t* tmp = nullptr;
+    AIM_CUDA(cudaMalloc(&tmp, sizeof(int32_t) * std::max<long long>(1, nnz)));
+    near_scan_kernel<true><<<nblk(N, 256), 256, 0, s>>>(p->rwg_c, N, cg, lim, p->nrow, nullptr, tmp);
+    note_launch("near_fill");
+    near_sort_kernel<<<nblk(N * 32, 256), 256, 0, s>>>(p->nrow, N, tmp, p->ncol);
+    note_launch("near_sort");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    cudaFree(d_cnt);
+    cudaFree(cg.cptr);
+    cudaFree(cg.cids);
+}
+
+// ------------------------------------------------------- S4 exact entries
+struct NearArgs {
+    const double* qp;      // [nt][7][3]
+    const double* qw;      // [nt][7]
+    const double* cor;     // [nt][3][3]
+    const int32_t* tv;     // [nt][3]
+    const int32_t* rt;     // [N][2]
+    const double* ra;      // [N][2]
+    const double* rp;      // [N][2][3]
+    const int32_t* base;   // [N][3]
+    const double* W;       // [N][S][4]
+    const int64_t* rowp;
+    const int32_t* col;
+    double2* val;
+    const double2* htab;   // [(D+1)^3] G(h |d|), G(0)=0
+    int D;
+    long long N;
+    double k, h, keta;     // keta = k eta0
+};
+
+struct Mom {
+    double2 I00, I11;
+    double2 I10[3], I01[3];
+};
+
+__device__ __forceinline__ double2 green_full(double R, double k) {
+    double s, c;
+    sincos(k * R, &s, &c);
+    const double f = 1.0 / (4.0 * kPi * R);
+    return make_double2(c * f, -s * f);
+}
+
+// G_s(R) = (exp(-jkR) - 1)/(4 pi R) = (-2 sin^2(kR/2) - j sin kR)/(4 pi R); G_s(0) = -jk/(4 pi)
+__device__ __forceinline__ double2 green_smooth(double R, double k) {
+    if (R == 0.0) return make_double2(0.0, -k / (4.0 * kPi));
+    const double sh = sin(0.5 * k * R);
+    const double f = 1.0 / (4.0 * kPi * R);
+    return make_double2(-2.0 * sh * sh * f, -sin(k * R) * f);
+}
+
+// Static potentials over the flat triangle cor[0..2] seen from r:
+//   J0 = int 1/R dS',  Jr = int r'/R dS'  (D8 closed forms)
+__device__ void static_pot(const double* r, const double* cor, double& J0, double Jr[3]) {
+    const double* v1 = cor;
+    const double* v2 = cor + 3;
+    const double* v3 = cor + 6;
+    double e1[3] = {v2[0] - v1[0], v2[1] - v1[1], v2[2] - v1[2]};
+    double e2[3] = {v3[0] - v1[0], v3[1] - v1[1], v3[2] - v1[2]};
+    double nv[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const double nn = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    nv[0] /= nn; nv[1] /= nn; nv[2] /= nn;
+    const double d = nv[0] * (r[0] - v1[0]) + nv[1] * (r[1] - v1[1]) + nv[2] * (r[2] - v1[2]);
+    const double rho[3] = {r[0] - d * nv[0], r[1] - d * nv[1], r[2] - d * nv[2]};
+    const double ad = fabs(d);
+    double I0 = 0.0, I1[3] = {0.0, 0.0, 0.0};
+    const double* A[3] = {v1, v2, v3};
+    const double* B[3] = {v2, v3, v1};
+    for (int e = 0; e < 3; ++e) {
+        const double* a = A[e];
+        const double* b = B[e];
+        double lv[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        const double le = sqrt(lv[0] * lv[0] + lv[1] * lv[1] + lv[2] * lv[2]);
+        lv[0] /= le; lv[1] /= le; lv[2] /= le;
+        const double u[3] = {lv[1] * nv[2] - lv[2] * nv[1], lv[2] * nv[0] - lv[0] * nv[2], lv[0] * nv[1] - lv[1] * nv[0]};
+        const double lp = (b[0] - rho[0]) * lv[0] + (b[1] - rho[1]) * lv[1] + (b[2] - rho[2]) * lv[2];
+        const double lm = (a[0] - rho[0]) * lv[0] + (a[1] - rho[1]) * lv[1] + (a[2] - rho[2]) * lv[2];
+        const double P0 = (a[0] - rho[0]) * u[0] + (a[1] - rho[1]) * u[1] + (a[2] - rho[2]) * u[2];
+        const double R0sq = P0 * P0 + d * d;
+        const double Rp = sqrt((r[0] - b[0]) * (r[0] - b[0]) + (r[1] - b[1]) * (r[1] - b[1]) + (r[2] - b[2]) * (r[2] - b[2]));
+        const double Rm = sqrt((r[0] - a[0]) * (r[0] - a[0]) + (r[1] - a[1]) * (r[1] - a[1]) + (r[2] - a[2]) * (r[2] - a[2]));
+        double f = 0.0;
+        if (R0sq > (1e-12 * le) * (1e-12 * le)) {
+            const double np_ = lp >= 0 ? Rp + lp : R0sq / (Rp - lp);
+            const double nm_ = lm >= 0 ? Rm + lm : R0sq / (Rm - lm);
+            f = log(np_ / nm_);
+        }
+        I0 += P0 * f - ad * (atan2(P0 * lp, R0sq + ad * Rp) - atan2(P0 * lm, R0sq + ad * Rm));
+        const double c = 0.5 * (R0sq * f + lp * Rp - lm * Rm);
+        I1[0] += c * u[0];
+        I1[1] += c * u[1];
+        I1[2] += c * u[2];
+    }
+    J0 = I0;
+    Jr[0] = I1[0] + rho[0] * I0;
+    Jr[1] = I1[1] + rho[1] * I0;
+    Jr[2] = I1[2] + rho[2] * I0;
+}
+
+// Moments of the triangle pair (t test/outer, tp source/inner)
+__device__ void pair_moments(const NearArgs& a, int t, int tp, bool sing, Mom& m) {
+    m.I00 = m.I11 = make_double2(0, 0);
+    for (int c = 0; c < 3; ++c) m.I10[c] = m.I01[c] = make_double2(0, 0);
+    for (int q = 0; q < 7; ++q) {
+        const double* rq = a.qp + (7 * t + q) * 3;
+        const double wq = a.qw[7 * t + q];
+        double2 in0 = make_double2(0, 0);
+        double2 in1[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+        for (int pp = 0; pp < 7; ++pp) {
+            const double* rpt = a.qp + (7 * tp + pp) * 3;
+            const double wp = a.qw[7 * tp + pp];
+            const double dx = rq[0] - rpt[0], dy = rq[1] - rpt[1], dz = rq[2] - rpt[2];
+            const double R = sqrt(dx * dx + dy * dy + dz * dz);
+            const double2 g = sing ? green_smooth(R, a.k) : green_full(R, a.k);
+            const double2 gw = make_double2(g.x * wp, g.y * wp);
+            in0.x += gw.x; in0.y += gw.y;
+            for (int c = 0; c < 3; ++c) { in1[c].x += gw.x * rpt[c]; in1[c].y += gw.y * rpt[c]; }
+        }
+        if (sing) {
+            double J0, Jr[3];
+            static_pot(rq, a.cor + 9 * tp, J0, Jr);
+            const double s = 1.0 / (4.0 * kPi);
+            in0.x += J0 * s;
+            for (int c = 0; c < 3; ++c) in1[c].x += Jr[c] * s;
+        }
+        m.I00.x += wq * in0.x; m.I00.y += wq * in0.y;
+        for (int c = 0; c < 3; ++c) {
+            m.I10[c].x += wq * in0.x * rq[c]; m.I10[c].y += wq * in0.y * rq[c];
+            m.I01[c].x += wq * in1[c].x;      m.I01[c].y += wq * in1[c].y;
+            m.I11.x += wq * rq[c] * in1[c].x; m.I11.y += wq * rq[c] * in1[c].y;
+        }
+    }
+}
+
+// alpha beta [I11 - pn.I10 - pm.I01 + (pm.pn) I00] - k^-2 (2 alpha)(2 beta) I00   (without j k eta0)
+__device__ __forceinline__ double2 combine(const Mom& m, double al, double be, const double* pm, const double* pn,
+                                           double k) {
+    double2 lam = m.I11;
+    const double pp = pm[0] * pn[0] + pm[1] * pn[1] + pm[2] * pn[2];
+    lam.x += pp * m.I00.x; lam.y += pp * m.I00.y;
+    for (int c = 0; c < 3; ++c) {
+        lam.x -= pn[c] * m.I10[c].x + pm[c] * m.I01[c].x;
+        lam.y -= pn[c] * m.I10[c].y + pm[c] * m.I01[c].y;
+    }
+    const double ab = al * be;
+    const double ch = 4.0 * ab / (k * k);
+    return make_double2(ab * lam.x - ch * m.I00.x, ab * lam.y - ch * m.I00.y);
+}
+
+__device__ __forceinline__ bool share_vertex(const int32_t* tv, int t, int tp) {
+    bool s = false;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) s |= (tv[3 * t + i] == tv[3 * tp + j]);
+    return s;
+}
+
+// Z_ex_sym[m,n] / (j k eta0): regular triangle pairs are symmetric under
+// swapping test and source (same 7x7 products), singular ones are averaged.
+__device__ double2 exact_sym(const NearArgs& a, long long m, long long n) {
+    double2 z = make_double2(0, 0);
+    for (int sm = 0; sm < 2; ++sm)
+        for (int sn = 0; sn < 2; ++sn) {
+            const int t = a.rt[2 * m + sm], tp = a.rt[2 * n + sn];
+            const double al = a.ra[2 * m + sm], be = a.ra[2 * n + sn];
+            const double* pm = a.rp + 6 * m + 3 * sm;
+            const double* pn = a.rp + 6 * n + 3 * sn;
+            Mom mo;
+            const bool sing = share_vertex(a.tv, t, tp);
+            pair_moments(a, t, tp, sing, mo);
+            double2 c = combine(mo, al, be, pm, pn, a.k);
+            if (sing) {
+                Mom mt;
+                pair_moments(a, tp, t, true, mt);  // test on n's triangle, source on m's
+                const double2 c2 = combine(mt, be, al, pn, pm, a.k);
+                c = make_double2(0.5 * (c.x + c2.x), 0.5 * (c.y + c2.y));
+            }
+            z.x += c.x; z.y += c.y;
+        }
+    return z;
+}
+
+// warp per row m, lanes over the row's near entries
+template <int M>
+__global__ void __launch_bounds__(256) near_values_kernel(NearArgs a) {
+    constexpr int M1 = M + 1, S = M1 * M1 * M1;
+    extern __shared__ double2 sh[];
+    const int D1 = a.D + 1;
+    const int ntab = D1 * D1 * D1;
+    double2* htab = sh;
+    double* wm_all = reinterpret_cast<double*>(sh + ntab);
+    for (int i = threadIdx.x; i < ntab; i += blockDim.x) htab[i] = a.htab[i];
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const long long m = (long long)blockIdx.x * (blockDim.x / 32) + warp;
+    if (m >= a.N) return;
+    double* wm = wm_all + warp * S * 4;
+    for (int i = lane; i < S * 4; i += 32) wm[i] = a.W[m * S * 4 + i];
+    __syncwarp();
+    const int bmx = a.base[3 * m], bmy = a.base[3 * m + 1], bmz = a.base[3 * m + 2];
+    for (long long e = a.rowp[m] + lane; e < a.rowp[m + 1]; e += 32) {
+        const long long n = a.col[e];
+        // grid part w_m^T H w_n (xyz) and (phi)
+        const int dx0 = bmx - a.base[3 * n], dy0 = bmy - a.base[3 * n + 1], dz0 = bmz - a.base[3 * n + 2];
+        double2 accA = make_double2(0, 0), accP = make_double2(0, 0);
+        const double* wn = a.W + n * S * 4;
+        for (int v = 0; v < S; ++v) {
+            const double2 w01 = __ldg(reinterpret_cast<const double2*>(wn + 4 * v));
+            const double2 w23 = __ldg(reinterpret_cast<const double2*>(wn + 4 * v) + 1);
+            const int vi = v / (M1 * M1), vj = (v / M1) % M1, vk = v % M1;
+#pragma unroll 4
+            for (int u = 0; u < S; ++u) {
+                const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
+                const int ix = abs(dx0 + ui - vi), iy = abs(dy0 + uj - vj), iz = abs(dz0 + uk - vk);
+                double2 H;
+                if (ix <= a.D && iy <= a.D && iz <= a.D) {
+                    H = htab[(ix * D1 + iy) * D1 + iz];
+                } else {
+                    const double R = a.h * sqrt((double)(ix * ix + iy * iy + iz * iz));
+                    H = green_full(R, a.k);
+                }
+                const double* w = wm + 4 * u;
+                const double s3 = w[0] * w01.x + w[1] * w01.y + w[2] * w23.x;
+                const double s1 = w[3] * w23.y;
+                accA.x += H.x * s3; accA.y += H.y * s3;
+                accP.x += H.x * s1; accP.y += H.y * s1;
+            }
+        }
+        const double ik2 = 1.0 / (a.k * a.k);
+        const double2 grid = make_double2(accA.x - accP.x * ik2, accA.y - accP.y * ik2);
+        const double2 ex = exact_sym(a, m, n);
+        const double2 d = make_double2(ex.x - grid.x, ex.y - grid.y);
+        // j k eta0 * d
+        a.val[e] = make_double2(-a.keta * d.y, a.keta * d.x);
+    }
+}
+
+__global__ void htab_kernel(double2* tab, int D, double h, double k) {
+    const int D1 = D + 1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= D1 * D1 * D1) return;
+    const int x = i / (D1 * D1), y = (i / D1) % D1, z = i % D1;
+    const int q = x * x + y * y + z * z;
+    tab[i] = q == 0 ? make_double2(0, 0) : green_full(h * sqrt((double)q), k);
+}
+
+void build_near_values(aim_plan* p, cudaStream_t s) {
+    p->nval = p->alloc<double2>(p->nnzN);
+    const double lim = p->r * (1.0 + 1e-9);
+    const int D = (int)std::floor(lim / p->h) + 1 + p->M;
+    const int D1 = D + 1;
+    double2* htab = nullptr;
+    AIM_CUDA(cudaMalloc(&htab, sizeof(double2) * D1 * D1 * D1));
+    htab_kernel<<<nblk(D1 * D1 * D1, 256), 256, 0, s>>>(htab, D, p->h, p->k);
+    note_launch("htab");
+    NearArgs a;
+    a.qp = p->tri_qp; a.qw = p->tri_qw; a.cor = p->tri_cor; a.tv = p->tri_v;
+    a.rt = p->rwg_t; a.ra = p->rwg_a; a.rp = p->rwg_p; a.base = p->base; a.W = p->W;
+    a.rowp = p->nrow; a.col = p->ncol; a.val = p->nval; a.htab = htab; a.D = D;
+    a.N = p->N; a.k = p->k; a.h = p->h; a.keta = p->k * eta0();
+    const int threads = 256, warps = threads / 32;
+    const size_t smem = sizeof(double2) * D1 * D1 * D1 + sizeof(double) * warps * p->S * 4;
+    switch (p->M) {
+#define NV_CASE(MM)                                                                                       \
+    case MM:                                                                                              \
+        AIM_CUDA(cudaFuncSetAttribute(near_values_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)std::max<size_t>(smem, 48 * 1024)));                         \
+        near_values_kernel<MM><<<nblk(p->N, warps), threads, smem, s>>>(a);                                \
+        break;
+        NV_CASE(1) NV_CASE(2) NV_CASE(3) NV_CASE(4) NV_CASE(5) NV_CASE(6)
+#undef NV_CASE
+    }
+    note_launch("near_values");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(htab);
+}
+
+// ------------------------------------------------------ S3 Green spectrum
+__global__ void kernel_sample(double2* K, int Px, int Py, int Pz, double h, double k) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long tot = (long long)Px * Py * Pz;
+    if (i >= tot) return;
+    const int x = (int)(i / ((long long)Py * Pz)), y = (int)((i / Pz) % Py), z = (int)(i % Pz);
+    const int ix = min(x, Px - x), iy = min(y, Py - y), iz = min(z, Pz - z);
+    const double q = (double)ix * ix + (double)iy * iy + (double)iz * iz;
+    K[i] = q == 0 ? make_double2(0, 0) : green_full(h * sqrt(q), k);
+}
+
+__global__ void spectrum_octant(const double2* F, double2* spec, int Px, int Py, int Pz, double scale) {
+    const int PxH = Px / 2 + 1, PyH = Py / 2 + 1, PzH = Pz / 2 + 1;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)PxH * PyH * PzH) return;
+    const int x = (int)(i / ((long long)PyH * PzH)), y = (int)((i / PzH) % PyH), z = (int)(i % PzH);
+    const double2 v = F[((long long)x * Py + y) * Pz + z];
+    spec[i] = make_double2(v.x * scale, v.y * scale);
+}
+
+void build_green_spectrum(aim_plan* p, cudaStream_t s) {
+    const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2];
+    const long long tot = (long long)Px * Py * Pz;
+    double2 *A = nullptr, *B = nullptr;
+    AIM_CUDA(cudaMalloc(&A, sizeof(double2) * tot));
+    AIM_CUDA(cudaMalloc(&B, sizeof(double2) * tot));
+    kernel_sample<<<nblk(tot, 256), 256, 0, s>>>(A, Px, Py, Pz, p->h, p->k);
+    note_launch("kernel_sample");
+    FftPass f{};
+    f.mode = 0;
+    // x: [1][Px][Py Pz]
+    f.in = A; f.out = B; f.outer = 1; f.Lin = f.Lout = Px; f.inner = (long long)Py * Pz; f.ax = p->ax[0];
+    f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    // y: [Px][Py][Pz]
+    f.in = B; f.out = A; f.outer = Px; f.Lin = f.Lout = Py; f.inner = Pz; f.ax = p->ax[1];
+    f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    // z: [Px Py][Pz][1]
+    f.in = A; f.out = B; f.outer = (long long)Px * Py; f.Lin = f.Lout = Pz; f.inner = 1; f.ax = p->ax[2];
+    f.TO = f.TI = 0;
+    launch_fft_pass(f, s);
+    const long long oct = (long long)(Px / 2 + 1) * (Py / 2 + 1) * (Pz / 2 + 1);
+    p->spec = p->alloc<double2>(oct);
+    spectrum_octant<<<nblk(oct, 256), 256, 0, s>>>(B, p->spec, Px, Py, Pz, 1.0 / ((double)tot));
+    note_launch("spectrum_octant");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(A);
+    cudaFree(B);
+}
+
+}  // namespace aim

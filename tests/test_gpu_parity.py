@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Tolerances (BASELINE.json north_star / DESIGN.md):
+  integer tables (stencils, near list, projection CSR): bit-exact;
+  plan values (weights, spectrum, near entries): 1e-12 relative to the table's max;
+  matvec: <= 1e-10 relative L2 (complex128); GMRES: <= 1e-5 at equal iteration counts.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import oracle_plan  # noqa: E402
+from workloads import get_config, make_mesh, make_vectors  # noqa: E402
+
+SMALL = ["c1", "t_m3", "t_vol", "t_dissim", "t_one"]
+_GPU = {}
+
+
+def gpu_plan(name, **over):
+    from paper_1712_02443_b200 import AimPlan
+    key = (name, tuple(sorted(over.items())))
+    if key not in _GPU:
+        cfg = get_config(name)
+        p = dict(k=cfg.k, h=cfg.h, M=cfg.M, near_radius=cfg.near_radius)
+        p.update(over)
+        _GPU[key] = AimPlan.from_mesh(make_mesh(cfg), p["k"], p["h"], p["M"], p["near_radius"])
+    return _GPU[key]
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_plan_tables(name):
+    G, O = gpu_plan(name), oracle_plan(name)
+    inf = G.info
+    assert inf["grid_dims"] == tuple(int(d) for d in O.dims)
+    assert inf["grid_origin"] == tuple(int(d) for d in O.origin)
+    assert all(p >= 2 * n - 1 for p, n in zip(inf["fft_dims"], inf["grid_dims"]))
+    # stencil tables: exact (D3 ties are systemic)
+    assert np.array_equal(G.export("bases"), O.bases.astype(np.int32))
+    W = G.export("weights")
+    assert np.abs(W - O.W).max() <= 1e-13 * np.abs(O.W).max()
+    # projection CSR: same (node, n, u) entry set, per node
+    prow, pent = G.export("proj_rowptr"), G.export("proj_ent")
+    assert prow[-1] == O.N * O.S
+    nodes = O.stencil_nodes()
+    ent_o = np.sort(nodes.ravel().astype(np.int64) * (O.N * O.S) + np.arange(O.N * O.S))
+    node_g = np.repeat(np.arange(prow.size - 1), np.diff(prow))
+    ent_g = np.sort(node_g.astype(np.int64) * (O.N * O.S) + pent)
+    assert np.array_equal(ent_g, ent_o)
+    # near list: exact (rows, ascending columns)
+    rp_o, col_o = O.near_pairs()
+    assert np.array_equal(G.export("near_rowptr"), rp_o)
+    assert np.array_equal(G.export("near_col"), col_o)
+    # near values: Z_ex_sym - Z_grid
+    val = G.export("near_val")
+    ref = O.near_full().data
+    assert np.abs(val - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["c1", "t_vol"])
+def test_green_spectrum(name):
+    G, O = gpu_plan(name), oracle_plan(name)
+    pads = G.info["fft_dims"]
+    F = np.fft.fftn(O.kernel_samples(pads)) / np.prod(pads)
+    oct_ = F[: pads[0] // 2 + 1, : pads[1] // 2 + 1, : pads[2] // 2 + 1]
+    g = G.export("green")
+    assert np.abs(g - oct_).max() <= 1e-13 * np.abs(oct_).max()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_stages(name):
+    G, O = gpu_plan(name), oracle_plan(name)
+    nrhs = get_config(name).nrhs
+    x = make_vectors(O.N, nrhs, 0)
+    xt = torch.from_numpy(x).cuda()
+    Q = G.project(xt)
+    Qo = O.project(x)
+    assert rel(Q.cpu().numpy(), Qo) <= 1e-13
+    Phi = G.convolve(Q.contiguous())
+    Phio = O.convolve_direct(Qo) if O.Ng <= 4000 else O.convolve_fft(Qo)
+    assert rel(Phi.cpu().numpy(), Phio) <= 1e-12
+    yf = G.interpolate(Phi.contiguous())
+    assert rel(yf.cpu().numpy(), O.interpolate(Phio)) <= 1e-12
+    yn = G.interpolate(None, xt, add_near=True)
+    assert rel(yn.cpu().numpy(), O.near_full() @ x) <= 1e-13
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_matvec_small(name):
+    G, O = gpu_plan(name), oracle_plan(name)
+    nrhs = get_config(name).nrhs
+    x = make_vectors(O.N, nrhs, 0)
+    y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel(y, O.matvec(x)) <= 1e-10
+
+
+@pytest.mark.parametrize("nrhs", [1, 2, 3, 5, 16, 33])
+def test_matvec_nrhs_and_determinism(nrhs):
+    G, O = gpu_plan("c1"), oracle_plan("c1")
+    x = make_vectors(O.N, nrhs, 7)
+    xt = torch.from_numpy(x).cuda()
+    y1 = G.matvec(xt).cpu().numpy()
+    y2 = G.matvec(xt).cpu().numpy()
+    assert np.array_equal(y1, y2)          # deterministic gathers, fixed reduction order
+    ref = O.matvec(x)
+    assert rel(y1, ref) <= 1e-10
+    # each column equals the single-RHS product
+    y0 = G.matvec(xt[:, 0].contiguous()).cpu().numpy()
+    assert rel(y1[:, 0], y0) <= 1e-14
+    # end-to-end host path
+    yh = G.matvec_host(x)
+    assert np.array_equal(yh, y1)
+
+
+def test_matvec_c2_full_size_sampled_rows():
+    """configs[1] at full size (N=115,200, 16 RHS, bench launch config):
+    sampled rows against the oracle computed row by row."""
+    G, O = gpu_plan("c2"), oracle_plan("c2")
+    x = make_vectors(O.N, 16, 0)
+    y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    rows = np.unique(np.concatenate([[0, O.N - 1], np.random.default_rng(0).integers(0, O.N, 48)]))
+    ref = O.matvec_rows(x, rows)
+    assert rel(y[rows], ref) <= 1e-10
+
+
+def test_planewave_rhs():
+    from oracle.excitation import plane_wave_rhs
+    G, O = gpu_plan("c1"), oracle_plan("c1")
+    V = G.planewave_rhs().cpu().numpy()
+    assert rel(V, plane_wave_rhs(O.ctx)) <= 1e-13
+    V2 = G.planewave_rhs(khat=(0.6, 0.0, 0.8), pol=(0.0, 1.0, 0.0), E0=2 - 1j).cpu().numpy()
+    assert rel(V2, plane_wave_rhs(O.ctx, (0.6, 0.0, 0.8), (0.0, 1.0, 0.0), 2 - 1j)) <= 1e-13
+
+
+def test_gmres_c1():
+    """D15: equal iteration counts -> <= 1e-5; converged counts within +-1."""
+    from oracle.gmres import gmres
+    from oracle.excitation import plane_wave_rhs
+    G, O = gpu_plan("c1"), oracle_plan("c1")
+    V = plane_wave_rhs(O.ctx)
+    Vt = torch.from_numpy(V).cuda()
+    ref = gmres(O.matvec, V, restart=50, tol=1e-4)
+    J, it, rr, st = G.gmres(Vt, restart=50, tol=1e-4)
+    assert st == "AIM_OK" and rr <= 1e-4
+    assert abs(it - ref["iters"]) <= 1
+    fixed = ref["iters"]
+    Jf, itf, _, _ = G.gmres(Vt, restart=50, tol=1e-4, fixed_iters=fixed)
+    assert itf == fixed
+    assert rel(Jf.cpu().numpy(), ref["x"]) <= 1e-5
+    # residual check with one oracle matvec on the GPU's solution
+    Jn = J.cpu().numpy()
+    assert np.linalg.norm(V - O.matvec(Jn)) / np.linalg.norm(V) <= 1e-4 * (1 + 1e-6)
+
+
+def test_errors():
+    from paper_1712_02443_b200 import AimPlan, AimError
+    m = make_mesh("t_one")
+    bad = m.rwg.copy()
+    bad[3, 3] = bad[3, 2]
+    with pytest.raises(AimError) as e:
+        AimPlan(m.vertices, m.triangles, bad, 2 * np.pi, 0.1, 2, 0.3)
+    assert e.value.status == -2
+    bad = m.rwg.copy()
+    bad[0, 0] = bad[5, 1] if bad[5, 1] != bad[0, 1] else bad[6, 1]
+    with pytest.raises(AimError) as e:
+        AimPlan(m.vertices, m.triangles, bad, 2 * np.pi, 0.1, 2, 0.3)
+    assert e.value.status == -2
+    with pytest.raises(AimError) as e:
+        AimPlan(m.vertices, m.triangles, m.rwg, 2 * np.pi, 0.0, 2, 0.3)
+    assert e.value.status == -1
+    with pytest.raises(AimError) as e:
+        AimPlan(m.vertices, m.triangles, m.rwg, 2 * np.pi, 1e-7, 2, 0.3)   # grid too large
+    assert e.value.status == -3
+
+
+def test_degenerate_cases():
+    """near_radius = 0 (self pairs only) and a radius covering everything."""
+    from oracle.aim import OraclePlan
+    from paper_1712_02443_b200 import AimPlan
+    m = make_mesh("t_one")
+    x = make_vectors(m.n_rwg, 2, 3)
+    for r in (0.0, 10.0):
+        G = AimPlan(m.vertices, m.triangles, m.rwg, 2 * np.pi, 0.1, 2, r)
+        O = OraclePlan(m, 2 * np.pi, 0.1, 2, r)
+        assert G.info["nnz_near"] == (m.n_rwg if r == 0 else m.n_rwg ** 2)
+        y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel(y, O.matvec(x)) <= 1e-10
+        G.close()
