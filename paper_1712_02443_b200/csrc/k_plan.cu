@@ -530,7 +530,9 @@ __global__ void htab_kernel(double2* tab, int D, double h, double k) {
 void build_near_values(aim_plan* p, cudaStream_t s) {
     p->nval = p->alloc<double2>(p->nnzN);
     const double lim = p->r * (1.0 + 1e-9);
-    const int D = (int)std::floor(lim / p->h) + 1 + p->M;
+    // table of G(h|d|) over |d_a| <= D in shared memory; offsets beyond the
+    // table (huge near radii) fall back to direct evaluation in the kernel
+    const int D = std::min((int)std::floor(lim / p->h) + 1 + p->M, 15);
     const int D1 = D + 1;
     double2* htab = nullptr;
     AIM_CUDA(cudaMalloc(&htab, sizeof(double2) * D1 * D1 * D1));
