@@ -71,6 +71,10 @@ typedef struct aim_info {
     double k, h, near_radius;
     int64_t device_bytes;   /* device memory owned by the plan (workspaces incl.) */
     double plan_seconds;    /* wall time of aim_plan_create                     */
+    int32_t conv_mode;      /* 0: 3-D FFT convolution, spectrum octant
+                               [(Px/2+1)][(Py/2+1)][(Pz/2+1)];
+                               1: planar -- 2-D FFT in x,y and direct Toeplitz
+                               product in z, spectrum [(Px/2+1)][(Py/2+1)][Nz]  */
 } aim_info;
 
 /*
@@ -170,7 +174,7 @@ enum {
     AIM_EXPORT_NEAR_ROWPTR = 2,/* int64   [N+1]                                 */
     AIM_EXPORT_NEAR_COL = 3,   /* int32   [nnz_near] (ascending within a row)   */
     AIM_EXPORT_NEAR_VAL = 4,   /* complex128 [nnz_near] Z_corr                  */
-    AIM_EXPORT_GREEN = 5,      /* complex128 [(Px/2+1)(Py/2+1)(Pz/2+1)] spectrum */
+    AIM_EXPORT_GREEN = 5,      /* complex128 spectrum, shape per aim_info.conv_mode */
     AIM_EXPORT_PROJ_ROWPTR = 6,/* int32   [Nx Ny Nz + 1]                        */
     AIM_EXPORT_PROJ_ENT = 7    /* int32   [N S] entries n*S + u                  */
 };
@@ -180,13 +184,13 @@ int aim_plan_export(const aim_plan* plan, int32_t what, void* dst, int64_t bytes
 /* ---- live stage timing (bench accounting) ------------------------------- */
 /* Stage ids of one aim_matvec, in launch order. */
 enum {
-    AIM_STAGE_PROJECT = 0,   /* H1 projection gather                         */
-    AIM_STAGE_FFT_X = 1,     /* H2 x forward pass (zero-pad fused)           */
-    AIM_STAGE_FFT_Y = 2,     /* H2 y forward pass (zero-pad fused)           */
-    AIM_STAGE_FFT_Z = 3,     /* H2-H4 z turnaround: fwd, x spectrum, inv     */
-    AIM_STAGE_IFFT_Y = 4,    /* H4 y inverse pass (pruned)                   */
-    AIM_STAGE_IFFT_X = 5,    /* H4 x inverse pass (pruned)                   */
-    AIM_STAGE_INTERP_NEAR = 6, /* H5+H6 interpolation + near SpMV            */
+    AIM_STAGE_PROJECT = 0,   /* H1 projection gather (main stream)                   */
+    AIM_STAGE_FFT_X = 1,     /* H2 x forward pass, zero-pad fused                    */
+    AIM_STAGE_FFT_YZ = 2,    /* H2-H4 y fwd, z convolution x spectrum, y inv         */
+    AIM_STAGE_IFFT_X = 3,    /* H4 x inverse pass, pruned                            */
+    AIM_STAGE_NEAR_WAIT = 4, /* main stream waiting for the near SpMV (0 if hidden)  */
+    AIM_STAGE_INTERP = 5,    /* H5 interpolation, adds the far field to y            */
+    AIM_STAGE_NEAR = 6,      /* H6 near-field SpMV on the side stream (overlaps 0-3) */
     AIM_NUM_STAGES = 7
 };
 /* enable != 0: every subsequent aim_matvec records CUDA events around each

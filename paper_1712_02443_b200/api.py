@@ -165,7 +165,7 @@ class AimPlan:
         return y
 
     # ---- live stage timing
-    STAGES = ("project", "fft_x", "fft_y", "fft_z_turn", "ifft_y", "ifft_x", "interp_near")
+    STAGES = ("project", "fft_x", "fft_yz", "ifft_x", "near_wait", "interp", "near")
 
     def profile(self, enable: bool):
         _check(_lib.load().aim_profile(self._p, 1 if enable else 0))
@@ -185,7 +185,8 @@ class AimPlan:
             "bases": (np.int32, (N, 3)), "weights": (np.float64, (N, S, 4)),
             "near_rowptr": (np.int64, (N + 1,)), "near_col": (np.int32, (inf["nnz_near"],)),
             "near_val": (np.complex128, (inf["nnz_near"],)),
-            "green": (np.complex128, (Px // 2 + 1, Py // 2 + 1, Pz // 2 + 1)),
+            "green": (np.complex128, (Px // 2 + 1, Py // 2 + 1,
+                                      inf["grid_dims"][2] if inf["conv_mode"] == 1 else Pz // 2 + 1)),
             "proj_rowptr": (np.int32, (inf["n_nodes"] + 1,)), "proj_ent": (np.int32, (inf["nnz_proj"],)),
         }
         dt, sh = shapes[what]

@@ -76,6 +76,9 @@ static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, co
     const auto t0 = std::chrono::steady_clock::now();
     AIM_CUDA(cudaGetDevice(&p->device));
     AIM_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    AIM_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    AIM_CUDA(cudaEventCreateWithFlags(&p->ev_x, cudaEventDisableTiming));
+    AIM_CUDA(cudaEventCreateWithFlags(&p->ev_n, cudaEventDisableTiming));
     p->N = N; p->nt = nt; p->nv = nv; p->k = k; p->h = h; p->M = M; p->r = r;
     p->S = (M + 1) * (M + 1) * (M + 1);
 
@@ -177,6 +180,7 @@ static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, co
     p->base = upload(p, base);
     p->node0 = upload(p, node0);
     for (int d = 0; d < 3; ++d) make_fft_axis(p->pads[d], p->ax[d]);
+    p->planar = planar_supported(p->pads[1], p->dims[2]) ? 1 : 0;
 
     // ---- device setup S2-S4
     cudaStream_t s = p->stream;
@@ -200,6 +204,9 @@ static void destroy(aim_plan* p) {
         if (p->ax[d].tw) cudaFree(p->ax[d].tw);
     for (auto e : p->ev_pool) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->side) cudaStreamDestroy(p->side);
+    if (p->ev_x) cudaEventDestroy(p->ev_x);
+    if (p->ev_n) cudaEventDestroy(p->ev_n);
     cudaSetDevice(cur);
     delete p;
 }
@@ -263,6 +270,7 @@ int aim_plan_info(const aim_plan* p, aim_info* info) {
     info->near_radius = p->r;
     info->device_bytes = p->device_bytes;
     info->plan_seconds = p->plan_seconds;
+    info->conv_mode = p->planar;
     return AIM_OK;
 }
 
@@ -338,8 +346,9 @@ int aim_interpolate(aim_plan* p, const void* Phi, const void* x, void* y, int32_
                     void* stream) {
     if (!p || !y || nrhs < 1 || (add_near && !x) || (!Phi && !add_near)) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
-        launch_interp_near(p, (const double2*)Phi, (const double2*)x, (double2*)y, nrhs, Phi != nullptr,
-                           add_near != 0, (cudaStream_t)stream);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (add_near) launch_near(p, (const double2*)x, (double2*)y, nrhs, s);
+        if (Phi) launch_interp(p, (const double2*)Phi, (double2*)y, nrhs, add_near != 0, s);
         return AIM_OK;
     });
 }
@@ -355,10 +364,7 @@ int aim_plan_export(const aim_plan* p, int32_t what, void* dst, int64_t bytes) {
             case AIM_EXPORT_NEAR_ROWPTR: src = p->nrow; need = 8 * (p->N + 1); break;
             case AIM_EXPORT_NEAR_COL: src = p->ncol; need = 4 * p->nnzN; break;
             case AIM_EXPORT_NEAR_VAL: src = p->nval; need = 16 * p->nnzN; break;
-            case AIM_EXPORT_GREEN:
-                src = p->spec;
-                need = 16LL * (p->pads[0] / 2 + 1) * (p->pads[1] / 2 + 1) * (p->pads[2] / 2 + 1);
-                break;
+            case AIM_EXPORT_GREEN: src = p->spec; need = 16 * p->spec_len; break;
             case AIM_EXPORT_PROJ_ROWPTR: src = p->prow; need = 4 * (p->Ng + 1); break;
             case AIM_EXPORT_PROJ_ENT: src = p->pent; need = 4 * p->nnzP; break;
             default: throw Error(AIM_E_ARG, "unknown export id");
@@ -384,15 +390,20 @@ int aim_profile_read(aim_plan* p, double* ms, int64_t* count) {
     if (!p || !ms || !count) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
         for (int i = 0; i < AIM_NUM_STAGES; ++i) ms[i] = 0.0;
-        const size_t per = AIM_NUM_STAGES + 1;
+        const size_t per = kProfEvents;
         if (p->ev_used % per) throw Error(AIM_E_ARG, "profiling events out of step");
-        if (p->ev_used) AIM_CUDA(cudaEventSynchronize(p->ev_pool[p->ev_used - 1]));
-        for (size_t b = 0; b < p->ev_used; b += per)
+        // (from, to) event slots of each stage, see matvec() in k_matvec.cu
+        static const int from[AIM_NUM_STAGES] = {0, 1, 2, 3, 4, 5, 7};
+        static const int to[AIM_NUM_STAGES] = {1, 2, 3, 4, 5, 6, 8};
+        for (size_t b = 0; b < p->ev_used; b += per) {
+            AIM_CUDA(cudaEventSynchronize(p->ev_pool[b + 6]));
+            AIM_CUDA(cudaEventSynchronize(p->ev_pool[b + 8]));
             for (int i = 0; i < AIM_NUM_STAGES; ++i) {
                 float t = 0.f;
-                AIM_CUDA(cudaEventElapsedTime(&t, p->ev_pool[b + i], p->ev_pool[b + i + 1]));
+                AIM_CUDA(cudaEventElapsedTime(&t, p->ev_pool[b + from[i]], p->ev_pool[b + to[i]]));
                 ms[i] += t;
             }
+        }
         *count = p->prof_count;
         p->ev_used = 0;
         p->prof_count = 0;

@@ -62,7 +62,20 @@ struct FftPass {
     int PyH, PzH;        // octant extents Py/2+1, Pz/2+1
 };
 
+// Fused planar y/z pass (planar arrays): y fwd, direct z convolution with the
+// 2-D spectrum G2[(Px/2+1)][(Py/2+1)][Nz], y inv; in place on [4][Px][Ny][Nz][R].
+constexpr int kPlanarMaxNz = 16;
+struct PlanarPass {
+    double2* W;
+    int Px, Ny, Nz, R, RC;
+    int PyH;
+    FftAxis ay;
+    const double2* spec;
+};
+
 void launch_fft_pass(const FftPass& p, cudaStream_t s);
+void launch_planar_yz(const PlanarPass& p, cudaStream_t s);
+bool planar_supported(int Py, int Nz);
 void make_fft_axis(int P, FftAxis& ax);    // factorisation + device twiddles
 int smooth_size_at_least(int n);           // smallest 2^a 3^b 5^c 7^d >= n
 
@@ -100,7 +113,9 @@ struct aim_plan {
     int64_t* nrow = nullptr;      // [N+1]
     int32_t* ncol = nullptr;      // [nnzN]
     double2* nval = nullptr;      // [nnzN]
-    double2* spec = nullptr;      // [(Px/2+1)(Py/2+1)(Pz/2+1)]
+    int planar = 0;               // 1: z handled by direct convolution (spec = G2)
+    double2* spec = nullptr;      // 3-D: [(Px/2+1)(Py/2+1)(Pz/2+1)]; planar: [(Px/2+1)(Py/2+1)][Nz]
+    int64_t spec_len = 0;
     aim::FftAxis ax[3];
 
     // workspaces (device), sized for ws_nrhs
@@ -118,7 +133,10 @@ struct aim_plan {
     double2* hx = nullptr;
     double2* hy = nullptr;
 
-    // live stage timing (aim_profile): 8 events per profiled matvec
+    // side stream for the near-field SpMV (overlaps the FFT passes)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_n = nullptr;
+    // live stage timing (aim_profile): kProfEvents events per profiled matvec
     int prof = 0;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -154,6 +172,8 @@ struct aim_plan {
 
 namespace aim {
 
+constexpr int kProfEvents = 9;
+
 // ---- plan-building launches (k_plan.cu)
 void build_weights(aim_plan* p, cudaStream_t s);
 void build_projection_csr(aim_plan* p, const std::vector<int32_t>& node0_host, cudaStream_t s);
@@ -163,14 +183,13 @@ void build_green_spectrum(aim_plan* p, cudaStream_t s);
 
 // ---- matvec launches (k_matvec.cu)
 void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s);
-void launch_interp_near(const aim_plan* p, const double2* Phi, const double2* x, double2* y, int R,
-                        bool far, bool near, cudaStream_t s);
+void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s);
+void launch_near(const aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
 void launch_planewave(const aim_plan* p, const double* khat, const double* pol, double2 E0, double2* V,
                       cudaStream_t s);
 void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s);
 void ensure_workspace(aim_plan* p, int R);
 void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
-void prof_mark(aim_plan* p, cudaStream_t s);  // records a stage-boundary event when profiling
 
 // ---- GMRES (k_gmres.cu)
 int gmres(aim_plan* p, const double2* V, double2* J, int restart, double tol, int max_iters, int fixed_iters,

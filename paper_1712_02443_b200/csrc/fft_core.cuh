@@ -1,0 +1,147 @@
+// Shared-memory mixed-radix Stockham FFT core used by the FFT pass kernels
+// (step (ii) of the AIM matvec, eq. AIM_step2).
+//
+// NL independent lines of length P live in shared memory laid out [P][NL]
+// (line index fastest => conflict-free butterflies), ping-ponged between two
+// buffers; each stage applies twiddles + the radix-R DFT in registers and
+// stores in Stockham (self-sorting) order.
+//   stage: j in [0, P/R), k = j mod Ns
+//     a_t = x[j + t P/R] * w^{t k P/(Ns R)},  b = DFT_R(a),
+//     y[(j div Ns) Ns R + k + u Ns] = b_u
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "aim_internal.cuh"
+
+namespace aim {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// cos / sin (2 pi (m+1) / R), m = 0 .. (R-3)/2, for the odd radices
+template <int R>
+__device__ __forceinline__ constexpr double oc(int m) {
+    return R == 3 ? -0.5
+         : R == 5 ? (m == 0 ? 0.309016994374947451263 : -0.809016994374947451263)
+                  : (m == 0 ? 0.623489801858733483364 : m == 1 ? -0.222520933956314392876 : -0.900968867902419145999);
+}
+template <int R>
+__device__ __forceinline__ constexpr double os(int m) {
+    return R == 3 ? 0.866025403784438596588
+         : R == 5 ? (m == 0 ? 0.951056516295153531182 : 0.587785252292473137103)
+                  : (m == 0 ? 0.781831482468029803634 : m == 1 ? 0.974927912181823619342 : 0.433883739117558120402);
+}
+
+// b_u = sum_t a_t exp(sign 2 pi i t u / R), in place
+template <int R>
+__device__ __forceinline__ void dft(double2* a, double sign) {
+    if constexpr (R == 2) {
+        const double2 t = a[0];
+        a[0] = cadd(t, a[1]);
+        a[1] = csub(t, a[1]);
+    } else if constexpr (R == 4) {
+        const double2 t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
+        const double2 t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
+        const double2 t3 = make_double2(-sign * d.y, sign * d.x);  // d * (sign i)
+        a[0] = cadd(t0, t2);
+        a[2] = csub(t0, t2);
+        a[1] = cadd(t1, t3);
+        a[3] = csub(t1, t3);
+    } else {
+        // odd R: p_t = a_t + a_{R-t}, m_t = a_t - a_{R-t}
+        //   b_u     = a0 + sum_t [cos(th) p_t + i sign sin(th) m_t]
+        //   b_{R-u} = a0 + sum_t [cos(th) p_t - i sign sin(th) m_t],  th = 2 pi t u / R
+        constexpr int H = (R - 1) / 2;
+        double2 p[H], m[H];
+#pragma unroll
+        for (int t = 1; t <= H; ++t) {
+            p[t - 1] = cadd(a[t], a[R - t]);
+            m[t - 1] = csub(a[t], a[R - t]);
+        }
+        const double2 a0 = a[0];
+        double2 s0 = a0;
+#pragma unroll
+        for (int t = 0; t < H; ++t) s0 = cadd(s0, p[t]);
+#pragma unroll
+        for (int u = 1; u <= H; ++u) {
+            double2 re = a0, im = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int t = 1; t <= H; ++t) {
+                const int idx = (t * u) % R;
+                const double c = idx <= H ? oc<R>(idx - 1) : oc<R>(R - idx - 1);
+                const double s = idx <= H ? os<R>(idx - 1) : -os<R>(R - idx - 1);
+                re.x = fma(c, p[t - 1].x, re.x);
+                re.y = fma(c, p[t - 1].y, re.y);
+                im.x = fma(s, m[t - 1].x, im.x);
+                im.y = fma(s, m[t - 1].y, im.y);
+            }
+            a[u] = make_double2(re.x - sign * im.y, re.y + sign * im.x);
+            a[R - u] = make_double2(re.x + sign * im.y, re.y - sign * im.x);
+        }
+        a[0] = s0;
+    }
+}
+
+// One Stockham stage of radix R over NL lines of length P, src -> dst
+// (ping-pong buffers; each thread loops over butterflies with R registers).
+template <int R>
+__device__ __forceinline__ void stage(const double2* __restrict__ src, double2* __restrict__ dst,
+                                      const double2* __restrict__ tw, int P, int NL, int Ns, double sign) {
+    const int B = P / R;
+    const int stride = P / (Ns * R);
+    const int total = NL * B;
+    for (int b = threadIdx.x; b < total; b += blockDim.x) {
+        const int l = b % NL;
+        const int j = b / NL;
+        const int k = j % Ns;
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = src[(j + t * B) * NL + l];
+        if (k) {
+#pragma unroll
+            for (int t = 1; t < R; ++t) {
+                double2 w = tw[t * k * stride];  // exp(-2 pi i e / P)
+                if (sign > 0) w.y = -w.y;
+                a[t] = cmul(a[t], w);
+            }
+        }
+        dft<R>(a, sign);
+        const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int u = 0; u < R; ++u) dst[(base + u * Ns) * NL + l] = a[u];
+    }
+}
+
+// Full transform of NL lines (sign -1 forward, +1 inverse, unscaled) between
+// the two buffers; returns the buffer holding the result.
+__device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const double2* tw, const FftAxis& ax, int NL,
+                                              double sign) {
+    int Ns = 1;
+    double2* src = b0;
+    double2* dst = b1;
+    for (int s = 0; s < ax.nst; ++s) {
+        switch (ax.radix[s]) {
+            case 2: stage<2>(src, dst, tw, ax.P, NL, Ns, sign); break;
+            case 3: stage<3>(src, dst, tw, ax.P, NL, Ns, sign); break;
+            case 4: stage<4>(src, dst, tw, ax.P, NL, Ns, sign); break;
+            case 5: stage<5>(src, dst, tw, ax.P, NL, Ns, sign); break;
+            case 7: stage<7>(src, dst, tw, ax.P, NL, Ns, sign); break;
+        }
+        __syncthreads();
+        Ns *= ax.radix[s];
+        double2* t = src;
+        src = dst;
+        dst = t;
+    }
+    return src;
+}
+
+// Complex elements per ping-pong buffer of one CTA (2 buffers + twiddles ~ 70 KB
+// -> 3 CTAs of 256 threads per SM).
+__host__ __device__ constexpr int fft_tile_capacity() { return 2304; }
+
+}  // namespace aim

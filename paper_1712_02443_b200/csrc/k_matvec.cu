@@ -90,88 +90,120 @@ void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cuda
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
-// ------------------------------------------------ H5 + H6 interp + near
+// ------------------------------------------------------ H5 interpolation
+// y[m,r] (+)= j k eta0 [sum_xyz sum_u w_{m,u} Phi[u,r] - k^-2 sum_u w^phi_{m,u} Phi^phi[u,r]]
 template <int M, int RC>
-__global__ void __launch_bounds__(256) interp_near_kernel(const double2* __restrict__ Phi,
-                                                          const double* __restrict__ W,
-                                                          const int32_t* __restrict__ node0, long long Ng, int Ny,
-                                                          int Nz, const int64_t* __restrict__ rowp,
-                                                          const int32_t* __restrict__ col,
-                                                          const double2* __restrict__ val,
-                                                          const double2* __restrict__ x, long long N, int R,
-                                                          double keta, double ik2, int do_far, int do_near,
-                                                          double2* __restrict__ y) {
+__global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__ Phi, const double* __restrict__ W,
+                                                     const int32_t* __restrict__ node0, long long Ng, int Ny, int Nz,
+                                                     long long N, int R, double keta, double ik2, int accumulate,
+                                                     double2* __restrict__ y) {
     constexpr int M1 = M + 1, S = M1 * M1 * M1;
     constexpr int G = 32 / RC;
     const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (m >= N) return;
     const int lane = threadIdx.x & 31;
     const int grp = lane / RC, r = lane % RC;
-    const long long g0 = do_far ? node0[m] : 0;
-    const long long e0 = rowp[m], e1 = rowp[m + 1];
+    const long long g0 = node0[m];
     for (int r0 = 0; r0 < R; r0 += RC) {
         const int rr = r0 + r;
         const bool act = rr < R;
-        double2 aA = make_double2(0, 0), aP = aA, aN = aA;
-        if (do_far) {
-            for (int u = grp; u < S; u += G) {
-                const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
-                const long long g = g0 + ((long long)ui * Ny + uj) * Nz + uk;
-                const double2 w01 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u));
-                const double2 w23 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u) + 1);
-                if (act) {
-                    const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
-                    const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
-                    const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
-                    const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
-                    aA.x = fma(w01.x, f0.x, aA.x); aA.y = fma(w01.x, f0.y, aA.y);
-                    aA.x = fma(w01.y, f1.x, aA.x); aA.y = fma(w01.y, f1.y, aA.y);
-                    aA.x = fma(w23.x, f2.x, aA.x); aA.y = fma(w23.x, f2.y, aA.y);
-                    aP.x = fma(w23.y, f3.x, aP.x); aP.y = fma(w23.y, f3.y, aP.y);
-                }
-            }
-        }
-        if (do_near) {
-            for (long long e = e0 + grp; e < e1; e += G) {
-                const double2 z = __ldg(&val[e]);
-                const int n = __ldg(&col[e]);
-                if (act) {
-                    const double2 xv = __ldg(&x[(long long)n * R + rr]);
-                    aN.x = fma(z.x, xv.x, aN.x); aN.x = fma(-z.y, xv.y, aN.x);
-                    aN.y = fma(z.x, xv.y, aN.y); aN.y = fma(z.y, xv.x, aN.y);
-                }
+        double2 aA = make_double2(0, 0), aP = aA;
+        for (int u = grp; u < S; u += G) {
+            const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
+            const long long g = g0 + ((long long)ui * Ny + uj) * Nz + uk;
+            const double2 w01 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u));
+            const double2 w23 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u) + 1);
+            if (act) {
+                const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
+                const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
+                const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
+                const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
+                aA.x = fma(w01.x, f0.x, aA.x); aA.y = fma(w01.x, f0.y, aA.y);
+                aA.x = fma(w01.y, f1.x, aA.x); aA.y = fma(w01.y, f1.y, aA.y);
+                aA.x = fma(w23.x, f2.x, aA.x); aA.y = fma(w23.x, f2.y, aA.y);
+                aP.x = fma(w23.y, f3.x, aP.x); aP.y = fma(w23.y, f3.y, aP.y);
             }
         }
         // far = j k eta0 (aA - aP / k^2)
-        double2 f = make_double2(aA.x - aP.x * ik2, aA.y - aP.y * ik2);
-        double2 tot = make_double2(aN.x - keta * f.y, aN.y + keta * f.x);
+        const double2 f = make_double2(aA.x - aP.x * ik2, aA.y - aP.y * ik2);
+        double2 tot = make_double2(-keta * f.y, keta * f.x);
 #pragma unroll
         for (int off = RC; off < 32; off <<= 1) {
             const double2 t = shfl_xor2(tot, off);
             tot.x += t.x; tot.y += t.y;
         }
-        if (grp == 0 && act) y[m * R + rr] = tot;
+        if (grp == 0 && act) {
+            if (accumulate) {
+                const double2 o = y[m * R + rr];
+                tot.x += o.x; tot.y += o.y;
+            }
+            y[m * R + rr] = tot;
+        }
     }
 }
 
-void launch_interp_near(const aim_plan* p, const double2* Phi, const double2* x, double2* y, int R, bool far,
-                        bool near, cudaStream_t s) {
+// ------------------------------------------------------- H6 near SpMV
+// y[m,r] = sum_{n in near(m)} Z_corr[m,n] x[n,r]; warp per row, lanes over
+// (entry group, rhs), fixed-order shuffle reduction.
+template <int RC>
+__global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ rowp, const int32_t* __restrict__ col,
+                                                   const double2* __restrict__ val, const double2* __restrict__ x,
+                                                   long long N, int R, double2* __restrict__ y) {
+    constexpr int G = 32 / RC;
+    const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (m >= N) return;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / RC, r = lane % RC;
+    const long long e0 = rowp[m], e1 = rowp[m + 1];
+    for (int r0 = 0; r0 < R; r0 += RC) {
+        const int rr = r0 + r;
+        const bool act = rr < R;
+        double2 aN = make_double2(0, 0);
+        for (long long e = e0 + grp; e < e1; e += G) {
+            const double2 z = __ldcs(&val[e]);
+            const int n = __ldcs(&col[e]);
+            if (act) {
+                const double2 xv = __ldg(&x[(long long)n * R + rr]);
+                aN.x = fma(z.x, xv.x, aN.x); aN.x = fma(-z.y, xv.y, aN.x);
+                aN.y = fma(z.x, xv.y, aN.y); aN.y = fma(z.y, xv.x, aN.y);
+            }
+        }
+#pragma unroll
+        for (int off = RC; off < 32; off <<= 1) {
+            const double2 t = shfl_xor2(aN, off);
+            aN.x += t.x; aN.y += t.y;
+        }
+        if (grp == 0 && act) y[m * R + rr] = aN;
+    }
+}
+
+void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s) {
     const int rc = rhs_chunk(R);
     const unsigned grid = nblk(p->N * 32, 256);
     const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
-#define IN(MM, RR)                                                                                              \
-    if (p->M == MM && rc == RR) {                                                                               \
-        interp_near_kernel<MM, RR><<<grid, 256, 0, s>>>(Phi, p->W, p->node0, p->Ng, p->dims[1], p->dims[2],     \
-                                                        p->nrow, p->ncol, p->nval, x, p->N, R, keta, ik2, far,  \
-                                                        near, y);                                               \
-        note_launch("interp_near");                                                                             \
-        return;                                                                                                 \
+#define IN(MM, RR)                                                                                        \
+    if (p->M == MM && rc == RR) {                                                                         \
+        interp_kernel<MM, RR><<<grid, 256, 0, s>>>(Phi, p->W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, R, \
+                                                   keta, ik2, accumulate ? 1 : 0, y);                     \
+        note_launch("interp");                                                                            \
+        return;                                                                                           \
     }
 #define INM(MM) IN(MM, 1) IN(MM, 2) IN(MM, 4) IN(MM, 8) IN(MM, 16) IN(MM, 32)
     INM(1) INM(2) INM(3) INM(4) INM(5) INM(6)
 #undef INM
 #undef IN
     throw Error(AIM_E_ARG, "unsupported M");
+}
+
+void launch_near(const aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
+    const int rc = rhs_chunk(R);
+    const unsigned grid = nblk(p->N * 32, 256);
+    switch (rc) {
+#define NK(RR) case RR: near_kernel<RR><<<grid, 256, 0, s>>>(p->nrow, p->ncol, p->nval, x, p->N, R, y); break;
+        NK(1) NK(2) NK(4) NK(8) NK(16) NK(32)
+#undef NK
+    }
+    note_launch("near");
 }
 
 // ------------------------------------------------------------ plane wave
@@ -214,66 +246,95 @@ void ensure_workspace(aim_plan* p, int R) {
     p->release(p->Q);
     p->release(p->W1);
     p->release(p->W2);
+    p->W2 = nullptr;
     const long long Nx = p->dims[0], Ny = p->dims[1], Nz = p->dims[2];
     const long long Px = p->pads[0], Py = p->pads[1];
     p->Q = p->alloc<double2>(4 * Nx * Ny * Nz * R);
     p->W1 = p->alloc<double2>(4 * Px * Ny * Nz * R);
-    p->W2 = p->alloc<double2>(4 * Px * Py * Nz * R);
+    if (!p->planar) p->W2 = p->alloc<double2>(4 * Px * Py * Nz * R);
     p->ws_nrhs = R;
 }
 
-void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s) {
+struct Prof {
+    aim_plan* p;
+    long long base = -1;
+    explicit Prof(aim_plan* pp) : p(pp) {
+        if (!p || !p->prof) return;
+        while (p->ev_pool.size() < p->ev_used + kProfEvents) {
+            cudaEvent_t e;
+            AIM_CUDA(cudaEventCreate(&e));
+            p->ev_pool.push_back(e);
+        }
+        base = (long long)p->ev_used;
+        p->ev_used += kProfEvents;
+        p->prof_count++;
+    }
+    void mark(int slot, cudaStream_t s) {
+        if (base >= 0) AIM_CUDA(cudaEventRecord(p->ev_pool[base + slot], s));
+    }
+};
+
+static void convolve_impl(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s, Prof* pr) {
     const long long Nx = p->dims[0], Ny = p->dims[1], Nz = p->dims[2];
     const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2];
     FftPass f{};
-    // A: x forward, [4][Nx -> Px][Ny Nz R]
+    // x forward, [4][Nx -> Px][Ny Nz R]
     f.in = Q; f.out = p->W1; f.outer = 4; f.Lin = (int)Nx; f.Lout = Px; f.inner = Ny * Nz * R;
     f.mode = 0; f.ax = p->ax[0]; f.TO = f.TI = 0;
     launch_fft_pass(f, s);
-    prof_mark(p, s);
-    // B1: y forward, [4 Px][Ny -> Py][Nz R]
-    f.in = p->W1; f.out = p->W2; f.outer = 4LL * Px; f.Lin = (int)Ny; f.Lout = Py; f.inner = Nz * R;
-    f.mode = 0; f.ax = p->ax[1]; f.TO = f.TI = 0;
-    launch_fft_pass(f, s);
-    prof_mark(p, s);
-    // B2: z turnaround in place, [4 Px Py][Nz -> Pz -> Nz][R]
-    f.in = p->W2; f.out = p->W2; f.outer = 4LL * Px * Py; f.Lin = (int)Nz; f.Lout = (int)Nz; f.inner = R;
-    f.mode = 2; f.ax = p->ax[2]; f.TO = f.TI = 0;
-    f.spec = p->spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
-    launch_fft_pass(f, s);
-    prof_mark(p, s);
-    // B3: y inverse, [4 Px][Py -> Ny][Nz R]
-    f.in = p->W2; f.out = p->W1; f.outer = 4LL * Px; f.Lin = Py; f.Lout = (int)Ny; f.inner = Nz * R;
-    f.mode = 1; f.ax = p->ax[1]; f.TO = f.TI = 0;
-    launch_fft_pass(f, s);
-    prof_mark(p, s);
-    // C: x inverse, [4][Px -> Nx][Ny Nz R]
+    if (pr) pr->mark(2, s);
+    if (p->planar) {
+        PlanarPass q{};
+        q.W = p->W1; q.Px = Px; q.Ny = (int)Ny; q.Nz = (int)Nz; q.R = R; q.PyH = Py / 2 + 1; q.ay = p->ax[1];
+        q.spec = p->spec;
+        launch_planar_yz(q, s);
+    } else {
+        // y forward, [4 Px][Ny -> Py][Nz R]
+        f.in = p->W1; f.out = p->W2; f.outer = 4LL * Px; f.Lin = (int)Ny; f.Lout = Py; f.inner = Nz * R;
+        f.mode = 0; f.ax = p->ax[1]; f.TO = f.TI = 0;
+        launch_fft_pass(f, s);
+        // z turnaround in place, [4 Px Py][Nz -> Pz -> Nz][R]
+        f.in = p->W2; f.out = p->W2; f.outer = 4LL * Px * Py; f.Lin = (int)Nz; f.Lout = (int)Nz; f.inner = R;
+        f.mode = 2; f.ax = p->ax[2]; f.TO = f.TI = 0;
+        f.spec = p->spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
+        launch_fft_pass(f, s);
+        // y inverse, [4 Px][Py -> Ny][Nz R]
+        f.in = p->W2; f.out = p->W1; f.outer = 4LL * Px; f.Lin = Py; f.Lout = (int)Ny; f.inner = Nz * R;
+        f.mode = 1; f.ax = p->ax[1]; f.TO = f.TI = 0;
+        launch_fft_pass(f, s);
+    }
+    if (pr) pr->mark(3, s);
+    // x inverse, [4][Px -> Nx][Ny Nz R]
     f.in = p->W1; f.out = Phi; f.outer = 4; f.Lin = Px; f.Lout = (int)Nx; f.inner = Ny * Nz * R;
     f.mode = 1; f.ax = p->ax[0]; f.TO = f.TI = 0;
     launch_fft_pass(f, s);
-    prof_mark(p, s);
+    if (pr) pr->mark(4, s);
 }
 
-void prof_mark(aim_plan* p, cudaStream_t s) {
-    if (!p->prof) return;
-    if (p->ev_used == p->ev_pool.size()) {
-        cudaEvent_t e;
-        AIM_CUDA(cudaEventCreate(&e));
-        p->ev_pool.push_back(e);
-    }
-    AIM_CUDA(cudaEventRecord(p->ev_pool[p->ev_used++], s));
+void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s) {
+    convolve_impl(p, Q, Phi, R, s, nullptr);
 }
 
+// y = Z_eq x.  The near-field SpMV (memory bound) runs on the plan's side
+// stream concurrently with the projection + FFT passes (FP64-ALU heavy);
+// the interpolation adds the far field to its result.
 void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
     ensure_workspace(p, R);
-    const int prof = p->prof;   // stages of one matvec are profiled together
-    prof_mark(p, s);
+    Prof pr(p);
+    pr.mark(0, s);
+    AIM_CUDA(cudaEventRecord(p->ev_x, s));
+    AIM_CUDA(cudaStreamWaitEvent(p->side, p->ev_x, 0));
+    pr.mark(7, p->side);
+    launch_near(p, x, y, R, p->side);
+    pr.mark(8, p->side);
+    AIM_CUDA(cudaEventRecord(p->ev_n, p->side));
     launch_project(p, x, p->Q, R, s);
-    prof_mark(p, s);
-    convolve(p, p->Q, p->Q, R, s);
-    launch_interp_near(p, p->Q, x, y, R, true, true, s);
-    prof_mark(p, s);
-    if (prof) p->prof_count++;
+    pr.mark(1, s);
+    convolve_impl(p, p->Q, p->Q, R, s, &pr);
+    AIM_CUDA(cudaStreamWaitEvent(s, p->ev_n, 0));
+    pr.mark(5, s);
+    launch_interp(p, p->Q, y, R, true, s);
+    pr.mark(6, s);
 }
 
 }  // namespace aim

@@ -561,50 +561,64 @@ void build_near_values(aim_plan* p, cudaStream_t s) {
 }
 
 // ------------------------------------------------------ S3 Green spectrum
-__global__ void kernel_sample(double2* K, int Px, int Py, int Pz, double h, double k) {
+// K[x][y][z] = G(h sqrt(xb^2 + yb^2 + zb^2)), xb = min(x, Px - x) (min image,
+// D12) for z < Lz; zb = min(z, Pz - z) in 3-D mode, zb = z (the |dz| of the
+// direct z convolution) in planar mode.
+__global__ void kernel_sample(double2* K, int Px, int Py, int Lz, int Pz, int planar, double h, double k) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long tot = (long long)Px * Py * Pz;
+    const long long tot = (long long)Px * Py * Lz;
     if (i >= tot) return;
-    const int x = (int)(i / ((long long)Py * Pz)), y = (int)((i / Pz) % Py), z = (int)(i % Pz);
-    const int ix = min(x, Px - x), iy = min(y, Py - y), iz = min(z, Pz - z);
+    const int x = (int)(i / ((long long)Py * Lz)), y = (int)((i / Lz) % Py), z = (int)(i % Lz);
+    const int ix = min(x, Px - x), iy = min(y, Py - y), iz = planar ? z : min(z, Pz - z);
     const double q = (double)ix * ix + (double)iy * iy + (double)iz * iz;
     K[i] = q == 0 ? make_double2(0, 0) : green_full(h * sqrt(q), k);
 }
 
-__global__ void spectrum_octant(const double2* F, double2* spec, int Px, int Py, int Pz, double scale) {
-    const int PxH = Px / 2 + 1, PyH = Py / 2 + 1, PzH = Pz / 2 + 1;
+// spec[(x PyH + y) Lo + z] = F[x][y][z] * scale for x <= Px/2, y <= Py/2, z < Lo
+__global__ void spectrum_octant(const double2* F, double2* spec, int Px, int Py, int Lz, int Lo, double scale) {
+    const int PxH = Px / 2 + 1, PyH = Py / 2 + 1;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (long long)PxH * PyH * PzH) return;
-    const int x = (int)(i / ((long long)PyH * PzH)), y = (int)((i / PzH) % PyH), z = (int)(i % PzH);
-    const double2 v = F[((long long)x * Py + y) * Pz + z];
+    if (i >= (long long)PxH * PyH * Lo) return;
+    const int x = (int)(i / ((long long)PyH * Lo)), y = (int)((i / Lo) % PyH), z = (int)(i % Lo);
+    const double2 v = F[((long long)x * Py + y) * Lz + z];
     spec[i] = make_double2(v.x * scale, v.y * scale);
 }
 
 void build_green_spectrum(aim_plan* p, cudaStream_t s) {
-    const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2];
-    const long long tot = (long long)Px * Py * Pz;
+    const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2], Nz = p->dims[2];
+    const int Lz = p->planar ? Nz : Pz;
+    const long long tot = (long long)Px * Py * Lz;
     double2 *A = nullptr, *B = nullptr;
     AIM_CUDA(cudaMalloc(&A, sizeof(double2) * tot));
     AIM_CUDA(cudaMalloc(&B, sizeof(double2) * tot));
-    kernel_sample<<<nblk(tot, 256), 256, 0, s>>>(A, Px, Py, Pz, p->h, p->k);
+    kernel_sample<<<nblk(tot, 256), 256, 0, s>>>(A, Px, Py, Lz, Pz, p->planar, p->h, p->k);
     note_launch("kernel_sample");
     FftPass f{};
     f.mode = 0;
-    // x: [1][Px][Py Pz]
-    f.in = A; f.out = B; f.outer = 1; f.Lin = f.Lout = Px; f.inner = (long long)Py * Pz; f.ax = p->ax[0];
+    // x: [1][Px][Py Lz]
+    f.in = A; f.out = B; f.outer = 1; f.Lin = f.Lout = Px; f.inner = (long long)Py * Lz; f.ax = p->ax[0];
     f.TO = f.TI = 0;
     launch_fft_pass(f, s);
-    // y: [Px][Py][Pz]
-    f.in = B; f.out = A; f.outer = Px; f.Lin = f.Lout = Py; f.inner = Pz; f.ax = p->ax[1];
+    // y: [Px][Py][Lz]
+    f.in = B; f.out = A; f.outer = Px; f.Lin = f.Lout = Py; f.inner = Lz; f.ax = p->ax[1];
     f.TO = f.TI = 0;
     launch_fft_pass(f, s);
-    // z: [Px Py][Pz][1]
-    f.in = A; f.out = B; f.outer = (long long)Px * Py; f.Lin = f.Lout = Pz; f.inner = 1; f.ax = p->ax[2];
-    f.TO = f.TI = 0;
-    launch_fft_pass(f, s);
-    const long long oct = (long long)(Px / 2 + 1) * (Py / 2 + 1) * (Pz / 2 + 1);
+    double2* F = A;
+    double scale = 1.0 / ((double)Px * Py);
+    int Lo = Nz;
+    if (!p->planar) {
+        // z: [Px Py][Pz][1]
+        f.in = A; f.out = B; f.outer = (long long)Px * Py; f.Lin = f.Lout = Pz; f.inner = 1; f.ax = p->ax[2];
+        f.TO = f.TI = 0;
+        launch_fft_pass(f, s);
+        F = B;
+        scale /= (double)Pz;
+        Lo = Pz / 2 + 1;
+    }
+    const long long oct = (long long)(Px / 2 + 1) * (Py / 2 + 1) * Lo;
     p->spec = p->alloc<double2>(oct);
-    spectrum_octant<<<nblk(oct, 256), 256, 0, s>>>(B, p->spec, Px, Py, Pz, 1.0 / ((double)tot));
+    p->spec_len = oct;
+    spectrum_octant<<<nblk(oct, 256), 256, 0, s>>>(F, p->spec, Px, Py, Lz, Lo, scale);
     note_launch("spectrum_octant");
     AIM_CUDA(cudaStreamSynchronize(s));
     cudaFree(A);

@@ -61,12 +61,20 @@ def test_plan_tables(name):
     assert np.abs(val - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("name", ["c1", "t_vol"])
+@pytest.mark.parametrize("name", ["c1", "t_vol", "t_m3"])
 def test_green_spectrum(name):
+    """3-D mode: octant of FFT3(K)/(PxPyPz); planar mode: FFT over x, y of
+    K(x, y, dz), dz < Nz, divided by PxPy (numpy FFT of the oracle's samples)."""
     G, O = gpu_plan(name), oracle_plan(name)
     pads = G.info["fft_dims"]
-    F = np.fft.fftn(O.kernel_samples(pads)) / np.prod(pads)
-    oct_ = F[: pads[0] // 2 + 1, : pads[1] // 2 + 1, : pads[2] // 2 + 1]
+    if G.info["conv_mode"] == 1:
+        Nz = G.info["grid_dims"][2]
+        K = O.kernel_samples((pads[0], pads[1], 2 * Nz))[:, :, :Nz]
+        F = np.fft.fft2(K, axes=(0, 1)) / (pads[0] * pads[1])
+        oct_ = F[: pads[0] // 2 + 1, : pads[1] // 2 + 1, :]
+    else:
+        F = np.fft.fftn(O.kernel_samples(pads)) / np.prod(pads)
+        oct_ = F[: pads[0] // 2 + 1, : pads[1] // 2 + 1, : pads[2] // 2 + 1]
     g = G.export("green")
     assert np.abs(g - oct_).max() <= 1e-13 * np.abs(oct_).max()
 
@@ -114,6 +122,11 @@ def test_matvec_nrhs_and_determinism(nrhs):
     # end-to-end host path
     yh = G.matvec_host(x)
     assert np.array_equal(yh, y1)
+
+
+def test_conv_modes_used():
+    assert gpu_plan("c1").info["conv_mode"] == 1      # planar: Nz = 7
+    assert gpu_plan("t_vol").info["conv_mode"] in (0, 1)
 
 
 def test_matvec_c2_full_size_sampled_rows():
