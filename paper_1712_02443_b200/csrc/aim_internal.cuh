@@ -42,6 +42,7 @@ struct FftAxis {
     int P = 1;                       // transform length
     int nst = 0;                     // number of Stockham stages
     int radix[kMaxStages] = {0};     // radices, product == P
+    unsigned long long nsM[kMaxStages] = {0};  // ceil(2^40 / Ns) of each stage (fast divide)
     double2* tw = nullptr;           // device twiddles exp(-2 pi i e / P), e in [0,P)
 };
 

@@ -86,18 +86,36 @@ __device__ __forceinline__ void dft(double2* a, double sign) {
     }
 }
 
-// One Stockham stage of radix R over NL lines of length P, src -> dst
-// (ping-pong buffers; each thread loops over butterflies with R registers).
+// n / d for 0 <= n < 2^20 via M = ceil(2^40 / d) (exact, no integer divide)
+__device__ __forceinline__ int fdiv(int n, unsigned long long M) {
+    return (int)(((unsigned long long)(unsigned)n * M) >> 40);
+}
+
+// Thread layout of a CTA working on NL lines: line l = tid % NL, and the
+// butterfly / row index advances from js in steps of JS = blockDim / NL.
+struct LineMap {
+    int l, js, JS;
+    bool active;
+    __device__ __forceinline__ explicit LineMap(int NL) {
+        JS = blockDim.x / NL;
+        l = threadIdx.x % NL;
+        js = threadIdx.x / NL;
+        active = js < JS;
+    }
+};
+
+// One Stockham stage of radix R over NL lines of length P, src -> dst.
 template <int R>
 __device__ __forceinline__ void stage(const double2* __restrict__ src, double2* __restrict__ dst,
-                                      const double2* __restrict__ tw, int P, int NL, int Ns, double sign) {
+                                      const double2* __restrict__ tw, int P, int NL, int Ns,
+                                      unsigned long long nsM, double sign, const LineMap& lm) {
+    if (!lm.active) return;
     const int B = P / R;
     const int stride = P / (Ns * R);
-    const int total = NL * B;
-    for (int b = threadIdx.x; b < total; b += blockDim.x) {
-        const int l = b % NL;
-        const int j = b / NL;
-        const int k = j % Ns;
+    const int l = lm.l;
+    for (int j = lm.js; j < B; j += lm.JS) {
+        const int jd = fdiv(j, nsM);
+        const int k = j - jd * Ns;
         double2 a[R];
 #pragma unroll
         for (int t = 0; t < R; ++t) a[t] = src[(j + t * B) * NL + l];
@@ -110,7 +128,7 @@ __device__ __forceinline__ void stage(const double2* __restrict__ src, double2* 
             }
         }
         dft<R>(a, sign);
-        const int base = (j / Ns) * Ns * R + k;
+        const int base = jd * Ns * R + k;
 #pragma unroll
         for (int u = 0; u < R; ++u) dst[(base + u * Ns) * NL + l] = a[u];
     }
@@ -119,17 +137,18 @@ __device__ __forceinline__ void stage(const double2* __restrict__ src, double2* 
 // Full transform of NL lines (sign -1 forward, +1 inverse, unscaled) between
 // the two buffers; returns the buffer holding the result.
 __device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const double2* tw, const FftAxis& ax, int NL,
-                                              double sign) {
+                                              double sign, const LineMap& lm) {
     int Ns = 1;
     double2* src = b0;
     double2* dst = b1;
     for (int s = 0; s < ax.nst; ++s) {
+        const unsigned long long M = ax.nsM[s];
         switch (ax.radix[s]) {
-            case 2: stage<2>(src, dst, tw, ax.P, NL, Ns, sign); break;
-            case 3: stage<3>(src, dst, tw, ax.P, NL, Ns, sign); break;
-            case 4: stage<4>(src, dst, tw, ax.P, NL, Ns, sign); break;
-            case 5: stage<5>(src, dst, tw, ax.P, NL, Ns, sign); break;
-            case 7: stage<7>(src, dst, tw, ax.P, NL, Ns, sign); break;
+            case 2: stage<2>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
+            case 3: stage<3>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
+            case 4: stage<4>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
+            case 5: stage<5>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
+            case 7: stage<7>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
         }
         __syncthreads();
         Ns *= ax.radix[s];

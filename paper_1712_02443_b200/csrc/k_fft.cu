@@ -35,55 +35,57 @@ __global__ void __launch_bounds__(256) fft_pass_kernel(FftPass p) {
     const long long i0 = (long long)(blockIdx.x % tilesI) * TI;
     const int to_n = (int)min((long long)TO, p.outer - o0);
     const int ti_n = (int)min((long long)TI, p.inner - i0);
+    const LineMap lm(NL);
+    const int o = lm.l / TI, i = lm.l - (lm.l / TI) * TI;
+    const bool live = lm.active && o < to_n && i < ti_n;
+    const double2* src = p.in + (o0 + o) * p.Lin * p.inner + i0 + i;
 
     for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = p.ax.tw[e];
-    // tile load with fused zero padding: element (o, j, i), i fastest
-    const int tot = TO * P * TI;
-    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-        const int i = idx % TI;
-        const int j = (idx / TI) % P;
-        const int o = idx / (TI * P);
-        double2 v = make_double2(0.0, 0.0);
-        if (o < to_n && i < ti_n && j < p.Lin) v = __ldcs(&p.in[((o0 + o) * p.Lin + j) * p.inner + i0 + i]);
-        buf[j * NL + o * TI + i] = v;
+    // tile load with fused zero padding: line l = (o, i), rows j
+    if (lm.active) {
+        int j = lm.js;
+        for (; j + 3 * lm.JS < p.Lin; j += 4 * lm.JS) {
+            double2 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                v[q] = live ? __ldcs(src + (long long)(j + q * lm.JS) * p.inner) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) buf[(j + q * lm.JS) * NL + lm.l] = v[q];
+        }
+        for (; j < P; j += lm.JS)
+            buf[j * NL + lm.l] = (live && j < p.Lin) ? __ldcs(src + (long long)j * p.inner) : make_double2(0.0, 0.0);
     }
     __syncthreads();
 
     double2* res;
     if (p.mode == 1) {
-        res = fft_lines(buf, alt, tw, p.ax, NL, +1.0);
+        res = fft_lines(buf, alt, tw, p.ax, NL, +1.0, lm);
     } else {
-        res = fft_lines(buf, alt, tw, p.ax, NL, -1.0);
+        res = fft_lines(buf, alt, tw, p.ax, NL, -1.0, lm);
         if (p.mode == 2) {
             // x spectrum: line (o, i) belongs to outer og = (c Px + kx) Py + ky; kz = j
-            for (int idx = threadIdx.x; idx < NL * P; idx += blockDim.x) {
-                const int l = idx % NL;
-                const int j = idx / NL;
-                const int o = l / TI;
+            if (lm.active) {
                 const long long og = o0 + min(o, to_n - 1);
                 const int ky = (int)(og % p.Py);
                 const int kx = (int)((og / p.Py) % p.Px);
-                const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky), az = min(j, P - j);
-                const double2 g = __ldg(&p.spec[((long long)ax_ * p.PyH + ay) * p.PzH + az]);
-                res[idx] = cmul(res[idx], g);
+                const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
+                const double2* g = p.spec + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                for (int j = lm.js; j < P; j += lm.JS) res[j * NL + lm.l] = cmul(res[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
             }
             __syncthreads();
-            res = fft_lines(res, res == buf ? alt : buf, tw, p.ax, NL, +1.0);
+            res = fft_lines(res, res == buf ? alt : buf, tw, p.ax, NL, +1.0, lm);
         }
     }
     // tile store with fused pruning
-    const int tot_out = TO * p.Lout * TI;
-    for (int idx = threadIdx.x; idx < tot_out; idx += blockDim.x) {
-        const int i = idx % TI;
-        const int j = (idx / TI) % p.Lout;
-        const int o = idx / (TI * p.Lout);
-        if (o < to_n && i < ti_n) __stcs(&p.out[((o0 + o) * p.Lout + j) * p.inner + i0 + i], res[j * NL + o * TI + i]);
+    if (live) {
+        double2* dst = p.out + (o0 + o) * p.Lout * p.inner + i0 + i;
+        for (int j = lm.js; j < p.Lout; j += lm.JS) __stcs(dst + (long long)j * p.inner, res[j * NL + lm.l]);
     }
 }
 
 // ------------------------------------------------------------ planar y/z
 // W[4][Px][Ny][Nz][R] in place.  CTA = (plane c*Px+kx, rhs chunk r0..r0+RC).
-// smem buf [Py][Nz*RC] (y lines indexed by (z, rl)).
+// smem [Py][Nz*RC] (y lines indexed by l = z*RC + rl).
 template <int NZ>
 __global__ void __launch_bounds__(256, 2) planar_yz_kernel(PlanarPass p) {
     extern __shared__ double2 sm[];
@@ -98,54 +100,54 @@ __global__ void __launch_bounds__(256, 2) planar_yz_kernel(PlanarPass p) {
     const int r0 = (int)(blockIdx.x % nchunk) * RC;
     const int rc_n = min(RC, p.R - r0);
     const int kx = (int)(plane % p.Px);
-    double2* W = p.W + plane * (long long)p.Ny * NZ * p.R;
+    const LineMap lm(NL);
+    const int z = lm.l / RC, rl = lm.l - (lm.l / RC) * RC;
+    const bool live = lm.active && rl < rc_n;
+    double2* W = p.W + plane * (long long)p.Ny * NZ * p.R + z * p.R + r0 + rl;   // + y * NZ * R
+    const long long ystride = (long long)NZ * p.R;
 
     for (int e = threadIdx.x; e < Py; e += blockDim.x) tw[e] = p.ay.tw[e];
-    const int tot = Py * NL;
-    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-        const int rl = idx % RC;
-        const int z = (idx / RC) % NZ;
-        const int y = idx / NL;
-        double2 v = make_double2(0.0, 0.0);
-        if (y < p.Ny && rl < rc_n) v = __ldcs(&W[((long long)y * NZ + z) * p.R + r0 + rl]);
-        buf[idx] = v;
+    if (lm.active) {
+        int y = lm.js;
+        for (; y + 3 * lm.JS < p.Ny; y += 4 * lm.JS) {
+            double2 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = live ? __ldcs(W + (y + q * lm.JS) * ystride) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) buf[(y + q * lm.JS) * NL + lm.l] = v[q];
+        }
+        for (; y < Py; y += lm.JS)
+            buf[y * NL + lm.l] = (live && y < p.Ny) ? __ldcs(W + y * ystride) : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    double2* res = fft_lines(buf, alt, tw, p.ay, NL, -1.0);
+    double2* res = fft_lines(buf, alt, tw, p.ay, NL, -1.0, lm);
     double2* oth = res == buf ? alt : buf;
     // z: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for every (ky, rl)
     const int ax_ = min(kx, p.Px - kx);
     const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
     for (int line = threadIdx.x; line < Py * RC; line += blockDim.x) {
-        const int ky = line / RC, rl = line % RC;
+        const int ky = line / RC, rr = line - (line / RC) * RC;
         const int ay = min(ky, Py - ky);
         const double2* g = G2 + (long long)ay * NZ;
-        double2 gk[NZ], in[NZ];
+        double2 in[NZ];
 #pragma unroll
-        for (int d = 0; d < NZ; ++d) gk[d] = __ldg(&g[d]);
+        for (int zz = 0; zz < NZ; ++zz) in[zz] = res[ky * NL + zz * RC + rr];
 #pragma unroll
-        for (int z = 0; z < NZ; ++z) in[z] = res[ky * NL + z * RC + rl];
-#pragma unroll
-        for (int z = 0; z < NZ; ++z) {
+        for (int zz = 0; zz < NZ; ++zz) {
             double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
             for (int zp = 0; zp < NZ; ++zp) {
-                const double2 gg = gk[z > zp ? z - zp : zp - z];
+                const double2 gg = __ldg(&g[zz > zp ? zz - zp : zp - zz]);
                 acc.x = fma(gg.x, in[zp].x, fma(-gg.y, in[zp].y, acc.x));
                 acc.y = fma(gg.x, in[zp].y, fma(gg.y, in[zp].x, acc.y));
             }
-            res[ky * NL + z * RC + rl] = acc;
+            res[ky * NL + zz * RC + rr] = acc;
         }
     }
     __syncthreads();
-    res = fft_lines(res, oth, tw, p.ay, NL, +1.0);
-    const int tout = p.Ny * NL;
-    for (int idx = threadIdx.x; idx < tout; idx += blockDim.x) {
-        const int rl = idx % RC;
-        const int z = (idx / RC) % NZ;
-        const int y = idx / NL;
-        if (rl < rc_n) __stcs(&W[((long long)y * NZ + z) * p.R + r0 + rl], res[idx]);
-    }
+    res = fft_lines(res, oth, tw, p.ay, NL, +1.0, lm);
+    if (live)
+        for (int y = lm.js; y < p.Ny; y += lm.JS) __stcs(W + y * ystride, res[y * NL + lm.l]);
 }
 
 // ------------------------------------------------------------------- host
@@ -168,6 +170,11 @@ void make_fft_axis(int P, FftAxis& ax) {
     for (int f : {3, 5, 7})
         while (r % f == 0) { ax.radix[ax.nst++] = f; r /= f; }
     if (r != 1 || ax.nst > kMaxStages) throw Error(AIM_E_GRID, "FFT size not 7-smooth");
+    long long Ns = 1;
+    for (int st = 0; st < ax.nst; ++st) {
+        ax.nsM[st] = ((1ULL << 40) + (unsigned long long)Ns - 1) / (unsigned long long)Ns;
+        Ns *= ax.radix[st];
+    }
     std::vector<double2> h(P);
     for (int e = 0; e < P; ++e) {
         long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)e / (long double)P;
@@ -185,10 +192,13 @@ void launch_fft_pass(const FftPass& p0, cudaStream_t s) {
     const int cap = std::max(fft_tile_capacity(), P);
     const int nl = std::max(1, cap / P);
     if (p.TI <= 0) {
-        long long ti = std::min<long long>(p.inner, nl);
-        if (p.inner > nl && ti >= 8) ti = (ti / 8) * 8;
+        // TI: power of two (coalesced rows of TI*16 bytes); TO fills the tile
+        long long ti = 1;
+        while (ti * 2 <= std::min<long long>(p.inner, nl) && ti * 2 <= kFftThreads) ti *= 2;
+        if (ti < p.inner && ti * 2 <= nl && ti * 2 <= kFftThreads) ti *= 2;  // one ragged tile is cheaper than many
         p.TI = (int)ti;
         p.TO = (int)std::max<long long>(1, std::min<long long>(p.outer, nl / p.TI));
+        p.TO = std::min(p.TO, kFftThreads / p.TI);
     }
     const long long tilesI = (p.inner + p.TI - 1) / p.TI;
     const long long tilesO = (p.outer + p.TO - 1) / p.TO;
@@ -211,7 +221,7 @@ void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
     PlanarPass p = p0;
     const int Py = p.ay.P;
     const int cap = 2 * fft_tile_capacity();
-    p.RC = std::max(1, std::min(p.R, cap / (Py * p.Nz)));
+    p.RC = std::max(1, std::min({p.R, cap / (Py * p.Nz), kFftThreads / p.Nz}));
     const long long nchunk = (p.R + p.RC - 1) / p.RC;
     const long long grid = 4LL * p.Px * nchunk;
     const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py);

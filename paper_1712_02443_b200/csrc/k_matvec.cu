@@ -23,6 +23,10 @@ __device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
 }
 
 // ------------------------------------------------------------ H1 projection
+// Warp per grid node.  Entries are consumed in batches of 32: every lane first
+// loads one entry's index and weights (coalesced / independent), then the
+// rhs lanes gather x for the batch (broadcast by shuffles), so each warp keeps
+// many independent loads in flight.
 template <int M, int RC>
 __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict__ prow,
                                                       const int32_t* __restrict__ pent,
@@ -35,20 +39,44 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
     const int lane = threadIdx.x & 31;
     const int grp = lane / RC, r = lane % RC;
     const int e0 = prow[g], e1 = prow[g + 1];
+    const double2* W2 = reinterpret_cast<const double2*>(W);
     for (int r0 = 0; r0 < R; r0 += RC) {
         const int rr = r0 + r;
         const bool act = rr < R;
         double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
-        for (int e = e0 + grp; e < e1; e += G) {
-            const int ent = __ldg(&pent[e]);
-            const int n = ent / S;
-            const double2 w01 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (long long)ent);
-            const double2 w23 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (long long)ent + 1);
-            const double2 xv = act ? __ldg(&x[(long long)n * R + rr]) : make_double2(0, 0);
-            a0.x = fma(w01.x, xv.x, a0.x); a0.y = fma(w01.x, xv.y, a0.y);
-            a1.x = fma(w01.y, xv.x, a1.x); a1.y = fma(w01.y, xv.y, a1.y);
-            a2.x = fma(w23.x, xv.x, a2.x); a2.y = fma(w23.x, xv.y, a2.y);
-            a3.x = fma(w23.y, xv.x, a3.x); a3.y = fma(w23.y, xv.y, a3.y);
+        for (int b = e0; b < e1; b += 32) {
+            const int cnt = min(32, e1 - b);
+            int n_l = 0;
+            double2 w01 = make_double2(0, 0), w23 = w01;
+            if (lane < cnt) {
+                const int ent = __ldg(&pent[b + lane]);
+                n_l = ent / S;
+                w01 = __ldcs(W2 + 2 * (long long)ent);
+                w23 = __ldcs(W2 + 2 * (long long)ent + 1);
+            }
+            if (RC == 1) {
+                if (lane < cnt) {
+                    const double2 xv = __ldg(&x[(long long)n_l * R + rr]);
+                    a0.x = fma(w01.x, xv.x, a0.x); a0.y = fma(w01.x, xv.y, a0.y);
+                    a1.x = fma(w01.y, xv.x, a1.x); a1.y = fma(w01.y, xv.y, a1.y);
+                    a2.x = fma(w23.x, xv.x, a2.x); a2.y = fma(w23.x, xv.y, a2.y);
+                    a3.x = fma(w23.y, xv.x, a3.x); a3.y = fma(w23.y, xv.y, a3.y);
+                }
+            } else {
+#pragma unroll 4
+                for (int t = grp; t < 32; t += G) {
+                    const int n = __shfl_sync(0xffffffffu, n_l, t);
+                    const double wx = __shfl_sync(0xffffffffu, w01.x, t), wy = __shfl_sync(0xffffffffu, w01.y, t);
+                    const double wz = __shfl_sync(0xffffffffu, w23.x, t), wp = __shfl_sync(0xffffffffu, w23.y, t);
+                    if (t < cnt && act) {
+                        const double2 xv = __ldg(&x[(long long)n * R + rr]);
+                        a0.x = fma(wx, xv.x, a0.x); a0.y = fma(wx, xv.y, a0.y);
+                        a1.x = fma(wy, xv.x, a1.x); a1.y = fma(wy, xv.y, a1.y);
+                        a2.x = fma(wz, xv.x, a2.x); a2.y = fma(wz, xv.y, a2.y);
+                        a3.x = fma(wp, xv.x, a3.x); a3.y = fma(wp, xv.y, a3.y);
+                    }
+                }
+            }
         }
 #pragma unroll
         for (int off = RC; off < 32; off <<= 1) {
@@ -61,13 +89,13 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
         if (RC == 1) {
             if (lane < 4) {
                 const double2 v = lane == 0 ? a0 : lane == 1 ? a1 : lane == 2 ? a2 : a3;
-                Q[((long long)lane * Ng + g) * R + rr] = v;
+                __stcs(&Q[((long long)lane * Ng + g) * R + rr], v);
             }
         } else if (grp == 0 && act) {
-            Q[(0 * Ng + g) * R + rr] = a0;
-            Q[(1 * Ng + g) * R + rr] = a1;
-            Q[(2 * Ng + g) * R + rr] = a2;
-            Q[(3 * Ng + g) * R + rr] = a3;
+            __stcs(&Q[(0 * Ng + g) * R + rr], a0);
+            __stcs(&Q[(1 * Ng + g) * R + rr], a1);
+            __stcs(&Q[(2 * Ng + g) * R + rr], a2);
+            __stcs(&Q[(3 * Ng + g) * R + rr], a3);
         }
     }
 }
@@ -92,6 +120,8 @@ void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cuda
 
 // ------------------------------------------------------ H5 interpolation
 // y[m,r] (+)= j k eta0 [sum_xyz sum_u w_{m,u} Phi[u,r] - k^-2 sum_u w^phi_{m,u} Phi^phi[u,r]]
+// Warp per RWG row: lane u first loads w_{m,u} (contiguous), then the rhs
+// lanes gather the stencil's potentials (weights broadcast by shuffles).
 template <int M, int RC>
 __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__ Phi, const double* __restrict__ W,
                                                      const int32_t* __restrict__ node0, long long Ng, int Ny, int Nz,
@@ -104,24 +134,50 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
     const int lane = threadIdx.x & 31;
     const int grp = lane / RC, r = lane % RC;
     const long long g0 = node0[m];
+    const double2* W2 = reinterpret_cast<const double2*>(W) + 2 * m * S;
     for (int r0 = 0; r0 < R; r0 += RC) {
         const int rr = r0 + r;
         const bool act = rr < R;
         double2 aA = make_double2(0, 0), aP = aA;
-        for (int u = grp; u < S; u += G) {
-            const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
-            const long long g = g0 + ((long long)ui * Ny + uj) * Nz + uk;
-            const double2 w01 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u));
-            const double2 w23 = __ldg(reinterpret_cast<const double2*>(W) + 2 * (m * S + u) + 1);
-            if (act) {
-                const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
-                const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
-                const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
-                const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
-                aA.x = fma(w01.x, f0.x, aA.x); aA.y = fma(w01.x, f0.y, aA.y);
-                aA.x = fma(w01.y, f1.x, aA.x); aA.y = fma(w01.y, f1.y, aA.y);
-                aA.x = fma(w23.x, f2.x, aA.x); aA.y = fma(w23.x, f2.y, aA.y);
-                aP.x = fma(w23.y, f3.x, aP.x); aP.y = fma(w23.y, f3.y, aP.y);
+        for (int ub = 0; ub < S; ub += 32) {
+            const int u_l = ub + lane;
+            double2 w01 = make_double2(0, 0), w23 = w01;
+            int g_l = 0;
+            if (u_l < S) {
+                w01 = __ldcs(W2 + 2 * u_l);
+                w23 = __ldcs(W2 + 2 * u_l + 1);
+                const int ui = u_l / (M1 * M1), uj = (u_l / M1) % M1, uk = u_l % M1;
+                g_l = (int)(g0 + ((long long)ui * Ny + uj) * Nz + uk);
+            }
+            if (RC == 1) {
+                if (u_l < S) {
+                    const double2 f0 = __ldg(&Phi[(0 * Ng + g_l) * R + rr]);
+                    const double2 f1 = __ldg(&Phi[(1 * Ng + g_l) * R + rr]);
+                    const double2 f2 = __ldg(&Phi[(2 * Ng + g_l) * R + rr]);
+                    const double2 f3 = __ldg(&Phi[(3 * Ng + g_l) * R + rr]);
+                    aA.x = fma(w01.x, f0.x, aA.x); aA.y = fma(w01.x, f0.y, aA.y);
+                    aA.x = fma(w01.y, f1.x, aA.x); aA.y = fma(w01.y, f1.y, aA.y);
+                    aA.x = fma(w23.x, f2.x, aA.x); aA.y = fma(w23.x, f2.y, aA.y);
+                    aP.x = fma(w23.y, f3.x, aP.x); aP.y = fma(w23.y, f3.y, aP.y);
+                }
+            } else {
+                const int cnt = min(32, S - ub);
+#pragma unroll 4
+                for (int t = grp; t < 32; t += G) {
+                    const long long g = __shfl_sync(0xffffffffu, g_l, t);
+                    const double wx = __shfl_sync(0xffffffffu, w01.x, t), wy = __shfl_sync(0xffffffffu, w01.y, t);
+                    const double wz = __shfl_sync(0xffffffffu, w23.x, t), wp = __shfl_sync(0xffffffffu, w23.y, t);
+                    if (t < cnt && act) {
+                        const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
+                        const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
+                        const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
+                        const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
+                        aA.x = fma(wx, f0.x, aA.x); aA.y = fma(wx, f0.y, aA.y);
+                        aA.x = fma(wy, f1.x, aA.x); aA.y = fma(wy, f1.y, aA.y);
+                        aA.x = fma(wz, f2.x, aA.x); aA.y = fma(wz, f2.y, aA.y);
+                        aP.x = fma(wp, f3.x, aP.x); aP.y = fma(wp, f3.y, aP.y);
+                    }
+                }
             }
         }
         // far = j k eta0 (aA - aP / k^2)
@@ -143,8 +199,10 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
 }
 
 // ------------------------------------------------------- H6 near SpMV
-// y[m,r] = sum_{n in near(m)} Z_corr[m,n] x[n,r]; warp per row, lanes over
-// (entry group, rhs), fixed-order shuffle reduction.
+// y[m,r] = sum_{n in near(m)} Z_corr[m,n] x[n,r]; warp per row.  Batches of
+// 32 entries: lane e loads (Z, col) of entry e (coalesced, streamed past L1),
+// then the rhs lanes gather x (entry broadcast by shuffles); fixed-order
+// shuffle reduction at the end.
 template <int RC>
 __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ rowp, const int32_t* __restrict__ col,
                                                    const double2* __restrict__ val, const double2* __restrict__ x,
@@ -159,13 +217,31 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
         const int rr = r0 + r;
         const bool act = rr < R;
         double2 aN = make_double2(0, 0);
-        for (long long e = e0 + grp; e < e1; e += G) {
-            const double2 z = __ldcs(&val[e]);
-            const int n = __ldcs(&col[e]);
-            if (act) {
-                const double2 xv = __ldg(&x[(long long)n * R + rr]);
-                aN.x = fma(z.x, xv.x, aN.x); aN.x = fma(-z.y, xv.y, aN.x);
-                aN.y = fma(z.x, xv.y, aN.y); aN.y = fma(z.y, xv.x, aN.y);
+        for (long long b = e0; b < e1; b += 32) {
+            const int cnt = (int)min(32LL, e1 - b);
+            double2 z_l = make_double2(0, 0);
+            int n_l = 0;
+            if (lane < cnt) {
+                z_l = __ldcs(&val[b + lane]);
+                n_l = __ldcs(&col[b + lane]);
+            }
+            if (RC == 1) {
+                if (lane < cnt) {
+                    const double2 xv = __ldg(&x[(long long)n_l * R + rr]);
+                    aN.x = fma(z_l.x, xv.x, aN.x); aN.x = fma(-z_l.y, xv.y, aN.x);
+                    aN.y = fma(z_l.x, xv.y, aN.y); aN.y = fma(z_l.y, xv.x, aN.y);
+                }
+            } else {
+#pragma unroll 8
+                for (int t = grp; t < 32; t += G) {
+                    const int n = __shfl_sync(0xffffffffu, n_l, t);
+                    const double zx = __shfl_sync(0xffffffffu, z_l.x, t), zy = __shfl_sync(0xffffffffu, z_l.y, t);
+                    if (t < cnt && act) {
+                        const double2 xv = __ldg(&x[(long long)n * R + rr]);
+                        aN.x = fma(zx, xv.x, aN.x); aN.x = fma(-zy, xv.y, aN.x);
+                        aN.y = fma(zx, xv.y, aN.y); aN.y = fma(zy, xv.x, aN.y);
+                    }
+                }
             }
         }
 #pragma unroll
