@@ -22,263 +22,292 @@ __device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
     return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
 
+// Lane layout of the gather kernels: LPE lanes share one CSR entry and each
+// holds RPL right-hand sides (r = r0 + sub + q*LPE), so a warp consumes
+// G = 32/LPE entries per step; the LPE lanes of a group read LPE*16
+// contiguous bytes per load.  Entries are staged 32 at a time: lane e loads
+// entry e's index / value (coalesced), then broadcasts it with shuffles.
+template <int LPE, int RPL>
+struct Lanes {
+    static constexpr int G = 32 / LPE;
+    static constexpr int RC = LPE * RPL;
+    int lane, grp, sub;
+    __device__ __forceinline__ Lanes() {
+        lane = threadIdx.x & 31;
+        grp = lane / LPE;
+        sub = lane % LPE;
+    }
+};
+
 // ------------------------------------------------------------ H1 projection
-// Warp per grid node.  Entries are consumed in batches of 32: every lane first
-// loads one entry's index and weights (coalesced / independent), then the
-// rhs lanes gather x for the batch (broadcast by shuffles), so each warp keeps
-// many independent loads in flight.
-template <int M, int RC>
+// Q^psi[u,r] = sum_{n in col(u)} w^psi_{n,u} x[n,r]; warp per grid node.
+template <int M, int LPE, int RPL>
 __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict__ prow,
                                                       const int32_t* __restrict__ pent,
                                                       const double* __restrict__ W, const double2* __restrict__ x,
                                                       long long Ng, int R, double2* __restrict__ Q) {
     constexpr int S = (M + 1) * (M + 1) * (M + 1);
-    constexpr int G = 32 / RC;
+    using L = Lanes<LPE, RPL>;
     const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (g >= Ng) return;
-    const int lane = threadIdx.x & 31;
-    const int grp = lane / RC, r = lane % RC;
+    const L ln;
     const int e0 = prow[g], e1 = prow[g + 1];
     const double2* W2 = reinterpret_cast<const double2*>(W);
-    for (int r0 = 0; r0 < R; r0 += RC) {
-        const int rr = r0 + r;
-        const bool act = rr < R;
-        double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
+    for (int r0 = 0; r0 < R; r0 += L::RC) {
+        double2 a[4][RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+            for (int c = 0; c < 4; ++c) a[c][q] = make_double2(0, 0);
         for (int b = e0; b < e1; b += 32) {
             const int cnt = min(32, e1 - b);
             int n_l = 0;
             double2 w01 = make_double2(0, 0), w23 = w01;
-            if (lane < cnt) {
-                const int ent = __ldg(&pent[b + lane]);
+            if (ln.lane < cnt) {
+                const int ent = __ldg(&pent[b + ln.lane]);
                 n_l = ent / S;
                 w01 = __ldcs(W2 + 2 * (long long)ent);
                 w23 = __ldcs(W2 + 2 * (long long)ent + 1);
             }
-            if (RC == 1) {
-                if (lane < cnt) {
-                    const double2 xv = __ldg(&x[(long long)n_l * R + rr]);
-                    a0.x = fma(w01.x, xv.x, a0.x); a0.y = fma(w01.x, xv.y, a0.y);
-                    a1.x = fma(w01.y, xv.x, a1.x); a1.y = fma(w01.y, xv.y, a1.y);
-                    a2.x = fma(w23.x, xv.x, a2.x); a2.y = fma(w23.x, xv.y, a2.y);
-                    a3.x = fma(w23.y, xv.x, a3.x); a3.y = fma(w23.y, xv.y, a3.y);
+#pragma unroll 2
+            for (int t = ln.grp; t < 32; t += L::G) {
+                int n;
+                double w[4];
+                if (LPE == 32) {
+                    n = n_l; w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
+                } else {
+                    n = __shfl_sync(0xffffffffu, n_l, t);
+                    w[0] = __shfl_sync(0xffffffffu, w01.x, t); w[1] = __shfl_sync(0xffffffffu, w01.y, t);
+                    w[2] = __shfl_sync(0xffffffffu, w23.x, t); w[3] = __shfl_sync(0xffffffffu, w23.y, t);
                 }
-            } else {
-#pragma unroll 4
-                for (int t = grp; t < 32; t += G) {
-                    const int n = __shfl_sync(0xffffffffu, n_l, t);
-                    const double wx = __shfl_sync(0xffffffffu, w01.x, t), wy = __shfl_sync(0xffffffffu, w01.y, t);
-                    const double wz = __shfl_sync(0xffffffffu, w23.x, t), wp = __shfl_sync(0xffffffffu, w23.y, t);
-                    if (t < cnt && act) {
-                        const double2 xv = __ldg(&x[(long long)n * R + rr]);
-                        a0.x = fma(wx, xv.x, a0.x); a0.y = fma(wx, xv.y, a0.y);
-                        a1.x = fma(wy, xv.x, a1.x); a1.y = fma(wy, xv.y, a1.y);
-                        a2.x = fma(wz, xv.x, a2.x); a2.y = fma(wz, xv.y, a2.y);
-                        a3.x = fma(wp, xv.x, a3.x); a3.y = fma(wp, xv.y, a3.y);
+                if (t < cnt) {
+                    const double2* xr = x + (long long)n * R + r0 + ln.sub;
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) {
+                        if (r0 + ln.sub + q * LPE < R) {
+                            const double2 xv = __ldg(xr + q * LPE);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                a[c][q].x = fma(w[c], xv.x, a[c][q].x);
+                                a[c][q].y = fma(w[c], xv.y, a[c][q].y);
+                            }
+                        }
                     }
                 }
             }
         }
 #pragma unroll
-        for (int off = RC; off < 32; off <<= 1) {
-            double2 t;
-            t = shfl_xor2(a0, off); a0.x += t.x; a0.y += t.y;
-            t = shfl_xor2(a1, off); a1.x += t.x; a1.y += t.y;
-            t = shfl_xor2(a2, off); a2.x += t.x; a2.y += t.y;
-            t = shfl_xor2(a3, off); a3.x += t.x; a3.y += t.y;
-        }
-        if (RC == 1) {
-            if (lane < 4) {
-                const double2 v = lane == 0 ? a0 : lane == 1 ? a1 : lane == 2 ? a2 : a3;
-                __stcs(&Q[((long long)lane * Ng + g) * R + rr], v);
+        for (int off = LPE; off < 32; off <<= 1)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const double2 t = shfl_xor2(a[c][q], off);
+                    a[c][q].x += t.x; a[c][q].y += t.y;
+                }
+        if (ln.grp == 0) {
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int rr = r0 + ln.sub + q * LPE;
+                if (rr < R)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) __stcs(&Q[((long long)c * Ng + g) * R + rr], a[c][q]);
             }
-        } else if (grp == 0 && act) {
-            __stcs(&Q[(0 * Ng + g) * R + rr], a0);
-            __stcs(&Q[(1 * Ng + g) * R + rr], a1);
-            __stcs(&Q[(2 * Ng + g) * R + rr], a2);
-            __stcs(&Q[(3 * Ng + g) * R + rr], a3);
         }
     }
 }
 
-static int rhs_chunk(int R) {
-    int rc = 1;
-    while (rc < R && rc < 32) rc <<= 1;
-    return rc;
-}
+// (LPE, RPL) per RHS count: one lane per entry below 4 RHS, 4 RHS per lane above.
+#define AIM_LANE_DISPATCH(R, CALL)                     \
+    if (R == 1) { CALL(1, 1); }                        \
+    else if (R == 2) { CALL(1, 2); }                   \
+    else if (R <= 4) { CALL(1, 4); }                   \
+    else if (R <= 8) { CALL(2, 4); }                   \
+    else if (R <= 16) { CALL(4, 4); }                  \
+    else { CALL(8, 4); }
 
 void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s) {
-    const int rc = rhs_chunk(R);
     const unsigned grid = nblk(p->Ng * 32, 256);
-#define PJ(MM, RR) \
-    if (p->M == MM && rc == RR) { project_kernel<MM, RR><<<grid, 256, 0, s>>>(p->prow, p->pent, p->W, x, p->Ng, R, Q); note_launch("project"); return; }
-#define PJM(MM) PJ(MM, 1) PJ(MM, 2) PJ(MM, 4) PJ(MM, 8) PJ(MM, 16) PJ(MM, 32)
-    PJM(1) PJM(2) PJM(3) PJM(4) PJM(5) PJM(6)
-#undef PJM
-#undef PJ
+#define PJ_CALL(LPE, RPL) project_kernel<MM, LPE, RPL><<<grid, 256, 0, s>>>(p->prow, p->pent, p->W, x, p->Ng, R, Q)
+#define PJ_M(MMV)                                   \
+    if (p->M == MMV) {                              \
+        constexpr int MM = MMV;                     \
+        AIM_LANE_DISPATCH(R, PJ_CALL)               \
+        note_launch("project");                     \
+        return;                                     \
+    }
+    PJ_M(1) PJ_M(2) PJ_M(3) PJ_M(4) PJ_M(5) PJ_M(6)
+#undef PJ_M
+#undef PJ_CALL
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
 // ------------------------------------------------------ H5 interpolation
 // y[m,r] (+)= j k eta0 [sum_xyz sum_u w_{m,u} Phi[u,r] - k^-2 sum_u w^phi_{m,u} Phi^phi[u,r]]
-// Warp per RWG row: lane u first loads w_{m,u} (contiguous), then the rhs
-// lanes gather the stencil's potentials (weights broadcast by shuffles).
-template <int M, int RC>
+// Warp per RWG row: lane u loads w_{m,u} (contiguous) and its node index, then
+// the rhs lanes gather the stencil's potentials (weights broadcast by shuffles).
+template <int M, int LPE, int RPL>
 __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__ Phi, const double* __restrict__ W,
                                                      const int32_t* __restrict__ node0, long long Ng, int Ny, int Nz,
                                                      long long N, int R, double keta, double ik2, int accumulate,
                                                      double2* __restrict__ y) {
     constexpr int M1 = M + 1, S = M1 * M1 * M1;
-    constexpr int G = 32 / RC;
+    using L = Lanes<LPE, RPL>;
     const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (m >= N) return;
-    const int lane = threadIdx.x & 31;
-    const int grp = lane / RC, r = lane % RC;
+    const L ln;
     const long long g0 = node0[m];
     const double2* W2 = reinterpret_cast<const double2*>(W) + 2 * m * S;
-    for (int r0 = 0; r0 < R; r0 += RC) {
-        const int rr = r0 + r;
-        const bool act = rr < R;
-        double2 aA = make_double2(0, 0), aP = aA;
+    for (int r0 = 0; r0 < R; r0 += L::RC) {
+        double2 aA[RPL], aP[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) aA[q] = aP[q] = make_double2(0, 0);
         for (int ub = 0; ub < S; ub += 32) {
-            const int u_l = ub + lane;
+            const int u_l = ub + ln.lane;
+            const int cnt = min(32, S - ub);
             double2 w01 = make_double2(0, 0), w23 = w01;
             int g_l = 0;
-            if (u_l < S) {
+            if (ln.lane < cnt) {
                 w01 = __ldcs(W2 + 2 * u_l);
                 w23 = __ldcs(W2 + 2 * u_l + 1);
                 const int ui = u_l / (M1 * M1), uj = (u_l / M1) % M1, uk = u_l % M1;
                 g_l = (int)(g0 + ((long long)ui * Ny + uj) * Nz + uk);
             }
-            if (RC == 1) {
-                if (u_l < S) {
-                    const double2 f0 = __ldg(&Phi[(0 * Ng + g_l) * R + rr]);
-                    const double2 f1 = __ldg(&Phi[(1 * Ng + g_l) * R + rr]);
-                    const double2 f2 = __ldg(&Phi[(2 * Ng + g_l) * R + rr]);
-                    const double2 f3 = __ldg(&Phi[(3 * Ng + g_l) * R + rr]);
-                    aA.x = fma(w01.x, f0.x, aA.x); aA.y = fma(w01.x, f0.y, aA.y);
-                    aA.x = fma(w01.y, f1.x, aA.x); aA.y = fma(w01.y, f1.y, aA.y);
-                    aA.x = fma(w23.x, f2.x, aA.x); aA.y = fma(w23.x, f2.y, aA.y);
-                    aP.x = fma(w23.y, f3.x, aP.x); aP.y = fma(w23.y, f3.y, aP.y);
+#pragma unroll 2
+            for (int t = ln.grp; t < 32; t += L::G) {
+                int g;
+                double w[4];
+                if (LPE == 32) {
+                    g = g_l; w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
+                } else {
+                    g = __shfl_sync(0xffffffffu, g_l, t);
+                    w[0] = __shfl_sync(0xffffffffu, w01.x, t); w[1] = __shfl_sync(0xffffffffu, w01.y, t);
+                    w[2] = __shfl_sync(0xffffffffu, w23.x, t); w[3] = __shfl_sync(0xffffffffu, w23.y, t);
                 }
-            } else {
-                const int cnt = min(32, S - ub);
-#pragma unroll 4
-                for (int t = grp; t < 32; t += G) {
-                    const long long g = __shfl_sync(0xffffffffu, g_l, t);
-                    const double wx = __shfl_sync(0xffffffffu, w01.x, t), wy = __shfl_sync(0xffffffffu, w01.y, t);
-                    const double wz = __shfl_sync(0xffffffffu, w23.x, t), wp = __shfl_sync(0xffffffffu, w23.y, t);
-                    if (t < cnt && act) {
-                        const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
-                        const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
-                        const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
-                        const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
-                        aA.x = fma(wx, f0.x, aA.x); aA.y = fma(wx, f0.y, aA.y);
-                        aA.x = fma(wy, f1.x, aA.x); aA.y = fma(wy, f1.y, aA.y);
-                        aA.x = fma(wz, f2.x, aA.x); aA.y = fma(wz, f2.y, aA.y);
-                        aP.x = fma(wp, f3.x, aP.x); aP.y = fma(wp, f3.y, aP.y);
+                if (t < cnt) {
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) {
+                        const int rr = r0 + ln.sub + q * LPE;
+                        if (rr < R) {
+                            const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
+                            const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
+                            const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
+                            const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
+                            aA[q].x = fma(w[0], f0.x, aA[q].x); aA[q].y = fma(w[0], f0.y, aA[q].y);
+                            aA[q].x = fma(w[1], f1.x, aA[q].x); aA[q].y = fma(w[1], f1.y, aA[q].y);
+                            aA[q].x = fma(w[2], f2.x, aA[q].x); aA[q].y = fma(w[2], f2.y, aA[q].y);
+                            aP[q].x = fma(w[3], f3.x, aP[q].x); aP[q].y = fma(w[3], f3.y, aP[q].y);
+                        }
                     }
                 }
             }
         }
-        // far = j k eta0 (aA - aP / k^2)
-        const double2 f = make_double2(aA.x - aP.x * ik2, aA.y - aP.y * ik2);
-        double2 tot = make_double2(-keta * f.y, keta * f.x);
 #pragma unroll
-        for (int off = RC; off < 32; off <<= 1) {
-            const double2 t = shfl_xor2(tot, off);
-            tot.x += t.x; tot.y += t.y;
-        }
-        if (grp == 0 && act) {
-            if (accumulate) {
-                const double2 o = y[m * R + rr];
-                tot.x += o.x; tot.y += o.y;
+        for (int q = 0; q < RPL; ++q) {
+            // far = j k eta0 (aA - aP / k^2)
+            const double2 f = make_double2(aA[q].x - aP[q].x * ik2, aA[q].y - aP[q].y * ik2);
+            double2 tot = make_double2(-keta * f.y, keta * f.x);
+#pragma unroll
+            for (int off = LPE; off < 32; off <<= 1) {
+                const double2 t = shfl_xor2(tot, off);
+                tot.x += t.x; tot.y += t.y;
             }
-            y[m * R + rr] = tot;
+            const int rr = r0 + ln.sub + q * LPE;
+            if (ln.grp == 0 && rr < R) {
+                if (accumulate) {
+                    const double2 o = y[m * R + rr];
+                    tot.x += o.x; tot.y += o.y;
+                }
+                y[m * R + rr] = tot;
+            }
         }
     }
 }
 
 // ------------------------------------------------------- H6 near SpMV
-// y[m,r] = sum_{n in near(m)} Z_corr[m,n] x[n,r]; warp per row.  Batches of
-// 32 entries: lane e loads (Z, col) of entry e (coalesced, streamed past L1),
-// then the rhs lanes gather x (entry broadcast by shuffles); fixed-order
-// shuffle reduction at the end.
-template <int RC>
+// y[m,r] = sum_{n in near(m)} Z_corr[m,n] x[n,r]; warp per row, entries
+// staged 32 at a time (values streamed past L1), fixed-order reduction.
+template <int LPE, int RPL>
 __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ rowp, const int32_t* __restrict__ col,
                                                    const double2* __restrict__ val, const double2* __restrict__ x,
                                                    long long N, int R, double2* __restrict__ y) {
-    constexpr int G = 32 / RC;
+    using L = Lanes<LPE, RPL>;
     const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (m >= N) return;
-    const int lane = threadIdx.x & 31;
-    const int grp = lane / RC, r = lane % RC;
+    const L ln;
     const long long e0 = rowp[m], e1 = rowp[m + 1];
-    for (int r0 = 0; r0 < R; r0 += RC) {
-        const int rr = r0 + r;
-        const bool act = rr < R;
-        double2 aN = make_double2(0, 0);
+    for (int r0 = 0; r0 < R; r0 += L::RC) {
+        double2 acc[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) acc[q] = make_double2(0, 0);
         for (long long b = e0; b < e1; b += 32) {
             const int cnt = (int)min(32LL, e1 - b);
             double2 z_l = make_double2(0, 0);
             int n_l = 0;
-            if (lane < cnt) {
-                z_l = __ldcs(&val[b + lane]);
-                n_l = __ldcs(&col[b + lane]);
+            if (ln.lane < cnt) {
+                z_l = __ldcs(&val[b + ln.lane]);
+                n_l = __ldcs(&col[b + ln.lane]);
             }
-            if (RC == 1) {
-                if (lane < cnt) {
-                    const double2 xv = __ldg(&x[(long long)n_l * R + rr]);
-                    aN.x = fma(z_l.x, xv.x, aN.x); aN.x = fma(-z_l.y, xv.y, aN.x);
-                    aN.y = fma(z_l.x, xv.y, aN.y); aN.y = fma(z_l.y, xv.x, aN.y);
+#pragma unroll 4
+            for (int t = ln.grp; t < 32; t += L::G) {
+                int n;
+                double zx, zy;
+                if (LPE == 32) {
+                    n = n_l; zx = z_l.x; zy = z_l.y;
+                } else {
+                    n = __shfl_sync(0xffffffffu, n_l, t);
+                    zx = __shfl_sync(0xffffffffu, z_l.x, t);
+                    zy = __shfl_sync(0xffffffffu, z_l.y, t);
                 }
-            } else {
-#pragma unroll 8
-                for (int t = grp; t < 32; t += G) {
-                    const int n = __shfl_sync(0xffffffffu, n_l, t);
-                    const double zx = __shfl_sync(0xffffffffu, z_l.x, t), zy = __shfl_sync(0xffffffffu, z_l.y, t);
-                    if (t < cnt && act) {
-                        const double2 xv = __ldg(&x[(long long)n * R + rr]);
-                        aN.x = fma(zx, xv.x, aN.x); aN.x = fma(-zy, xv.y, aN.x);
-                        aN.y = fma(zx, xv.y, aN.y); aN.y = fma(zy, xv.x, aN.y);
+                if (t < cnt) {
+                    const double2* xr = x + (long long)n * R + r0 + ln.sub;
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) {
+                        if (r0 + ln.sub + q * LPE < R) {
+                            const double2 xv = __ldg(xr + q * LPE);
+                            acc[q].x = fma(zx, xv.x, acc[q].x); acc[q].x = fma(-zy, xv.y, acc[q].x);
+                            acc[q].y = fma(zx, xv.y, acc[q].y); acc[q].y = fma(zy, xv.x, acc[q].y);
+                        }
                     }
                 }
             }
         }
 #pragma unroll
-        for (int off = RC; off < 32; off <<= 1) {
-            const double2 t = shfl_xor2(aN, off);
-            aN.x += t.x; aN.y += t.y;
+        for (int q = 0; q < RPL; ++q) {
+#pragma unroll
+            for (int off = LPE; off < 32; off <<= 1) {
+                const double2 t = shfl_xor2(acc[q], off);
+                acc[q].x += t.x; acc[q].y += t.y;
+            }
+            const int rr = r0 + ln.sub + q * LPE;
+            if (ln.grp == 0 && rr < R) y[m * R + rr] = acc[q];
         }
-        if (grp == 0 && act) y[m * R + rr] = aN;
     }
 }
 
 void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s) {
-    const int rc = rhs_chunk(R);
     const unsigned grid = nblk(p->N * 32, 256);
     const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
-#define IN(MM, RR)                                                                                        \
-    if (p->M == MM && rc == RR) {                                                                         \
-        interp_kernel<MM, RR><<<grid, 256, 0, s>>>(Phi, p->W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, R, \
-                                                   keta, ik2, accumulate ? 1 : 0, y);                     \
-        note_launch("interp");                                                                            \
-        return;                                                                                           \
+#define IN_CALL(LPE, RPL)                                                                                     \
+    interp_kernel<MM, LPE, RPL><<<grid, 256, 0, s>>>(Phi, p->W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, R, \
+                                                     keta, ik2, accumulate ? 1 : 0, y)
+#define IN_M(MMV)                     \
+    if (p->M == MMV) {                \
+        constexpr int MM = MMV;       \
+        AIM_LANE_DISPATCH(R, IN_CALL) \
+        note_launch("interp");        \
+        return;                       \
     }
-#define INM(MM) IN(MM, 1) IN(MM, 2) IN(MM, 4) IN(MM, 8) IN(MM, 16) IN(MM, 32)
-    INM(1) INM(2) INM(3) INM(4) INM(5) INM(6)
-#undef INM
-#undef IN
+    IN_M(1) IN_M(2) IN_M(3) IN_M(4) IN_M(5) IN_M(6)
+#undef IN_M
+#undef IN_CALL
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
 void launch_near(const aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
-    const int rc = rhs_chunk(R);
     const unsigned grid = nblk(p->N * 32, 256);
-    switch (rc) {
-#define NK(RR) case RR: near_kernel<RR><<<grid, 256, 0, s>>>(p->nrow, p->ncol, p->nval, x, p->N, R, y); break;
-        NK(1) NK(2) NK(4) NK(8) NK(16) NK(32)
-#undef NK
-    }
+#define NK_CALL(LPE, RPL) near_kernel<LPE, RPL><<<grid, 256, 0, s>>>(p->nrow, p->ncol, p->nval, x, p->N, R, y)
+    AIM_LANE_DISPATCH(R, NK_CALL)
+#undef NK_CALL
     note_launch("near");
 }
 
