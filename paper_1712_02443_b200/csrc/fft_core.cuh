@@ -36,10 +36,53 @@ __device__ __forceinline__ constexpr double os(int m) {
                   : (m == 0 ? 0.781831482468029803634 : m == 1 ? 0.974927912181823619342 : 0.433883739117558120402);
 }
 
+// Twiddles of the composite in-register radices: c_rtw[rtw_off(R) + j] =
+// exp(-2 pi i j / R) (filled once per device by init_radix_twiddles()).
+constexpr int kRtwTotal = 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16;
+__host__ __device__ constexpr int rtw_off(int R) {
+    return R == 6 ? 0 : R == 8 ? 6 : R == 9 ? 14 : R == 10 ? 23 : R == 12 ? 33 : R == 14 ? 45 : R == 15 ? 59 : 74;
+}
+__constant__ double2 c_rtw[kRtwTotal];
+
+// composite R = A * B, A the first (prime-power) factor
+template <int R>
+struct Split {
+    static constexpr int A = R == 16 ? 4 : R == 12 ? 4 : R == 8 ? 2 : (R % 2 == 0) ? 2 : 3;
+    static constexpr int B = R / A;
+};
+
 // b_u = sum_t a_t exp(sign 2 pi i t u / R), in place
 template <int R>
 __device__ __forceinline__ void dft(double2* a, double sign) {
-    if constexpr (R == 2) {
+    if constexpr (R == 1) {
+    } else if constexpr (R != 2 && R != 3 && R != 4 && R != 5 && R != 7) {
+        // decimation in time inside registers: Y_r = DFT_B(a[A m + r]),
+        // X[k + B s] = DFT_A over r of W_R^{r k} Y_r[k]
+        constexpr int A = Split<R>::A, B = Split<R>::B;
+        double2 y[A][B];
+#pragma unroll
+        for (int r = 0; r < A; ++r) {
+#pragma unroll
+            for (int m = 0; m < B; ++m) y[r][m] = a[A * m + r];
+            dft<B>(y[r], sign);
+        }
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            double2 t[A];
+#pragma unroll
+            for (int r = 0; r < A; ++r) {
+                t[r] = y[r][k];
+                if ((r * k) % R) {
+                    double2 w = c_rtw[rtw_off(R) + (r * k) % R];
+                    if (sign > 0) w.y = -w.y;
+                    t[r] = cmul(t[r], w);
+                }
+            }
+            dft<A>(t, sign);
+#pragma unroll
+            for (int q = 0; q < A; ++q) a[k + B * q] = t[q];
+        }
+    } else if constexpr (R == 2) {
         const double2 t = a[0];
         a[0] = cadd(t, a[1]);
         a[1] = csub(t, a[1]);
@@ -144,11 +187,10 @@ __device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const do
     for (int s = 0; s < ax.nst; ++s) {
         const unsigned long long M = ax.nsM[s];
         switch (ax.radix[s]) {
-            case 2: stage<2>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
-            case 3: stage<3>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
-            case 4: stage<4>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
-            case 5: stage<5>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
-            case 7: stage<7>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
+#define AIM_STAGE(RR) case RR: stage<RR>(src, dst, tw, ax.P, NL, Ns, M, sign, lm); break;
+            AIM_STAGE(2) AIM_STAGE(3) AIM_STAGE(4) AIM_STAGE(5) AIM_STAGE(6) AIM_STAGE(7) AIM_STAGE(8)
+            AIM_STAGE(9) AIM_STAGE(10) AIM_STAGE(12) AIM_STAGE(14) AIM_STAGE(15) AIM_STAGE(16)
+#undef AIM_STAGE
         }
         __syncthreads();
         Ns *= ax.radix[s];

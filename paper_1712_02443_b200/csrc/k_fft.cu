@@ -21,7 +21,7 @@
 
 namespace aim {
 
-__global__ void __launch_bounds__(256) fft_pass_kernel(FftPass p) {
+__global__ void __launch_bounds__(256, 3) fft_pass_kernel(FftPass p) {
     extern __shared__ double2 sm[];
     const int P = p.ax.P;
     const int TO = p.TO, TI = p.TI;
@@ -161,15 +161,48 @@ int smooth_size_at_least(int n) {
     }
 }
 
+// Radices available as one in-register butterfly (composites via fft_core's
+// nested DFT).  Stage plan: fewest stages, then the larger first radix.
+static const int kRadices[] = {16, 15, 14, 12, 10, 9, 8, 7, 6, 5, 4, 3, 2};
+
+static void plan_radices(int P, std::vector<int>& best, std::vector<int>& cur) {
+    if (P == 1) {
+        if (best.empty() || cur.size() < best.size()) best = cur;
+        return;
+    }
+    if (!best.empty() && cur.size() + 1 >= best.size()) return;
+    for (int r : kRadices)
+        if (P % r == 0) {
+            cur.push_back(r);
+            plan_radices(P / r, best, cur);
+            cur.pop_back();
+        }
+}
+
+void init_radix_twiddles() {
+    static bool done[64] = {false};
+    int dev = 0;
+    AIM_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && done[dev]) return;
+    std::vector<double2> h(kRtwTotal);
+    for (int R : {6, 8, 9, 10, 12, 14, 15, 16})
+        for (int j = 0; j < R; ++j) {
+            long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)j / (long double)R;
+            h[rtw_off(R) + j] = make_double2((double)cosl(a), (double)sinl(a));
+        }
+    AIM_CUDA(cudaMemcpyToSymbol(c_rtw, h.data(), sizeof(double2) * kRtwTotal));
+    if (dev < 64) done[dev] = true;
+}
+
 void make_fft_axis(int P, FftAxis& ax) {
+    init_radix_twiddles();
     ax.P = P;
     ax.nst = 0;
-    int r = P;
-    while (r % 4 == 0) { ax.radix[ax.nst++] = 4; r /= 4; }
-    while (r % 2 == 0) { ax.radix[ax.nst++] = 2; r /= 2; }
-    for (int f : {3, 5, 7})
-        while (r % f == 0) { ax.radix[ax.nst++] = f; r /= f; }
-    if (r != 1 || ax.nst > kMaxStages) throw Error(AIM_E_GRID, "FFT size not 7-smooth");
+    std::vector<int> best, cur;
+    plan_radices(P, best, cur);
+    if (P > 1 && best.empty()) throw Error(AIM_E_GRID, "FFT size not 7-smooth");
+    if ((int)best.size() > kMaxStages) throw Error(AIM_E_GRID, "too many FFT stages");
+    for (int r : best) ax.radix[ax.nst++] = r;
     long long Ns = 1;
     for (int st = 0; st < ax.nst; ++st) {
         ax.nsM[st] = ((1ULL << 40) + (unsigned long long)Ns - 1) / (unsigned long long)Ns;

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
             for (int t = ln.grp; t < 32; t += L::G) {
                 int n;
                 double w[4];
-                if (LPE == 32) {
+                if (LPE == 1) {
                     n = n_l; w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
                 } else {
                     n = __shfl_sync(0xffffffffu, n_l, t);
@@ -116,14 +116,22 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
     }
 }
 
-// (LPE, RPL) per RHS count: one lane per entry below 4 RHS, 4 RHS per lane above.
-#define AIM_LANE_DISPATCH(R, CALL)                     \
+// (LPE, RPL) per RHS count.  NEAR: 4 RHS per lane (instruction-bound SpMV);
+// GATHER (projection / interpolation): one RHS per lane (latency-bound).
+#define AIM_LANE_DISPATCH_NEAR(R, CALL)                \
     if (R == 1) { CALL(1, 1); }                        \
     else if (R == 2) { CALL(1, 2); }                   \
     else if (R <= 4) { CALL(1, 4); }                   \
     else if (R <= 8) { CALL(2, 4); }                   \
     else if (R <= 16) { CALL(4, 4); }                  \
     else { CALL(8, 4); }
+#define AIM_LANE_DISPATCH_GATHER(R, CALL)              \
+    if (R == 1) { CALL(1, 1); }                        \
+    else if (R == 2) { CALL(2, 1); }                   \
+    else if (R <= 4) { CALL(4, 1); }                   \
+    else if (R <= 8) { CALL(8, 1); }                   \
+    else if (R <= 16) { CALL(16, 1); }                 \
+    else { CALL(32, 1); }
 
 void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s) {
     const unsigned grid = nblk(p->Ng * 32, 256);
@@ -131,7 +139,7 @@ void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cuda
 #define PJ_M(MMV)                                   \
     if (p->M == MMV) {                              \
         constexpr int MM = MMV;                     \
-        AIM_LANE_DISPATCH(R, PJ_CALL)               \
+        AIM_LANE_DISPATCH_GATHER(R, PJ_CALL)               \
         note_launch("project");                     \
         return;                                     \
     }
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
             for (int t = ln.grp; t < 32; t += L::G) {
                 int g;
                 double w[4];
-                if (LPE == 32) {
+                if (LPE == 1) {
                     g = g_l; w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
                 } else {
                     g = __shfl_sync(0xffffffffu, g_l, t);
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
             for (int t = ln.grp; t < 32; t += L::G) {
                 int n;
                 double zx, zy;
-                if (LPE == 32) {
+                if (LPE == 1) {
                     n = n_l; zx = z_l.x; zy = z_l.y;
                 } else {
                     n = __shfl_sync(0xffffffffu, n_l, t);
@@ -293,7 +301,7 @@ void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, boo
 #define IN_M(MMV)                     \
     if (p->M == MMV) {                \
         constexpr int MM = MMV;       \
-        AIM_LANE_DISPATCH(R, IN_CALL) \
+        AIM_LANE_DISPATCH_GATHER(R, IN_CALL) \
         note_launch("interp");        \
         return;                       \
     }
@@ -306,7 +314,7 @@ void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, boo
 void launch_near(const aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
     const unsigned grid = nblk(p->N * 32, 256);
 #define NK_CALL(LPE, RPL) near_kernel<LPE, RPL><<<grid, 256, 0, s>>>(p->nrow, p->ncol, p->nval, x, p->N, R, y)
-    AIM_LANE_DISPATCH(R, NK_CALL)
+    AIM_LANE_DISPATCH_NEAR(R, NK_CALL)
 #undef NK_CALL
     note_launch("near");
 }
