@@ -47,18 +47,46 @@ def load_peaks():
 
 
 def alg_bytes(info, R):
-    """Compulsory bytes per matvec and of the fused
-    interpolation + near kernel, for R right-hand sides."""
+    """Compulsory (algorithmic) bytes per matvec and per
+    launch of each stage kernel, for R right-hand sides."""
     N, S, Ng = info["n_rwg"], info["S"], info["n_nodes"]
     nnzP, nnzN = info["nnz_proj"], info["nnz_near"]
     Px, Py, Pz = info["fft_dims"]
-    spec = 16 * (Px // 2 + 1) * (Py // 2 + 1) * (Pz // 2 + 1)
+    Nx, Ny, Nz = info["grid_dims"]
+    spec = 16 * (Px // 2 + 1) * (Py // 2 + 1) * (Nz if info["conv_mode"] == 1 else Pz // 2 + 1)
     matvec = (16 * N * R + 36 * nnzP + 4 * (Ng + 1) + 4 * 64 * Ng * R + spec
               + 32 * nnzP + 4 * N + 20 * nnzN + 4 * (N + 1) + 16 * N * R)
-    interp_near = (32 * nnzP + 4 * N + 64 * Ng * R      # weights, base index, grid potentials
-                   + 20 * nnzN + 8 * (N + 1)            # near CSR values + columns, row pointers
-                   + 16 * N * R + 16 * N * R)           # x gathered, y written
-    return matvec, interp_near
+    grid = 64 * Ng * R                                   # one 4-component grid, R RHS
+    xpad = 64 * Px * Ny * Nz * R                         # x-padded grid
+    stages = {
+        "near": 20 * nnzN + 8 * (N + 1) + 16 * N * R + 16 * N * R,          # Z, col, rowptr, x, y
+        "project": 36 * nnzP + 4 * (Ng + 1) + 16 * N * R + grid,            # ent+w, rowptr, x, Q
+        "interp": 32 * nnzP + 4 * N + grid + 2 * 16 * N * R,                # w, base, Phi, y (r+w)
+        "fft_x": grid + xpad,                                              # Q -> W1
+        "fft_yz": 2 * xpad + spec,                                         # W1 in place + spectrum
+        "ifft_x": xpad + grid,                                             # W1 -> Phi
+    }
+    return matvec, stages
+
+
+KERNEL_NAMES = {
+    "near": "near_kernel (H6 precorrected near-field SpMV, side stream)",
+    "project": "project_kernel (H1 projection gather)",
+    "interp": "interp_kernel (H5 interpolation)",
+    "fft_x": "fft_pass_kernel (x forward, zero-pad fused)",
+    "fft_yz": "planar_yz_kernel / fft_pass_kernel x3 (y fwd, z convolution, y inv)",
+    "ifft_x": "fft_pass_kernel (x inverse, pruned)",
+}
+
+
+def load_traffic(stage):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu
+    capture (profiles/traffic_c2.json: dram__bytes_read.sum + write), if any."""
+    path = os.path.join(ROOT, "profiles", "traffic_c2.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get(stage)
+    return None
 
 
 class ClockSampler:
@@ -248,19 +276,17 @@ def main():
            "d2h_bytes_per_step": int(xh.nbytes), "steps": args.e2e_steps, "timer": "host wall clock (synchronous call)"}
 
     peak, peak_src = load_peaks()
-    b_mv, b_in = alg_bytes(info, R)
+    b_mv, b_stage = alg_bytes(info, R)
     stage_ms = {k: v / max(1, nprof) for k, v in stages.items()}
-    dom = max(stage_ms, key=stage_ms.get)
-    dom_bytes = b_in if dom == "interp_near" else None
-    roof = None
-    if dom_bytes is not None:
-        ach = dom_bytes / (stage_ms[dom] / 1e3) / 1e9
-        roof = {"kernel": "interp_near_kernel (H5 interpolation + H6 near SpMV)", "bound": "hbm",
-                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
-                "alg_bytes_per_launch": dom_bytes, "ms_per_launch": stage_ms[dom], "peak_source": peak_src}
-    else:
-        roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
-                "traffic": None, "ms_per_launch": stage_ms[dom], "peak_source": peak_src}
+    stage_gbs = {k: (b_stage[k] / (stage_ms[k] / 1e3) / 1e9 if stage_ms.get(k) else None) for k in b_stage}
+    dom = max(b_stage, key=lambda k: stage_ms.get(k, 0.0))
+    ach = stage_gbs[dom]
+    traffic = load_traffic(dom)
+    roof = {"kernel": KERNEL_NAMES[dom], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": b_stage[dom],
+            "ms_per_launch": stage_ms[dom], "peak_source": peak_src,
+            "timing": "CUDA events recorded by the library around the kernel on its launch stream, "
+                      "averaged over the timed region"}
     ms_step = 1e3 * t / args.steps
     mv_ach = b_mv / (ms_step / 1e3) / 1e9
     line = {
@@ -275,7 +301,7 @@ def main():
         "roofline": roof,
         "matvec_roofline": {"bound": "hbm", "alg_bytes": b_mv, "achieved": mv_ach, "peak": peak, "unit": "GB/s",
                             "frac": mv_ach / peak},
-        "stage_ms": stage_ms,
+        "stage_ms": stage_ms, "stage_alg_gbs": stage_gbs,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "plan_seconds": info["plan_seconds"], "device_bytes": info["device_bytes"],
     }

@@ -84,10 +84,11 @@ __global__ void __launch_bounds__(256, 3) fft_pass_kernel(FftPass p) {
 }
 
 // ------------------------------------------------------------ planar y/z
+constexpr int kPlanarThreads = 256;   // max; launched with min(256, Py*RC rounded to 32)
 // W[4][Px][Ny][Nz][R] in place.  CTA = (plane c*Px+kx, rhs chunk r0..r0+RC).
 // smem [Py][Nz*RC] (y lines indexed by l = z*RC + rl).
 template <int NZ>
-__global__ void __launch_bounds__(256, 2) planar_yz_kernel(PlanarPass p) {
+__global__ void __launch_bounds__(kPlanarThreads, 2) planar_yz_kernel(PlanarPass p) {
     extern __shared__ double2 sm[];
     const int Py = p.ay.P;
     const int RC = p.RC;
@@ -122,30 +123,36 @@ __global__ void __launch_bounds__(256, 2) planar_yz_kernel(PlanarPass p) {
     __syncthreads();
     double2* res = fft_lines(buf, alt, tw, p.ay, NL, -1.0, lm);
     double2* oth = res == buf ? alt : buf;
-    // z: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for every (ky, rl)
+    // z: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for every (ky, rl), one
+    // line per thread, all indices compile-time (G2 row and inputs in registers),
+    // symmetric Toeplitz: out[z] = g0 in[z] + sum_{d>0} g_d (in[z-d] + in[z+d]).
     const int ax_ = min(kx, p.Px - kx);
     const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
     for (int line = threadIdx.x; line < Py * RC; line += blockDim.x) {
         const int ky = line / RC, rr = line - (line / RC) * RC;
         const int ay = min(ky, Py - ky);
         const double2* g = G2 + (long long)ay * NZ;
-        double2 in[NZ];
+        double2 gk[NZ], in[NZ];
+#pragma unroll
+        for (int d = 0; d < NZ; ++d) gk[d] = __ldg(&g[d]);
 #pragma unroll
         for (int zz = 0; zz < NZ; ++zz) in[zz] = res[ky * NL + zz * RC + rr];
 #pragma unroll
         for (int zz = 0; zz < NZ; ++zz) {
-            double2 acc = make_double2(0.0, 0.0);
+            double2 acc = cmul(gk[0], in[zz]);
 #pragma unroll
-            for (int zp = 0; zp < NZ; ++zp) {
-                const double2 gg = __ldg(&g[zz > zp ? zz - zp : zp - zz]);
-                acc.x = fma(gg.x, in[zp].x, fma(-gg.y, in[zp].y, acc.x));
-                acc.y = fma(gg.x, in[zp].y, fma(gg.y, in[zp].x, acc.y));
+            for (int d = 1; d < NZ; ++d) {
+                if (zz - d < 0 && zz + d >= NZ) continue;
+                double2 sum = zz - d >= 0 ? in[zz - d] : make_double2(0.0, 0.0);
+                if (zz + d < NZ) sum = cadd(sum, in[zz + d]);
+                acc.x = fma(gk[d].x, sum.x, fma(-gk[d].y, sum.y, acc.x));
+                acc.y = fma(gk[d].x, sum.y, fma(gk[d].y, sum.x, acc.y));
             }
-            res[ky * NL + zz * RC + rr] = acc;
+            oth[ky * NL + zz * RC + rr] = acc;
         }
     }
     __syncthreads();
-    res = fft_lines(res, oth, tw, p.ay, NL, +1.0, lm);
+    res = fft_lines(oth, res, tw, p.ay, NL, +1.0, lm);
     if (live)
         for (int y = lm.js; y < p.Ny; y += lm.JS) __stcs(W + y * ystride, res[y * NL + lm.l]);
 }
@@ -254,9 +261,11 @@ void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
     PlanarPass p = p0;
     const int Py = p.ay.P;
     const int cap = 2 * fft_tile_capacity();
-    p.RC = std::max(1, std::min({p.R, cap / (Py * p.Nz), kFftThreads / p.Nz}));
+    p.RC = std::max(1, std::min({p.R, cap / (Py * p.Nz), kPlanarThreads / p.Nz}));
     const long long nchunk = (p.R + p.RC - 1) / p.RC;
     const long long grid = 4LL * p.Px * nchunk;
+    // one z line per thread in the convolution step; NL lines for the FFT stages
+    const int threads = std::max(32 * ((p.Nz * p.RC + 31) / 32), std::min(kPlanarThreads, 32 * ((Py * p.RC + 31) / 32)));
     const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py);
     switch (p.Nz) {
 #define PZ(NZ)                                                                                              \
@@ -267,7 +276,7 @@ void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
                                           227 * 1024));                                                     \
             attr = true;                                                                                    \
         }                                                                                                   \
-        planar_yz_kernel<NZ><<<(unsigned)grid, kFftThreads, smem, s>>>(p);                                   \
+        planar_yz_kernel<NZ><<<(unsigned)grid, threads, smem, s>>>(p);                                   \
         break;                                                                                              \
     }
         PZ(1) PZ(2) PZ(3) PZ(4) PZ(5) PZ(6) PZ(7) PZ(8) PZ(9) PZ(10) PZ(11) PZ(12) PZ(13) PZ(14) PZ(15) PZ(16)
