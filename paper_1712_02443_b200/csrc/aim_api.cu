@@ -180,7 +180,7 @@ static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, co
     p->base = upload(p, base);
     p->node0 = upload(p, node0);
     for (int d = 0; d < 3; ++d) make_fft_axis(p->pads[d], p->ax[d]);
-    p->planar = planar_supported(p->pads[1], p->dims[2]) ? 1 : 0;
+    p->planar = planar_supported(p->pads[1], p->dims[2], p->ax[1].min_radix) ? 1 : 0;
 
     // ---- device setup S2-S4
     cudaStream_t s = p->stream;

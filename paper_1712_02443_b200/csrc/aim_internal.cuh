@@ -43,6 +43,7 @@ struct FftAxis {
     int nst = 0;                     // number of Stockham stages
     int radix[kMaxStages] = {0};     // radices, product == P
     unsigned long long nsM[kMaxStages] = {0};  // ceil(2^40 / Ns) of each stage (fast divide)
+    int min_radix = 1;                          // smallest stage radix
     double2* tw = nullptr;           // device twiddles exp(-2 pi i e / P), e in [0,P)
 };
 
@@ -76,7 +77,7 @@ struct PlanarPass {
 
 void launch_fft_pass(const FftPass& p, cudaStream_t s);
 void launch_planar_yz(const PlanarPass& p, cudaStream_t s);
-bool planar_supported(int Py, int Nz);
+bool planar_supported(int Py, int Nz, int min_radix);
 void make_fft_axis(int P, FftAxis& ax);    // factorisation + device twiddles
 int smooth_size_at_least(int n);           // smallest 2^a 3^b 5^c 7^d >= n
 

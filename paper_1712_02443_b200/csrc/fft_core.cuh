@@ -201,6 +201,69 @@ __device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const do
     return src;
 }
 
+// In-place variant: every thread owns at most ONE butterfly per stage (the
+// host guarantees NL * P / min_radix <= blockDim), so a stage is
+// load-to-registers, barrier, compute, store -- a single shared buffer.
+// One fixed register array serves every radix (kept out of the switch so it
+// stays in registers across the barrier).
+template <int R>
+__device__ __forceinline__ void ip_load(double2* a, const double2* __restrict__ buf, int B, int NL, int j, int l) {
+#pragma unroll
+    for (int t = 0; t < R; ++t) a[t] = buf[(j + t * B) * NL + l];
+}
+
+template <int R>
+__device__ __forceinline__ void ip_store(double2* a, double2* __restrict__ buf, const double2* __restrict__ tw, int P,
+                                         int NL, int Ns, unsigned long long nsM, double sign, int j, int l) {
+    const int stride = P / (Ns * R);
+    const int jd = fdiv(j, nsM);
+    const int k = j - jd * Ns;
+    if (k) {
+#pragma unroll
+        for (int t = 1; t < R; ++t) {
+            double2 w = tw[t * k * stride];
+            if (sign > 0) w.y = -w.y;
+            a[t] = cmul(a[t], w);
+        }
+    }
+    dft<R>(a, sign);
+    const int base = jd * Ns * R + k;
+#pragma unroll
+    for (int u = 0; u < R; ++u) buf[(base + u * Ns) * NL + l] = a[u];
+}
+
+__device__ __forceinline__ void fft_lines_inplace(double2* buf, const double2* tw, const FftAxis& ax, int NL,
+                                                  double sign, const LineMap& lm) {
+    int Ns = 1;
+    for (int s = 0; s < ax.nst; ++s) {
+        const int R = ax.radix[s];
+        const int B = ax.P / R;
+        const int j = lm.js;
+        const bool mine = lm.active && j < B;
+        double2 a[16];
+        if (mine) {
+            switch (R) {
+#define AIM_LD(RR) case RR: ip_load<RR>(a, buf, B, NL, j, lm.l); break;
+                AIM_LD(2) AIM_LD(3) AIM_LD(4) AIM_LD(5) AIM_LD(6) AIM_LD(7) AIM_LD(8)
+                AIM_LD(9) AIM_LD(10) AIM_LD(12) AIM_LD(14) AIM_LD(15) AIM_LD(16)
+#undef AIM_LD
+            }
+        }
+        __syncthreads();
+        if (mine) {
+            const unsigned long long M = ax.nsM[s];
+            switch (R) {
+#define AIM_ST(RR) case RR: ip_store<RR>(a, buf, tw, ax.P, NL, Ns, M, sign, j, lm.l); break;
+                AIM_ST(2) AIM_ST(3) AIM_ST(4) AIM_ST(5) AIM_ST(6) AIM_ST(7) AIM_ST(8)
+                AIM_ST(9) AIM_ST(10) AIM_ST(12) AIM_ST(14) AIM_ST(15) AIM_ST(16)
+#undef AIM_ST
+            }
+        }
+        __syncthreads();
+        Ns *= R;
+    }
+}
+
 // Complex elements per ping-pong buffer of one CTA (2 buffers + twiddles ~ 70 KB
 // -> 3 CTAs of 256 threads per SM).
 __host__ __device__ constexpr int fft_tile_capacity() { return 2304; }

@@ -21,14 +21,15 @@
 
 namespace aim {
 
-__global__ void __launch_bounds__(256, 3) fft_pass_kernel(FftPass p) {
+template <bool INPLACE>
+__global__ void __launch_bounds__(256, 2) fft_pass_kernel(FftPass p) {
     extern __shared__ double2 sm[];
     const int P = p.ax.P;
     const int TO = p.TO, TI = p.TI;
     const int NL = TO * TI;
     double2* buf = sm;
-    double2* alt = sm + (size_t)P * NL;
-    double2* tw = sm + (size_t)2 * P * NL;
+    double2* alt = INPLACE ? sm : sm + (size_t)P * NL;
+    double2* tw = sm + (size_t)(INPLACE ? 1 : 2) * P * NL;
 
     const long long tilesI = (p.inner + TI - 1) / TI;
     const long long o0 = (long long)(blockIdx.x / tilesI) * TO;
@@ -57,11 +58,13 @@ __global__ void __launch_bounds__(256, 3) fft_pass_kernel(FftPass p) {
     }
     __syncthreads();
 
-    double2* res;
+    double2* res = buf;
     if (p.mode == 1) {
-        res = fft_lines(buf, alt, tw, p.ax, NL, +1.0, lm);
+        if (INPLACE) fft_lines_inplace(buf, tw, p.ax, NL, +1.0, lm);
+        else res = fft_lines(buf, alt, tw, p.ax, NL, +1.0, lm);
     } else {
-        res = fft_lines(buf, alt, tw, p.ax, NL, -1.0, lm);
+        if (INPLACE) fft_lines_inplace(buf, tw, p.ax, NL, -1.0, lm);
+        else res = fft_lines(buf, alt, tw, p.ax, NL, -1.0, lm);
         if (p.mode == 2) {
             // x spectrum: line (o, i) belongs to outer og = (c Px + kx) Py + ky; kz = j
             if (lm.active) {
@@ -73,7 +76,8 @@ __global__ void __launch_bounds__(256, 3) fft_pass_kernel(FftPass p) {
                 for (int j = lm.js; j < P; j += lm.JS) res[j * NL + lm.l] = cmul(res[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
             }
             __syncthreads();
-            res = fft_lines(res, res == buf ? alt : buf, tw, p.ax, NL, +1.0, lm);
+            if (INPLACE) fft_lines_inplace(res, tw, p.ax, NL, +1.0, lm);
+            else res = fft_lines(res, res == buf ? alt : buf, tw, p.ax, NL, +1.0, lm);
         }
     }
     // tile store with fused pruning
@@ -94,8 +98,7 @@ __global__ void __launch_bounds__(kPlanarThreads, 2) planar_yz_kernel(PlanarPass
     const int RC = p.RC;
     const int NL = NZ * RC;
     double2* buf = sm;
-    double2* alt = sm + (size_t)Py * NL;
-    double2* tw = sm + (size_t)2 * Py * NL;
+    double2* tw = sm + (size_t)Py * NL;
     const int nchunk = (p.R + RC - 1) / RC;
     const long long plane = blockIdx.x / nchunk;
     const int r0 = (int)(blockIdx.x % nchunk) * RC;
@@ -121,8 +124,9 @@ __global__ void __launch_bounds__(kPlanarThreads, 2) planar_yz_kernel(PlanarPass
             buf[y * NL + lm.l] = (live && y < p.Ny) ? __ldcs(W + y * ystride) : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    double2* res = fft_lines(buf, alt, tw, p.ay, NL, -1.0, lm);
-    double2* oth = res == buf ? alt : buf;
+    fft_lines_inplace(buf, tw, p.ay, NL, -1.0, lm);
+    double2* res = buf;
+    double2* oth = buf;   // each z line is read into registers and rewritten by one thread
     // z: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for every (ky, rl), one
     // line per thread, all indices compile-time (G2 row and inputs in registers),
     // symmetric Toeplitz: out[z] = g0 in[z] + sum_{d>0} g_d (in[z-d] + in[z+d]).
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(kPlanarThreads, 2) planar_yz_kernel(PlanarPass
         }
     }
     __syncthreads();
-    res = fft_lines(oth, res, tw, p.ay, NL, +1.0, lm);
+    fft_lines_inplace(buf, tw, p.ay, NL, +1.0, lm);
     if (live)
         for (int y = lm.js; y < p.Ny; y += lm.JS) __stcs(W + y * ystride, res[y * NL + lm.l]);
 }
@@ -210,6 +214,8 @@ void make_fft_axis(int P, FftAxis& ax) {
     if (P > 1 && best.empty()) throw Error(AIM_E_GRID, "FFT size not 7-smooth");
     if ((int)best.size() > kMaxStages) throw Error(AIM_E_GRID, "too many FFT stages");
     for (int r : best) ax.radix[ax.nst++] = r;
+    ax.min_radix = P;
+    for (int r : best) ax.min_radix = std::min(ax.min_radix, r);
     long long Ns = 1;
     for (int st = 0; st < ax.nst; ++st) {
         ax.nsM[st] = ((1ULL << 40) + (unsigned long long)Ns - 1) / (unsigned long long)Ns;
@@ -229,8 +235,11 @@ static constexpr int kFftThreads = 256;
 void launch_fft_pass(const FftPass& p0, cudaStream_t s) {
     FftPass p = p0;
     const int P = p.ax.P;
+    // in place when one butterfly per thread per stage suffices for >= 4 lines
+    const int nl_inplace = kFftThreads * p.ax.min_radix / P;
+    const bool inplace = nl_inplace >= 2;
     const int cap = std::max(fft_tile_capacity(), P);
-    const int nl = std::max(1, cap / P);
+    const int nl = inplace ? nl_inplace : std::max(1, cap / P);
     if (p.TI <= 0) {
         // TI: power of two (coalesced rows of TI*16 bytes); TO fills the tile
         long long ti = 1;
@@ -244,29 +253,35 @@ void launch_fft_pass(const FftPass& p0, cudaStream_t s) {
     const long long tilesO = (p.outer + p.TO - 1) / p.TO;
     const long long grid = tilesI * tilesO;
     if (grid <= 0) return;
-    const size_t smem = sizeof(double2) * ((size_t)2 * P * p.TO * p.TI + P);
+    const size_t smem = sizeof(double2) * ((size_t)(inplace ? 1 : 2) * P * p.TO * p.TI + P);
     if (smem > 227 * 1024) throw Error(AIM_E_GRID, "FFT length exceeds the shared-memory tile capacity");
     static bool attr = false;
     if (!attr) {
-        AIM_CUDA(cudaFuncSetAttribute(fft_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        AIM_CUDA(cudaFuncSetAttribute(fft_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        AIM_CUDA(cudaFuncSetAttribute(fft_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
-    fft_pass_kernel<<<(unsigned)grid, kFftThreads, smem, s>>>(p);
+    if (inplace) fft_pass_kernel<true><<<(unsigned)grid, kFftThreads, smem, s>>>(p);
+    else fft_pass_kernel<false><<<(unsigned)grid, kFftThreads, smem, s>>>(p);
     note_launch("fft_pass");
 }
 
-bool planar_supported(int Py, int Nz) { return Nz <= kPlanarMaxNz && Py * Nz <= 2 * fft_tile_capacity(); }
+// planar pass: one CTA holds a (Py x Nz) plane in place, one butterfly per thread per stage
+bool planar_supported(int Py, int Nz, int min_radix) {
+    return Nz <= kPlanarMaxNz && (long long)Nz * Py / min_radix <= kPlanarThreads && Py * Nz * 16 <= 200 * 1024;
+}
 
 void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
     PlanarPass p = p0;
     const int Py = p.ay.P;
-    const int cap = 2 * fft_tile_capacity();
-    p.RC = std::max(1, std::min({p.R, cap / (Py * p.Nz), kPlanarThreads / p.Nz}));
+    const int rc_fft = (int)(kPlanarThreads * (long long)p.ay.min_radix / ((long long)Py * p.Nz));
+    p.RC = std::max(1, std::min({p.R, rc_fft, kPlanarThreads / p.Nz}));
     const long long nchunk = (p.R + p.RC - 1) / p.RC;
     const long long grid = 4LL * p.Px * nchunk;
     // one z line per thread in the convolution step; NL lines for the FFT stages
-    const int threads = std::max(32 * ((p.Nz * p.RC + 31) / 32), std::min(kPlanarThreads, 32 * ((Py * p.RC + 31) / 32)));
-    const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py);
+    const int bfly = (int)((long long)p.Nz * p.RC * Py / p.ay.min_radix);   // butterflies per stage (max)
+    const int threads = std::min(kPlanarThreads, 32 * ((std::max({bfly, Py * p.RC, p.Nz * p.RC}) + 31) / 32));
+    const size_t smem = sizeof(double2) * ((size_t)Py * p.Nz * p.RC + Py);
     switch (p.Nz) {
 #define PZ(NZ)                                                                                              \
     case NZ: {                                                                                              \
