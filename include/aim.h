@@ -182,15 +182,16 @@ enum {
 int aim_plan_export(const aim_plan* plan, int32_t what, void* dst, int64_t bytes);
 
 /* ---- live stage timing (bench accounting) ------------------------------- */
-/* Stage ids of one aim_matvec, in launch order. */
+/* Stage ids of one aim_matvec (all on the caller's stream; launch order:
+ * NEAR, PROJECT, FFT_X, FFT_YZ, IFFT_X, INTERP). */
 enum {
-    AIM_STAGE_PROJECT = 0,   /* H1 projection gather (main stream)                   */
+    AIM_STAGE_PROJECT = 0,   /* H1 projection gather                                 */
     AIM_STAGE_FFT_X = 1,     /* H2 x forward pass, zero-pad fused                    */
     AIM_STAGE_FFT_YZ = 2,    /* H2-H4 y fwd, z convolution x spectrum, y inv         */
     AIM_STAGE_IFFT_X = 3,    /* H4 x inverse pass, pruned                            */
-    AIM_STAGE_NEAR_WAIT = 4, /* main stream waiting for the near SpMV (0 if hidden)  */
+    AIM_STAGE_NEAR_WAIT = 4, /* (unused: 0)                                          */
     AIM_STAGE_INTERP = 5,    /* H5 interpolation, adds the far field to y            */
-    AIM_STAGE_NEAR = 6,      /* H6 near-field SpMV on the side stream (overlaps 0-3) */
+    AIM_STAGE_NEAR = 6,      /* H6 near-field SpMV, writes y                         */
     AIM_NUM_STAGES = 7
 };
 /* enable != 0: every subsequent aim_matvec records CUDA events around each

@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaim_b200.so")
+LIB_PATH = os.environ.get("AIM_LIB") or os.path.join(HERE, "libaim_b200.so")
 
 
 class AimInfo(ctypes.Structure):

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <string>
@@ -26,6 +27,12 @@ void note_launch(const char* name) {
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(AIM_E_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+    // AIM_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel
+    static const bool sync_debug = getenv("AIM_SYNC_DEBUG") && getenv("AIM_SYNC_DEBUG")[0] == '1';
+    if (sync_debug) {
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) throw Error(AIM_E_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+    }
 }
 
 static int fail(int status, const std::string& msg) {
@@ -393,7 +400,7 @@ int aim_profile_read(aim_plan* p, double* ms, int64_t* count) {
         const size_t per = kProfEvents;
         if (p->ev_used % per) throw Error(AIM_E_ARG, "profiling events out of step");
         // (from, to) event slots of each stage, see matvec() in k_matvec.cu
-        static const int from[AIM_NUM_STAGES] = {0, 1, 2, 3, 4, 5, 7};
+        static const int from[AIM_NUM_STAGES] = {8, 1, 2, 3, 4, 5, 7};
         static const int to[AIM_NUM_STAGES] = {1, 2, 3, 4, 5, 6, 8};
         for (size_t b = 0; b < p->ev_used; b += per) {
             AIM_CUDA(cudaEventSynchronize(p->ev_pool[b + 6]));

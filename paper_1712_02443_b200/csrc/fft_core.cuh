@@ -15,6 +15,9 @@
 #include "aim_internal.cuh"
 
 namespace aim {
+#ifdef AIM_BOUNDS_DEBUG
+__device__ int g_aim_dbg = 0;
+#endif
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -232,6 +235,8 @@ __device__ __forceinline__ void ip_store(double2* a, double2* __restrict__ buf, 
     for (int u = 0; u < R; ++u) buf[(base + u * Ns) * NL + l] = a[u];
 }
 
+// In-place transform with runtime radices (fallback for sizes without a
+// compile-time plan): every thread owns at most ONE butterfly per stage.
 __device__ __forceinline__ void fft_lines_inplace(double2* buf, const double2* tw, const FftAxis& ax, int NL,
                                                   double sign, const LineMap& lm) {
     int Ns = 1;
@@ -263,6 +268,78 @@ __device__ __forceinline__ void fft_lines_inplace(double2* buf, const double2* t
         Ns *= R;
     }
 }
+
+template <int... Rs>
+struct MinOf;
+template <int R>
+struct MinOf<R> { static constexpr int v = R; };
+template <int R, int... Rs>
+struct MinOf<R, Rs...> { static constexpr int v = R < MinOf<Rs...>::v ? R : MinOf<Rs...>::v; };
+
+// ------------------------------------------- compile-time ping-pong plans
+// Stockham stage src -> dst with compile-time P, Ns, R, line count NL and
+// thread count T: each thread walks butterflies j = tid/NL, += T/NL (one
+// butterfly live at a time: no register array survives a barrier).
+template <int P, int Ns, int R, int SIGN, int NL, int T>
+__device__ __forceinline__ void ctp_stage(const double2* src, double2* dst, const double2* tw) {
+    constexpr double sign = SIGN;
+    constexpr int B = P / R;
+    constexpr int stride = P / (Ns * R);
+    constexpr int JS = T / NL;
+    const int l = threadIdx.x % NL;
+    int j = threadIdx.x / NL;
+    if (j < JS) {
+#pragma unroll 1
+        for (; j < B; j += JS) {
+            double2 a[R];
+            const double2* sp = src + j * NL + l;   // + t * B * NL
+#pragma unroll
+            for (int t = 0; t < R; ++t) a[t] = sp[t * B * NL];
+#ifdef AIM_BOUNDS_DEBUG
+            if (!((j + (R - 1) * B) * NL + l < P * NL)) atomicCAS(&g_aim_dbg, 0, 201);
+#endif
+            const int jd = j / Ns;
+            const int k = j - jd * Ns;
+            if (Ns > 1 && k) {
+#pragma unroll
+                for (int t = 1; t < R; ++t) {
+                    double2 w = tw[t * k * stride];   // exp(-2 pi i t k stride / P)
+                    if (sign > 0) w.y = -w.y;
+                    a[t] = cmul(a[t], w);
+                }
+            }
+            dft<R>(a, sign);
+            double2* dp = dst + (jd * Ns * R + k) * NL + l;   // + u * Ns * NL
+#ifdef AIM_BOUNDS_DEBUG
+            if (!((jd * Ns * R + k + (R - 1) * Ns) * NL + l < P * NL)) atomicCAS(&g_aim_dbg, 0, 202);
+            if (Ns > 1 && k && !((R - 1) * k * stride < P)) atomicCAS(&g_aim_dbg, 0, 203);
+#endif
+#pragma unroll
+            for (int u = 0; u < R; ++u) dp[u * Ns * NL] = a[u];
+        }
+    }
+    __syncthreads();
+}
+
+// Stages alternate a -> b -> a ...; returns the buffer holding the result.
+template <int SIGN, int NL, int T, int P, int Ns, int R, int... Rs>
+__device__ __forceinline__ double2* ctp_fft(double2* a, double2* b, const double2* tw) {
+    ctp_stage<P, Ns, R, SIGN, NL, T>(a, b, tw);
+    if constexpr (sizeof...(Rs) > 0) return ctp_fft<SIGN, NL, T, P, Ns * R, Rs...>(b, a, tw);
+    else return b;
+}
+
+template <int NL_, int T_, int P_, int... Rs>
+struct CtpPlan {
+    static constexpr int P = P_;
+    static constexpr int NL = NL_;
+    static constexpr int T = T_;
+    static constexpr int min_radix = MinOf<Rs...>::v;
+    template <int SIGN>
+    __device__ __forceinline__ static double2* run(double2* a, double2* b, const double2* tw) {
+        return ctp_fft<SIGN, NL, T, P, 1, Rs...>(a, b, tw);
+    }
+};
 
 // Complex elements per ping-pong buffer of one CTA (2 buffers + twiddles ~ 70 KB
 // -> 3 CTAs of 256 threads per SM).

@@ -19,17 +19,335 @@
 
 #include "fft_core.cuh"
 
+#ifdef AIM_BOUNDS_DEBUG
+#define AIM_CHK(cond, code) do { if (!(cond)) { atomicCAS(&g_aim_dbg, 0, (code)); } } while (0)
+#else
+#define AIM_CHK(cond, code) do { } while (0)
+#endif
+
 namespace aim {
 
-template <bool INPLACE>
-__global__ void __launch_bounds__(256, 2) fft_pass_kernel(FftPass p) {
+// ---------------------------------------------------------- async copies
+// cp.async 16 B global -> shared; valid == false zero-fills the 16 bytes
+// (src-size 0: nothing is read), which is how zero padding is fused in.
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Runtime radices and line count (any 7-smooth length without a compile-time
+// plan; in place, one butterfly per thread per stage).
+struct RtPlan {
+    static constexpr int P = 0;
+    static constexpr int NL = 0;
+    static constexpr bool compile_time = false;
+    template <int SIGN>
+    __device__ __forceinline__ static void run(double2* buf, const double2* tw, const FftAxis& ax, int NL) {
+        const LineMap lm(NL);
+        fft_lines_inplace(buf, tw, ax, NL, (double)SIGN, lm);
+    }
+};
+
+// contiguous, balanced range of tiles for this CTA (persistent grid)
+__device__ __forceinline__ void tile_range(int tiles, int& t0, int& t1) {
+    const int per = tiles / (int)gridDim.x, extra = tiles % (int)gridDim.x;
+    t0 = (int)blockIdx.x * per + min((int)blockIdx.x, extra);
+    t1 = t0 + per + ((int)blockIdx.x < extra ? 1 : 0);
+}
+
+// Compile-time ping-pong plans (CtpPlan<lines, threads, P, radices...>) of the
+// lengths the BASELINE configs use; other lengths run the runtime-radix
+// kernels.  Radices <= 7: one butterfly's registers stay small.
+using Ct210 = CtpPlan<8, 336, 210, 7, 6, 5>;      // x passes of C2: 8 lines (128 B rows)
+using Ct24 = CtpPlan<32, 192, 24, 6, 4>;          // x passes of C1 (1 RHS): 32 lines
+using Ct210z11 = CtpPlan<11, 480, 210, 7, 6, 5>;  // planar y/z of C2, one RHS per tile
+using Ct24z7 = CtpPlan<7, 64, 24, 6, 4>;          // planar y/z of C1, one RHS per tile
+
+// ------------------------------------------------------ generic axis pass
+// Persistent CTAs walk a contiguous range of (outer x inner) tiles; tile t+1
+// is fetched with cp.async into the second buffer while tile t is
+// transformed in place (one butterfly per thread per stage) and stored.
+// Tile indices are 32-bit and advanced incrementally (no 64-bit divides:
+// their call sequences pin registers and cause spills).
+template <class F, int MODE, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int tiles) {
+    extern __shared__ double2 sm[];
+    const int P = F::compile_time ? F::P : p.ax.P;
+    const int TO = p.TO, TI = p.TI, NL = F::compile_time ? F::NL : TO * TI;
+    double2* tw = sm;
+    double2* const buf0 = sm + P;
+    double2* const buf1 = sm + P + (size_t)P * NL;
+    const int outer = (int)p.outer, inner = (int)p.inner;
+    const int tilesI = (inner + TI - 1) / TI;
+    const LineMap lm(NL);
+    const int o = lm.l / TI, i = lm.l - (lm.l / TI) * TI;
+    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = p.ax.tw[e];
+    int t0, t1;
+    tile_range(tiles, t0, t1);
+    if (t0 >= t1) return;
+
+    // (ot, it) = tile coordinates of the tile being loaded
+    int ot = t0 / tilesI, itl = t0 - (t0 / tilesI) * tilesI;
+    auto issue = [&](double2* buf) {
+        if (!lm.active) return;
+        const int oo = ot * TO + o, ii = itl * TI + i;
+        const bool live = oo < outer && ii < inner;
+        const double2* src = p.in + (live ? (long long)oo * p.Lin * inner + ii : 0);
+#pragma unroll 4
+        for (int j = lm.js; j < P; j += lm.JS) {
+            const bool v = live && j < p.Lin;
+            cp_async16(&buf[j * NL + lm.l], v ? src + (long long)j * inner : p.in, v);
+        }
+    };
+    auto advance = [&]() {
+        if (++itl == tilesI) { itl = 0; ++ot; }
+    };
+    issue(buf0);
+    cp_commit();
+    int cur_o = ot, cur_i = itl;   // coordinates of the tile being computed
+    advance();
+    for (int t = t0; t < t1; ++t) {
+        const bool odd = (t - t0) & 1;
+        double2* buf = odd ? buf1 : buf0;
+        if (t + 1 < t1) issue(odd ? buf0 : buf1);
+        cp_commit();
+        cp_wait_prev();
+        __syncthreads();
+        if constexpr (MODE == 1) {
+            F::template run<+1>(buf, tw, p.ax, NL);
+        } else {
+            F::template run<-1>(buf, tw, p.ax, NL);
+            if constexpr (MODE == 2) {
+                // x spectrum: line (o, i) belongs to outer og = (c Px + kx) Py + ky; kz = j
+                if (lm.active) {
+                    const int og = min(cur_o * TO + o, outer - 1);
+                    const int ky = og % p.Py;
+                    const int kx = (og / p.Py) % p.Px;
+                    const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
+                    const double2* g = p.spec + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                    for (int j = lm.js; j < P; j += lm.JS)
+                        buf[j * NL + lm.l] = cmul(buf[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
+                }
+                __syncthreads();
+                F::template run<+1>(buf, tw, p.ax, NL);
+            }
+        }
+        // tile store with fused pruning
+        const int oo = cur_o * TO + o, ii = cur_i * TI + i;
+        if (lm.active && oo < outer && ii < inner) {
+            double2* dst = p.out + (long long)oo * p.Lout * inner + ii;
+#pragma unroll 4
+            for (int j = lm.js; j < p.Lout; j += lm.JS) __stcs(dst + (long long)j * inner, buf[j * NL + lm.l]);
+        }
+        cur_o = ot;
+        cur_i = itl;
+        advance();
+        __syncthreads();
+    }
+}
+
+// z step of the planar pass: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for
+// every (ky, rl), one line per thread, all indices compile-time (inputs in
+// registers), symmetric Toeplitz: out[z] = g0 in[z] + sum_{d>0} g_d (in[z-d] + in[z+d]).
+template <int NZ>
+__device__ __forceinline__ void planar_toeplitz(double2* buf, const double2* g2, int Py, int RC, int NL) {
+#pragma unroll 1
+    for (int line = threadIdx.x; line < Py * RC; line += blockDim.x) {
+        const int ky = line / RC, rr = line - (line / RC) * RC;
+        const int ay = min(ky, Py - ky);
+        const double2* g = g2 + ay * NZ;
+        double2* row = buf + ky * NL + rr;   // + zz * RC
+        double2 in[NZ];
+#pragma unroll
+        for (int zz = 0; zz < NZ; ++zz) in[zz] = row[zz * RC];
+#pragma unroll
+        for (int zz = 0; zz < NZ; ++zz) {
+            double2 acc = cmul(g[0], in[zz]);
+#pragma unroll
+            for (int d = 1; d < NZ; ++d) {
+                if (zz - d < 0 && zz + d >= NZ) continue;
+                double2 sum = zz - d >= 0 ? in[zz - d] : make_double2(0.0, 0.0);
+                if (zz + d < NZ) sum = zz - d >= 0 ? cadd(sum, in[zz + d]) : in[zz + d];
+                const double2 gd = g[d];
+                acc.x = fma(gd.x, sum.x, fma(-gd.y, sum.y, acc.x));
+                acc.y = fma(gd.x, sum.y, fma(gd.y, sum.x, acc.y));
+            }
+            row[zz * RC] = acc;
+        }
+    }
+}
+
+// --------------------------------------------- compile-time pass kernels
+// Persistent CTAs, three tile buffers: X holds the tile being transformed, Y
+// is the ping-pong scratch, Z receives the next tile by cp.async; X and Z
+// swap after every tile.  All sizes compile-time (F::P, F::NL, F::T).
+template <class F, int MODE, int MINB>
+__global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles) {
+    constexpr int P = F::P, NL = F::NL, T = F::T, JS = T / NL;
+    extern __shared__ double2 sm[];
+    double2* tw = sm;
+    double2* X = sm + P;
+    double2* Y = X + P * NL;
+    double2* Z = Y + P * NL;
+    const int TI = p.TI;
+    const int outer = (int)p.outer, inner = (int)p.inner;
+    const int tilesI = (inner + TI - 1) / TI;
+    const int l = threadIdx.x % NL, js = threadIdx.x / NL;
+    const bool act = js < JS;
+    const int o = l / TI, i = l - (l / TI) * TI;
+    for (int e = threadIdx.x; e < P; e += T) tw[e] = p.ax.tw[e];
+    int t0, t1;
+    tile_range(tiles, t0, t1);
+    if (t0 >= t1) return;
+    int ot = t0 / tilesI, itl = t0 - (t0 / tilesI) * tilesI;
+    auto issue = [&](double2* buf) {
+        if (!act) return;
+        const int oo = ot * (NL / TI) + o, ii = itl * TI + i;
+        const bool live = oo < outer && ii < inner;
+        const double2* src = p.in + (live ? (long long)oo * p.Lin * inner + ii : 0);
+#pragma unroll 2
+        for (int j = js; j < P; j += JS) {
+            const bool v = live && j < p.Lin;
+            cp_async16(&buf[j * NL + l], v ? src + (long long)j * inner : p.in, v);
+        }
+    };
+    auto advance = [&]() {
+        if (++itl == tilesI) { itl = 0; ++ot; }
+    };
+    issue(X);
+    cp_commit();
+    int cur_o = ot, cur_i = itl;
+    advance();
+    for (int t = t0; t < t1; ++t) {
+        if (t + 1 < t1) issue(Z);
+        cp_commit();
+        cp_wait_prev();
+        __syncthreads();
+        double2* res;
+        if constexpr (MODE == 1) {
+            res = F::template run<+1>(X, Y, tw);
+        } else {
+            res = F::template run<-1>(X, Y, tw);
+            if constexpr (MODE == 2) {
+                if (act) {
+                    const int og = min(cur_o * (NL / TI) + o, outer - 1);
+                    const int ky = og % p.Py;
+                    const int kx = (og / p.Py) % p.Px;
+                    const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
+                    const double2* g = p.spec + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                    for (int j = js; j < P; j += JS) res[j * NL + l] = cmul(res[j * NL + l], __ldg(&g[min(j, P - j)]));
+                }
+                __syncthreads();
+                res = F::template run<+1>(res, res == X ? Y : X, tw);
+            }
+        }
+        const int oo = cur_o * (NL / TI) + o, ii = cur_i * TI + i;
+        if (act && oo < outer && ii < inner) {
+            double2* dst = p.out + (long long)oo * p.Lout * inner + ii;
+#pragma unroll 2
+            for (int j = js; j < p.Lout; j += JS) __stcs(dst + (long long)j * inner, res[j * NL + l]);
+        }
+        cur_o = ot;
+        cur_i = itl;
+        advance();
+        double2* tmp = X;
+        X = Z;
+        Z = tmp;
+        __syncthreads();
+    }
+}
+
+template <int NZ, class F, int MINB>
+__global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int tiles) {
+    constexpr int Py = F::P, NL = F::NL, T = F::T, JS = T / NL;
+    static_assert(NL == NZ, "one RHS per tile");
+    extern __shared__ double2 sm[];
+    double2* tw = sm;
+    double2* g2 = sm + Py;
+    double2* X = g2 + (Py / 2 + 1) * NZ;
+    double2* Y = X + Py * NL;
+    double2* Z = Y + Py * NL;
+    const int nchunk = p.R;
+    const int l = threadIdx.x % NL, js = threadIdx.x / NL;   // l = z
+    const bool act = js < JS;
+    const int ystride = NZ * p.R;
+    for (int e = threadIdx.x; e < Py; e += T) tw[e] = p.ay.tw[e];
+    int t0, t1;
+    tile_range(tiles, t0, t1);
+    if (t0 >= t1) return;
+    int lkx = t0 / (4 * nchunk), lc = (t0 / nchunk) % 4, lch = t0 % nchunk;
+    auto base_of = [&](int kx, int c, int r) -> double2* {
+        const long long plane = (long long)c * p.Px + kx;
+        return p.W + plane * p.Ny * ystride + l * p.R + r;   // + y * ystride
+    };
+    auto issue = [&](double2* buf) {
+        if (!act) return;
+        const double2* src = base_of(lkx, lc, lch);
+#pragma unroll 2
+        for (int y = js; y < Py; y += JS) {
+            const bool v = y < p.Ny;
+            AIM_CHK(!v || (src + y * ystride - p.W) < 4LL * p.Px * p.Ny * ystride, 101);
+            AIM_CHK(y * NL + l < Py * NL, 102);
+            cp_async16(&buf[y * NL + l], v ? src + y * ystride : p.W, v);
+        }
+    };
+    auto advance = [&]() {
+        if (++lch == nchunk) {
+            lch = 0;
+            if (++lc == 4) { lc = 0; ++lkx; }
+        }
+    };
+    issue(X);
+    cp_commit();
+    int ckx = lkx, cc = lc, cch = lch;
+    advance();
+    int cur_ax = -1;
+    for (int t = t0; t < t1; ++t) {
+        if (t + 1 < t1) issue(Z);
+        cp_commit();
+        cp_wait_prev();
+        const int ax_ = min(ckx, p.Px - ckx);
+        if (ax_ != cur_ax) {   // uniform: G2 slice of this kx (rare: tiles are kx-major)
+            const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
+            AIM_CHK(ax_ >= 0 && ax_ <= p.Px / 2, 104);
+            for (int e = threadIdx.x; e < p.PyH * NZ; e += T) g2[e] = __ldg(&G2[e]);
+            cur_ax = ax_;
+        }
+        __syncthreads();
+        double2* res = F::template run<-1>(X, Y, tw);
+        planar_toeplitz<NZ>(res, g2, Py, 1, NL);
+        __syncthreads();
+        res = F::template run<+1>(res, res == X ? Y : X, tw);
+        if (act) {
+            double2* dst = base_of(ckx, cc, cch);
+#pragma unroll 2
+            for (int y = js; y < p.Ny; y += JS) {
+                AIM_CHK((dst + y * ystride - p.W) < 4LL * p.Px * p.Ny * ystride && dst + y * ystride >= p.W, 103);
+                __stcs(dst + y * ystride, res[y * NL + l]);
+            }
+        }
+        ckx = lkx; cc = lc; cch = lch;
+        advance();
+        double2* tmp = X;
+        X = Z;
+        Z = tmp;
+        __syncthreads();
+    }
+}
+
+// Ping-pong fallback (lines too long for one butterfly per thread): one tile
+// per CTA, two buffers.
+__global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
     extern __shared__ double2 sm[];
     const int P = p.ax.P;
     const int TO = p.TO, TI = p.TI;
     const int NL = TO * TI;
     double2* buf = sm;
-    double2* alt = INPLACE ? sm : sm + (size_t)P * NL;
-    double2* tw = sm + (size_t)(INPLACE ? 1 : 2) * P * NL;
+    double2* alt = sm + (size_t)P * NL;
+    double2* tw = sm + (size_t)2 * P * NL;
 
     const long long tilesI = (p.inner + TI - 1) / TI;
     const long long o0 = (long long)(blockIdx.x / tilesI) * TO;
@@ -42,31 +360,21 @@ __global__ void __launch_bounds__(256, 2) fft_pass_kernel(FftPass p) {
     const double2* src = p.in + (o0 + o) * p.Lin * p.inner + i0 + i;
 
     for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = p.ax.tw[e];
-    // tile load with fused zero padding: line l = (o, i), rows j
-    if (lm.active) {
-        int j = lm.js;
-        for (; j + 3 * lm.JS < p.Lin; j += 4 * lm.JS) {
-            double2 v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                v[q] = live ? __ldcs(src + (long long)(j + q * lm.JS) * p.inner) : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) buf[(j + q * lm.JS) * NL + lm.l] = v[q];
+    if (lm.active)
+        for (int j = lm.js; j < P; j += lm.JS) {
+            const bool v = live && j < p.Lin;
+            cp_async16(&buf[j * NL + lm.l], v ? src + (long long)j * p.inner : p.in, v);
         }
-        for (; j < P; j += lm.JS)
-            buf[j * NL + lm.l] = (live && j < p.Lin) ? __ldcs(src + (long long)j * p.inner) : make_double2(0.0, 0.0);
-    }
+    cp_commit();
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
 
     double2* res = buf;
     if (p.mode == 1) {
-        if (INPLACE) fft_lines_inplace(buf, tw, p.ax, NL, +1.0, lm);
-        else res = fft_lines(buf, alt, tw, p.ax, NL, +1.0, lm);
+        res = fft_lines(buf, alt, tw, p.ax, NL, +1.0, lm);
     } else {
-        if (INPLACE) fft_lines_inplace(buf, tw, p.ax, NL, -1.0, lm);
-        else res = fft_lines(buf, alt, tw, p.ax, NL, -1.0, lm);
+        res = fft_lines(buf, alt, tw, p.ax, NL, -1.0, lm);
         if (p.mode == 2) {
-            // x spectrum: line (o, i) belongs to outer og = (c Px + kx) Py + ky; kz = j
             if (lm.active) {
                 const long long og = o0 + min(o, to_n - 1);
                 const int ky = (int)(og % p.Py);
@@ -76,11 +384,9 @@ __global__ void __launch_bounds__(256, 2) fft_pass_kernel(FftPass p) {
                 for (int j = lm.js; j < P; j += lm.JS) res[j * NL + lm.l] = cmul(res[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
             }
             __syncthreads();
-            if (INPLACE) fft_lines_inplace(res, tw, p.ax, NL, +1.0, lm);
-            else res = fft_lines(res, res == buf ? alt : buf, tw, p.ax, NL, +1.0, lm);
+            res = fft_lines(res, res == buf ? alt : buf, tw, p.ax, NL, +1.0, lm);
         }
     }
-    // tile store with fused pruning
     if (live) {
         double2* dst = p.out + (o0 + o) * p.Lout * p.inner + i0 + i;
         for (int j = lm.js; j < p.Lout; j += lm.JS) __stcs(dst + (long long)j * p.inner, res[j * NL + lm.l]);
@@ -88,77 +394,86 @@ __global__ void __launch_bounds__(256, 2) fft_pass_kernel(FftPass p) {
 }
 
 // ------------------------------------------------------------ planar y/z
-constexpr int kPlanarThreads = 256;   // max; launched with min(256, Py*RC rounded to 32)
-// W[4][Px][Ny][Nz][R] in place.  CTA = (plane c*Px+kx, rhs chunk r0..r0+RC).
-// smem [Py][Nz*RC] (y lines indexed by l = z*RC + rl).
-template <int NZ>
-__global__ void __launch_bounds__(kPlanarThreads, 2) planar_yz_kernel(PlanarPass p) {
+constexpr int kPlanarThreads = 256;   // max; launched with >= one butterfly per line element / min radix
+// W[4][Px][Ny][Nz][R] in place.  Tile = (plane c*Px+kx, rhs chunk r0..r0+RC),
+// ordered kx-major so a CTA's contiguous tile range needs the G2 slice of one
+// or two kx only (kept in smem).  smem: twiddles [Py], G2 slice [PyH][NZ],
+// two tile buffers [Py][NZ*RC] (y lines indexed by l = z*RC + rl).
+template <int NZ, class F, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int tiles) {
     extern __shared__ double2 sm[];
-    const int Py = p.ay.P;
-    const int RC = p.RC;
+    const int Py = F::compile_time ? F::P : p.ay.P;
+    const int RC = F::compile_time ? 1 : p.RC;
     const int NL = NZ * RC;
-    double2* buf = sm;
-    double2* tw = sm + (size_t)Py * NL;
+    double2* tw = sm;
+    double2* g2 = sm + Py;
+    double2* const buf0 = g2 + (size_t)p.PyH * NZ;
+    double2* const buf1 = buf0 + (size_t)Py * NL;
     const int nchunk = (p.R + RC - 1) / RC;
-    const long long plane = blockIdx.x / nchunk;
-    const int r0 = (int)(blockIdx.x % nchunk) * RC;
-    const int rc_n = min(RC, p.R - r0);
-    const int kx = (int)(plane % p.Px);
     const LineMap lm(NL);
     const int z = lm.l / RC, rl = lm.l - (lm.l / RC) * RC;
-    const bool live = lm.active && rl < rc_n;
-    double2* W = p.W + plane * (long long)p.Ny * NZ * p.R + z * p.R + r0 + rl;   // + y * NZ * R
-    const long long ystride = (long long)NZ * p.R;
-
+    const int ystride = NZ * p.R;
     for (int e = threadIdx.x; e < Py; e += blockDim.x) tw[e] = p.ay.tw[e];
-    if (lm.active) {
-        int y = lm.js;
-        for (; y + 3 * lm.JS < p.Ny; y += 4 * lm.JS) {
-            double2 v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = live ? __ldcs(W + (y + q * lm.JS) * ystride) : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) buf[(y + q * lm.JS) * NL + lm.l] = v[q];
+    int t0, t1;
+    tile_range(tiles, t0, t1);
+    if (t0 >= t1) return;
+
+    // tile t -> (kx, c, chunk) = (t / (4 nchunk), (t / nchunk) % 4, t % nchunk); advanced incrementally
+    int lkx = t0 / (4 * nchunk), lc = (t0 / nchunk) % 4, lch = t0 % nchunk;
+    auto base_of = [&](int kx, int c, int ch, bool& live) -> double2* {
+        const int r0 = ch * RC;
+        live = lm.active && r0 + rl < p.R;
+        const long long plane = (long long)c * p.Px + kx;
+        return p.W + plane * p.Ny * ystride + z * p.R + r0 + rl;   // + y * ystride
+    };
+    auto issue = [&](double2* buf) {
+        if (!lm.active) return;
+        bool live;
+        const double2* src = base_of(lkx, lc, lch, live);
+#pragma unroll 4
+        for (int y = lm.js; y < Py; y += lm.JS) {
+            const bool v = live && y < p.Ny;
+            cp_async16(&buf[y * NL + lm.l], v ? src + y * ystride : p.W, v);
         }
-        for (; y < Py; y += lm.JS)
-            buf[y * NL + lm.l] = (live && y < p.Ny) ? __ldcs(W + y * ystride) : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    fft_lines_inplace(buf, tw, p.ay, NL, -1.0, lm);
-    double2* res = buf;
-    double2* oth = buf;   // each z line is read into registers and rewritten by one thread
-    // z: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for every (ky, rl), one
-    // line per thread, all indices compile-time (G2 row and inputs in registers),
-    // symmetric Toeplitz: out[z] = g0 in[z] + sum_{d>0} g_d (in[z-d] + in[z+d]).
-    const int ax_ = min(kx, p.Px - kx);
-    const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
-    for (int line = threadIdx.x; line < Py * RC; line += blockDim.x) {
-        const int ky = line / RC, rr = line - (line / RC) * RC;
-        const int ay = min(ky, Py - ky);
-        const double2* g = G2 + (long long)ay * NZ;
-        double2 gk[NZ], in[NZ];
-#pragma unroll
-        for (int d = 0; d < NZ; ++d) gk[d] = __ldg(&g[d]);
-#pragma unroll
-        for (int zz = 0; zz < NZ; ++zz) in[zz] = res[ky * NL + zz * RC + rr];
-#pragma unroll
-        for (int zz = 0; zz < NZ; ++zz) {
-            double2 acc = cmul(gk[0], in[zz]);
-#pragma unroll
-            for (int d = 1; d < NZ; ++d) {
-                if (zz - d < 0 && zz + d >= NZ) continue;
-                double2 sum = zz - d >= 0 ? in[zz - d] : make_double2(0.0, 0.0);
-                if (zz + d < NZ) sum = cadd(sum, in[zz + d]);
-                acc.x = fma(gk[d].x, sum.x, fma(-gk[d].y, sum.y, acc.x));
-                acc.y = fma(gk[d].x, sum.y, fma(gk[d].y, sum.x, acc.y));
-            }
-            oth[ky * NL + zz * RC + rr] = acc;
+    };
+    auto advance = [&]() {
+        if (++lch == nchunk) {
+            lch = 0;
+            if (++lc == 4) { lc = 0; ++lkx; }
         }
+    };
+    issue(buf0);
+    cp_commit();
+    int ckx = lkx, cc = lc, cch = lch;   // tile being computed
+    advance();
+    int cur_ax = -1;
+    for (int t = t0; t < t1; ++t) {
+        const bool odd = (t - t0) & 1;
+        double2* buf = odd ? buf1 : buf0;
+        if (t + 1 < t1) issue(odd ? buf0 : buf1);
+        cp_commit();
+        cp_wait_prev();
+        const int ax_ = min(ckx, p.Px - ckx);
+        if (ax_ != cur_ax) {   // uniform: G2 slice of this kx (rare: tiles are kx-major)
+            const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
+            for (int e = threadIdx.x; e < p.PyH * NZ; e += blockDim.x) g2[e] = __ldg(&G2[e]);
+            cur_ax = ax_;
+        }
+        __syncthreads();
+        F::template run<-1>(buf, tw, p.ay, NL);
+        planar_toeplitz<NZ>(buf, g2, Py, RC, NL);
+        __syncthreads();
+        F::template run<+1>(buf, tw, p.ay, NL);
+        bool live;
+        double2* dst = base_of(ckx, cc, cch, live);
+        if (live) {
+#pragma unroll 4
+            for (int y = lm.js; y < p.Ny; y += lm.JS) __stcs(dst + y * ystride, buf[y * NL + lm.l]);
+        }
+        ckx = lkx; cc = lc; cch = lch;
+        advance();
+        __syncthreads();
     }
-    __syncthreads();
-    fft_lines_inplace(buf, tw, p.ay, NL, +1.0, lm);
-    if (live)
-        for (int y = lm.js; y < p.Ny; y += lm.JS) __stcs(W + y * ystride, res[y * NL + lm.l]);
 }
 
 // ------------------------------------------------------------------- host
@@ -176,12 +491,21 @@ int smooth_size_at_least(int n) {
 // nested DFT).  Stage plan: fewest stages, then the larger first radix.
 static const int kRadices[] = {16, 15, 14, 12, 10, 9, 8, 7, 6, 5, 4, 3, 2};
 
+static int min_of(const std::vector<int>& v) {
+    int m = 1 << 30;
+    for (int r : v) m = std::min(m, r);
+    return m;
+}
+
+// fewest stages, then the largest smallest radix (fewer threads idle in the
+// in-place kernels), then the first found (larger first radix)
 static void plan_radices(int P, std::vector<int>& best, std::vector<int>& cur) {
     if (P == 1) {
-        if (best.empty() || cur.size() < best.size()) best = cur;
+        if (best.empty() || cur.size() < best.size() || (cur.size() == best.size() && min_of(cur) > min_of(best)))
+            best = cur;
         return;
     }
-    if (!best.empty() && cur.size() + 1 >= best.size()) return;
+    if (!best.empty() && cur.size() + 1 > best.size()) return;
     for (int r : kRadices)
         if (P % r == 0) {
             cur.push_back(r);
@@ -232,68 +556,182 @@ void make_fft_axis(int P, FftAxis& ax) {
 
 static constexpr int kFftThreads = 256;
 
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        AIM_CUDA(cudaGetDevice(&dev));
+        AIM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+// Opt a kernel into the full 227 KB of dynamic shared memory (once per kernel
+// and device; kernels are distinguished by address, not by signature).
+template <class K>
+static void ensure_smem_attr(K kernel) {
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    AIM_CUDA(cudaGetDevice(&dev));
+    const void* key = (const void*)kernel;
+    for (auto& d : done)
+        if (d.first == key && d.second == dev) return;
+    AIM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    done.emplace_back(key, dev);
+}
+
+template <class K>
+static long long persistent_grid(K kernel, int threads, size_t smem, long long tiles) {
+    if (tiles >= (1LL << 31)) throw Error(AIM_E_GRID, "FFT pass: tile count exceeds 2^31");
+    int per = 0;
+    AIM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem));
+    return std::max(1LL, std::min(tiles, (long long)std::max(1, per) * sm_count()));
+}
+
+// Tile shape for TI x TO lines of a pass with nl lines available.
+static void tile_shape(FftPass& p, int nl) {
+    long long ti = 1;
+    while (ti * 2 <= std::min<long long>(p.inner, nl) && ti * 2 <= kFftThreads) ti *= 2;
+    if (ti < p.inner && ti * 2 <= nl && ti * 2 <= kFftThreads) ti *= 2;  // one ragged tile is cheaper than many
+    p.TI = (int)ti;
+    p.TO = (int)std::max<long long>(1, std::min<long long>(p.outer, nl / p.TI));
+    p.TO = std::min(p.TO, std::max(1, nl / p.TI));
+}
+
+template <class K>
+static void launch_pipe(K kern, const FftPass& p, int threads, cudaStream_t s) {
+    const int P = p.ax.P;
+    const long long tiles = ((p.inner + p.TI - 1) / p.TI) * ((p.outer + p.TO - 1) / p.TO);
+    if (tiles <= 0) return;
+    const size_t smem = sizeof(double2) * ((size_t)2 * P * p.TO * p.TI + P);
+    if (smem > 227 * 1024) throw Error(AIM_E_GRID, "FFT length exceeds the shared-memory tile capacity");
+    ensure_smem_attr(kern);
+    const long long grid = persistent_grid(kern, threads, smem, tiles);
+    kern<<<(unsigned)grid, threads, smem, s>>>(p, (int)tiles);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw Error(AIM_E_CUDA, "fft_pipe_kernel P=" + std::to_string(P) + " NL=" + std::to_string(p.TO * p.TI) +
+                                    " threads=" + std::to_string(threads) + " grid=" + std::to_string(grid) +
+                                    " smem=" + std::to_string(smem) + ": " + cudaGetErrorString(e));
+}
+
+template <class F, int MINB>
+static bool try_ct_pass(FftPass p, cudaStream_t s) {
+    if (p.ax.P != F::P || p.TI > 0) return false;
+    // F::NL lines: TI = the largest power of two <= inner dividing NL, TO = NL / TI
+    int ti = 1;
+    while (F::NL % (ti * 2) == 0 && ti * 2 <= p.inner) ti *= 2;
+    if (F::NL / ti > p.outer) return false;
+    p.TI = ti;
+    p.TO = F::NL / ti;
+    const long long tiles = ((p.inner + p.TI - 1) / p.TI) * ((p.outer + p.TO - 1) / p.TO);
+    const size_t smem = sizeof(double2) * ((size_t)3 * F::P * F::NL + F::P);
+    auto go = [&](auto kern) {
+        ensure_smem_attr(kern);
+        const long long grid = persistent_grid(kern, F::T, smem, tiles);
+        kern<<<(unsigned)grid, F::T, smem, s>>>(p, (int)tiles);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+            throw Error(AIM_E_CUDA, "fft_ct_kernel P=" + std::to_string(F::P) + ": " + cudaGetErrorString(e));
+    };
+    if (p.mode == 0) go(fft_ct_kernel<F, 0, MINB>);
+    else if (p.mode == 1) go(fft_ct_kernel<F, 1, MINB>);
+    else go(fft_ct_kernel<F, 2, MINB>);
+    return true;
+}
+
 void launch_fft_pass(const FftPass& p0, cudaStream_t s) {
     FftPass p = p0;
     const int P = p.ax.P;
-    // in place when one butterfly per thread per stage suffices for >= 4 lines
+    if (p.outer <= 0 || p.inner <= 0) return;
+    if (try_ct_pass<Ct210, 2>(p, s) || try_ct_pass<Ct24, 2>(p, s)) {
+        note_launch("fft_pass");
+        return;
+    }
+    // runtime radices: in place when one butterfly per thread per stage suffices for >= 2 lines
     const int nl_inplace = kFftThreads * p.ax.min_radix / P;
     const bool inplace = nl_inplace >= 2;
     const int cap = std::max(fft_tile_capacity(), P);
-    const int nl = inplace ? nl_inplace : std::max(1, cap / P);
-    if (p.TI <= 0) {
-        // TI: power of two (coalesced rows of TI*16 bytes); TO fills the tile
-        long long ti = 1;
-        while (ti * 2 <= std::min<long long>(p.inner, nl) && ti * 2 <= kFftThreads) ti *= 2;
-        if (ti < p.inner && ti * 2 <= nl && ti * 2 <= kFftThreads) ti *= 2;  // one ragged tile is cheaper than many
-        p.TI = (int)ti;
-        p.TO = (int)std::max<long long>(1, std::min<long long>(p.outer, nl / p.TI));
-        p.TO = std::min(p.TO, kFftThreads / p.TI);
+    if (p.TI <= 0) tile_shape(p, inplace ? nl_inplace : std::max(1, cap / P));
+    if (inplace) {
+        if (p.mode == 0) launch_pipe(fft_pipe_kernel<RtPlan, 0, kFftThreads, 2>, p, kFftThreads, s);
+        else if (p.mode == 1) launch_pipe(fft_pipe_kernel<RtPlan, 1, kFftThreads, 2>, p, kFftThreads, s);
+        else launch_pipe(fft_pipe_kernel<RtPlan, 2, kFftThreads, 2>, p, kFftThreads, s);
+    } else {
+        const long long tiles = ((p.inner + p.TI - 1) / p.TI) * ((p.outer + p.TO - 1) / p.TO);
+        const size_t smem = sizeof(double2) * ((size_t)2 * P * p.TO * p.TI + P);
+        if (smem > 227 * 1024) throw Error(AIM_E_GRID, "FFT length exceeds the shared-memory tile capacity");
+        ensure_smem_attr(fft_pp_kernel);
+        fft_pp_kernel<<<(unsigned)tiles, kFftThreads, smem, s>>>(p);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+            throw Error(AIM_E_CUDA, "fft_pp_kernel P=" + std::to_string(P) + " tiles=" + std::to_string(tiles) +
+                                        " smem=" + std::to_string(smem) + ": " + cudaGetErrorString(e));
     }
-    const long long tilesI = (p.inner + p.TI - 1) / p.TI;
-    const long long tilesO = (p.outer + p.TO - 1) / p.TO;
-    const long long grid = tilesI * tilesO;
-    if (grid <= 0) return;
-    const size_t smem = sizeof(double2) * ((size_t)(inplace ? 1 : 2) * P * p.TO * p.TI + P);
-    if (smem > 227 * 1024) throw Error(AIM_E_GRID, "FFT length exceeds the shared-memory tile capacity");
-    static bool attr = false;
-    if (!attr) {
-        AIM_CUDA(cudaFuncSetAttribute(fft_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        AIM_CUDA(cudaFuncSetAttribute(fft_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
-    if (inplace) fft_pass_kernel<true><<<(unsigned)grid, kFftThreads, smem, s>>>(p);
-    else fft_pass_kernel<false><<<(unsigned)grid, kFftThreads, smem, s>>>(p);
     note_launch("fft_pass");
 }
 
 // planar pass: one CTA holds a (Py x Nz) plane in place, one butterfly per thread per stage
 bool planar_supported(int Py, int Nz, int min_radix) {
-    return Nz <= kPlanarMaxNz && (long long)Nz * Py / min_radix <= kPlanarThreads && Py * Nz * 16 <= 200 * 1024;
+    const size_t smem = sizeof(double2) * ((size_t)2 * Py * Nz + (size_t)(Py / 2 + 1) * Nz + Py);
+    return Nz <= kPlanarMaxNz && (long long)Nz * Py / min_radix <= kPlanarThreads && smem <= 200 * 1024;
+}
+
+template <class K>
+static void launch_planar(K kern, const PlanarPass& p, int threads, cudaStream_t s) {
+    const int Py = p.ay.P;
+    const long long tiles = 4LL * p.Px * ((p.R + p.RC - 1) / p.RC);
+    const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + (size_t)p.PyH * p.Nz + Py);
+    ensure_smem_attr(kern);
+    const long long grid = persistent_grid(kern, threads, smem, tiles);
+    kern<<<(unsigned)grid, threads, smem, s>>>(p, (int)tiles);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw Error(AIM_E_CUDA, "planar_yz_kernel Py=" + std::to_string(Py) + " Nz=" + std::to_string(p.Nz) +
+                                    " RC=" + std::to_string(p.RC) + " threads=" + std::to_string(threads) +
+                                    " smem=" + std::to_string(smem) + ": " + cudaGetErrorString(e));
+}
+
+template <int NZ, class F, int MINB>
+static bool try_ct_planar(PlanarPass p, cudaStream_t s) {
+    if (p.ay.P != F::P || p.Nz != NZ || p.PyH != F::P / 2 + 1) return false;
+    p.RC = 1;
+    const long long tiles = 4LL * p.Px * p.R;
+    const size_t smem = sizeof(double2) * ((size_t)3 * F::P * NZ + (size_t)(F::P / 2 + 1) * NZ + F::P);
+    auto kern = planar_ct_kernel<NZ, F, MINB>;
+    ensure_smem_attr(kern);
+    const long long grid = persistent_grid(kern, F::T, smem, tiles);
+    kern<<<(unsigned)grid, F::T, smem, s>>>(p, (int)tiles);
+#ifdef AIM_BOUNDS_DEBUG
+    {
+        cudaDeviceSynchronize();
+        int flag = 0;
+        cudaMemcpyFromSymbol(&flag, g_aim_dbg, sizeof(int));
+        if (flag) throw Error(AIM_E_CUDA, "planar_ct_kernel bounds check " + std::to_string(flag));
+    }
+#endif
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw Error(AIM_E_CUDA, "planar_ct_kernel Py=" + std::to_string(F::P) + ": " + cudaGetErrorString(e));
+    return true;
 }
 
 void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
     PlanarPass p = p0;
+    if (try_ct_planar<11, Ct210z11, 1>(p, s) || try_ct_planar<7, Ct24z7, 2>(p, s)) {
+        note_launch("planar_yz");
+        return;
+    }
     const int Py = p.ay.P;
     const int rc_fft = (int)(kPlanarThreads * (long long)p.ay.min_radix / ((long long)Py * p.Nz));
     p.RC = std::max(1, std::min({p.R, rc_fft, kPlanarThreads / p.Nz}));
-    const long long nchunk = (p.R + p.RC - 1) / p.RC;
-    const long long grid = 4LL * p.Px * nchunk;
-    // one z line per thread in the convolution step; NL lines for the FFT stages
-    const int bfly = (int)((long long)p.Nz * p.RC * Py / p.ay.min_radix);   // butterflies per stage (max)
+    while (p.RC > 1 && sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + (size_t)p.PyH * p.Nz + Py) > 110 * 1024)
+        --p.RC;
+    // one butterfly per thread per FFT stage; one (ky, rhs) z line per thread in the convolution
+    const int bfly = (int)((long long)p.Nz * p.RC * Py / p.ay.min_radix);
     const int threads = std::min(kPlanarThreads, 32 * ((std::max({bfly, Py * p.RC, p.Nz * p.RC}) + 31) / 32));
-    const size_t smem = sizeof(double2) * ((size_t)Py * p.Nz * p.RC + Py);
     switch (p.Nz) {
-#define PZ(NZ)                                                                                              \
-    case NZ: {                                                                                              \
-        static bool attr = false;                                                                           \
-        if (!attr) {                                                                                        \
-            AIM_CUDA(cudaFuncSetAttribute(planar_yz_kernel<NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                          227 * 1024));                                                     \
-            attr = true;                                                                                    \
-        }                                                                                                   \
-        planar_yz_kernel<NZ><<<(unsigned)grid, threads, smem, s>>>(p);                                   \
-        break;                                                                                              \
-    }
+#define PZ(NZ) case NZ: launch_planar(planar_yz_kernel<NZ, RtPlan, kPlanarThreads, 2>, p, threads, s); break;
         PZ(1) PZ(2) PZ(3) PZ(4) PZ(5) PZ(6) PZ(7) PZ(8) PZ(9) PZ(10) PZ(11) PZ(12) PZ(13) PZ(14) PZ(15) PZ(16)
 #undef PZ
         default: throw Error(AIM_E_GRID, "planar pass: Nz out of range");

@@ -428,23 +428,21 @@ void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s
     convolve_impl(p, Q, Phi, R, s, nullptr);
 }
 
-// y = Z_eq x.  The near-field SpMV (memory bound) runs on the plan's side
-// stream concurrently with the projection + FFT passes (FP64-ALU heavy);
-// the interpolation adds the far field to its result.
+// y = Z_eq x.  All stages run in order on the caller's stream: the near-field
+// SpMV first (it writes y), then projection, the FFT passes and the
+// interpolation, which accumulates the far field into y.  (Running the SpMV
+// on a side stream bought nothing: its 14k CTAs occupy every SM and the
+// persistent FFT CTAs queue behind them.)
 void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
     ensure_workspace(p, R);
     Prof pr(p);
     pr.mark(0, s);
-    AIM_CUDA(cudaEventRecord(p->ev_x, s));
-    AIM_CUDA(cudaStreamWaitEvent(p->side, p->ev_x, 0));
-    pr.mark(7, p->side);
-    launch_near(p, x, y, R, p->side);
-    pr.mark(8, p->side);
-    AIM_CUDA(cudaEventRecord(p->ev_n, p->side));
+    pr.mark(7, s);
+    launch_near(p, x, y, R, s);
+    pr.mark(8, s);
     launch_project(p, x, p->Q, R, s);
     pr.mark(1, s);
     convolve_impl(p, p->Q, p->Q, R, s, &pr);
-    AIM_CUDA(cudaStreamWaitEvent(s, p->ev_n, 0));
     pr.mark(5, s);
     launch_interp(p, p->Q, y, R, true, s);
     pr.mark(6, s);
