@@ -115,6 +115,15 @@ struct aim_plan {
     int64_t* nrow = nullptr;      // [N+1]
     int32_t* ncol = nullptr;      // [nnzN]
     double2* nval = nullptr;      // [nnzN]
+    // near field in 4-row blocks (multi-RHS products; built on first use):
+    // rows of a block are 4 consecutive RWGs in Morton order of their centres,
+    // columns the sorted union of the 4 rows' columns, values dense 4 per column
+    int64_t nb_count = 0;         // number of blocks (0 = not built)
+    int64_t nbc = 0;              // block columns
+    int32_t* nb_rows = nullptr;   // [nb_count][4] row ids, -1 = padding
+    int64_t* nb_ptr = nullptr;    // [nb_count+1]
+    int32_t* nb_col = nullptr;    // [nbc]
+    double2* nb_val = nullptr;    // [nbc][4]
     int planar = 0;               // 1: z handled by direct convolution (spec = G2)
     double2* spec = nullptr;      // 3-D: [(Px/2+1)(Py/2+1)(Pz/2+1)]; planar: [(Px/2+1)(Py/2+1)][Nz]
     int64_t spec_len = 0;
@@ -182,11 +191,12 @@ void build_projection_csr(aim_plan* p, const std::vector<int32_t>& node0_host, c
 void build_near_list(aim_plan* p, cudaStream_t s);
 void build_near_values(aim_plan* p, cudaStream_t s);
 void build_green_spectrum(aim_plan* p, cudaStream_t s);
+void build_near_blocks(aim_plan* p, cudaStream_t s);
 
 // ---- matvec launches (k_matvec.cu)
 void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s);
 void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s);
-void launch_near(const aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
+void launch_near(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
 void launch_planewave(const aim_plan* p, const double* khat, const double* pol, double2 E0, double2* V,
                       cudaStream_t s);
 void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s);

@@ -63,7 +63,7 @@ __device__ __forceinline__ void tile_range(int tiles, int& t0, int& t1) {
 // kernels.  Radices <= 7: one butterfly's registers stay small.
 using Ct210 = CtpPlan<8, 336, 210, 7, 6, 5>;      // x passes of C2: 8 lines (128 B rows)
 using Ct24 = CtpPlan<32, 192, 24, 6, 4>;          // x passes of C1 (1 RHS): 32 lines
-using Ct210z11 = CtpPlan<11, 480, 210, 7, 6, 5>;  // planar y/z of C2, one RHS per tile
+using Ct210z11 = CtpPlan<11, 240, 210, 7, 6, 5>;  // planar y/z of C2, one RHS per tile
 using Ct24z7 = CtpPlan<7, 64, 24, 6, 4>;          // planar y/z of C1, one RHS per tile
 
 // ------------------------------------------------------ generic axis pass
@@ -160,18 +160,20 @@ __device__ __forceinline__ void planar_toeplitz(double2* buf, const double2* g2,
         const int ay = min(ky, Py - ky);
         const double2* g = g2 + ay * NZ;
         double2* row = buf + ky * NL + rr;   // + zz * RC
-        double2 in[NZ];
+        double2 gk[NZ], in[NZ];
+#pragma unroll
+        for (int d = 0; d < NZ; ++d) gk[d] = __ldg(&g[d]);
 #pragma unroll
         for (int zz = 0; zz < NZ; ++zz) in[zz] = row[zz * RC];
 #pragma unroll
         for (int zz = 0; zz < NZ; ++zz) {
-            double2 acc = cmul(g[0], in[zz]);
+            double2 acc = cmul(gk[0], in[zz]);
 #pragma unroll
             for (int d = 1; d < NZ; ++d) {
                 if (zz - d < 0 && zz + d >= NZ) continue;
                 double2 sum = zz - d >= 0 ? in[zz - d] : make_double2(0.0, 0.0);
                 if (zz + d < NZ) sum = zz - d >= 0 ? cadd(sum, in[zz + d]) : in[zz + d];
-                const double2 gd = g[d];
+                const double2 gd = gk[d];
                 acc.x = fma(gd.x, sum.x, fma(-gd.y, sum.y, acc.x));
                 acc.y = fma(gd.x, sum.y, fma(gd.y, sum.x, acc.y));
             }
@@ -260,21 +262,23 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
     }
 }
 
+// Planar y/z pass with a compile-time plan: persistent CTAs, three tile
+// buffers (X being transformed, Y ping-pong scratch, Z receiving the next
+// tile by cp.async); the twiddles and the G2 slice are read through L1
+// (__ldg) so two CTAs fit per SM (barrier stalls of one overlap the other).
 template <int NZ, class F, int MINB>
 __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int tiles) {
     constexpr int Py = F::P, NL = F::NL, T = F::T, JS = T / NL;
     static_assert(NL == NZ, "one RHS per tile");
     extern __shared__ double2 sm[];
-    double2* tw = sm;
-    double2* g2 = sm + Py;
-    double2* X = g2 + (Py / 2 + 1) * NZ;
+    double2* X = sm;
     double2* Y = X + Py * NL;
     double2* Z = Y + Py * NL;
+    const double2* tw = p.ay.tw;
     const int nchunk = p.R;
     const int l = threadIdx.x % NL, js = threadIdx.x / NL;   // l = z
     const bool act = js < JS;
     const int ystride = NZ * p.R;
-    for (int e = threadIdx.x; e < Py; e += T) tw[e] = p.ay.tw[e];
     int t0, t1;
     tile_range(tiles, t0, t1);
     if (t0 >= t1) return;
@@ -289,8 +293,6 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
 #pragma unroll 2
         for (int y = js; y < Py; y += JS) {
             const bool v = y < p.Ny;
-            AIM_CHK(!v || (src + y * ystride - p.W) < 4LL * p.Px * p.Ny * ystride, 101);
-            AIM_CHK(y * NL + l < Py * NL, 102);
             cp_async16(&buf[y * NL + l], v ? src + y * ystride : p.W, v);
         }
     };
@@ -304,19 +306,13 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
     cp_commit();
     int ckx = lkx, cc = lc, cch = lch;
     advance();
-    int cur_ax = -1;
     for (int t = t0; t < t1; ++t) {
         if (t + 1 < t1) issue(Z);
         cp_commit();
         cp_wait_prev();
-        const int ax_ = min(ckx, p.Px - ckx);
-        if (ax_ != cur_ax) {   // uniform: G2 slice of this kx (rare: tiles are kx-major)
-            const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
-            AIM_CHK(ax_ >= 0 && ax_ <= p.Px / 2, 104);
-            for (int e = threadIdx.x; e < p.PyH * NZ; e += T) g2[e] = __ldg(&G2[e]);
-            cur_ax = ax_;
-        }
         __syncthreads();
+        const int ax_ = min(ckx, p.Px - ckx);
+        const double2* g2 = p.spec + (long long)ax_ * p.PyH * NZ;
         double2* res = F::template run<-1>(X, Y, tw);
         planar_toeplitz<NZ>(res, g2, Py, 1, NL);
         __syncthreads();
@@ -324,10 +320,7 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
         if (act) {
             double2* dst = base_of(ckx, cc, cch);
 #pragma unroll 2
-            for (int y = js; y < p.Ny; y += JS) {
-                AIM_CHK((dst + y * ystride - p.W) < 4LL * p.Px * p.Ny * ystride && dst + y * ystride >= p.W, 103);
-                __stcs(dst + y * ystride, res[y * NL + l]);
-            }
+            for (int y = js; y < p.Ny; y += JS) __stcs(dst + y * ystride, res[y * NL + l]);
         }
         ckx = lkx; cc = lc; cch = lch;
         advance();
@@ -396,9 +389,9 @@ __global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
 // ------------------------------------------------------------ planar y/z
 constexpr int kPlanarThreads = 256;   // max; launched with >= one butterfly per line element / min radix
 // W[4][Px][Ny][Nz][R] in place.  Tile = (plane c*Px+kx, rhs chunk r0..r0+RC),
-// ordered kx-major so a CTA's contiguous tile range needs the G2 slice of one
-// or two kx only (kept in smem).  smem: twiddles [Py], G2 slice [PyH][NZ],
-// two tile buffers [Py][NZ*RC] (y lines indexed by l = z*RC + rl).
+// ordered kx-major (a CTA's tile range touches the G2 slices of one or two kx,
+// read through L1).  smem: twiddles [Py], two tile buffers [Py][NZ*RC]
+// (y lines indexed by l = z*RC + rl).
 template <int NZ, class F, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int tiles) {
     extern __shared__ double2 sm[];
@@ -406,8 +399,7 @@ __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int
     const int RC = F::compile_time ? 1 : p.RC;
     const int NL = NZ * RC;
     double2* tw = sm;
-    double2* g2 = sm + Py;
-    double2* const buf0 = g2 + (size_t)p.PyH * NZ;
+    double2* const buf0 = sm + Py;
     double2* const buf1 = buf0 + (size_t)Py * NL;
     const int nchunk = (p.R + RC - 1) / RC;
     const LineMap lm(NL);
@@ -446,7 +438,6 @@ __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int
     cp_commit();
     int ckx = lkx, cc = lc, cch = lch;   // tile being computed
     advance();
-    int cur_ax = -1;
     for (int t = t0; t < t1; ++t) {
         const bool odd = (t - t0) & 1;
         double2* buf = odd ? buf1 : buf0;
@@ -454,11 +445,7 @@ __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int
         cp_commit();
         cp_wait_prev();
         const int ax_ = min(ckx, p.Px - ckx);
-        if (ax_ != cur_ax) {   // uniform: G2 slice of this kx (rare: tiles are kx-major)
-            const double2* G2 = p.spec + (long long)ax_ * p.PyH * NZ;
-            for (int e = threadIdx.x; e < p.PyH * NZ; e += blockDim.x) g2[e] = __ldg(&G2[e]);
-            cur_ax = ax_;
-        }
+        const double2* g2 = p.spec + (long long)ax_ * p.PyH * NZ;   // G2 slice of this kx (read through L1)
         __syncthreads();
         F::template run<-1>(buf, tw, p.ay, NL);
         planar_toeplitz<NZ>(buf, g2, Py, RC, NL);
@@ -681,7 +668,7 @@ template <class K>
 static void launch_planar(K kern, const PlanarPass& p, int threads, cudaStream_t s) {
     const int Py = p.ay.P;
     const long long tiles = 4LL * p.Px * ((p.R + p.RC - 1) / p.RC);
-    const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + (size_t)p.PyH * p.Nz + Py);
+    const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py);
     ensure_smem_attr(kern);
     const long long grid = persistent_grid(kern, threads, smem, tiles);
     kern<<<(unsigned)grid, threads, smem, s>>>(p, (int)tiles);
@@ -697,7 +684,7 @@ static bool try_ct_planar(PlanarPass p, cudaStream_t s) {
     if (p.ay.P != F::P || p.Nz != NZ || p.PyH != F::P / 2 + 1) return false;
     p.RC = 1;
     const long long tiles = 4LL * p.Px * p.R;
-    const size_t smem = sizeof(double2) * ((size_t)3 * F::P * NZ + (size_t)(F::P / 2 + 1) * NZ + F::P);
+    const size_t smem = sizeof(double2) * ((size_t)3 * F::P * NZ);
     auto kern = planar_ct_kernel<NZ, F, MINB>;
     ensure_smem_attr(kern);
     const long long grid = persistent_grid(kern, F::T, smem, tiles);
@@ -718,14 +705,14 @@ static bool try_ct_planar(PlanarPass p, cudaStream_t s) {
 
 void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
     PlanarPass p = p0;
-    if (try_ct_planar<11, Ct210z11, 1>(p, s) || try_ct_planar<7, Ct24z7, 2>(p, s)) {
+    if (try_ct_planar<11, Ct210z11, 2>(p, s) || try_ct_planar<7, Ct24z7, 2>(p, s)) {
         note_launch("planar_yz");
         return;
     }
     const int Py = p.ay.P;
     const int rc_fft = (int)(kPlanarThreads * (long long)p.ay.min_radix / ((long long)Py * p.Nz));
     p.RC = std::max(1, std::min({p.R, rc_fft, kPlanarThreads / p.Nz}));
-    while (p.RC > 1 && sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + (size_t)p.PyH * p.Nz + Py) > 110 * 1024)
+    while (p.RC > 1 && sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py) > 110 * 1024)
         --p.RC;
     // one butterfly per thread per FFT stage; one (ky, rhs) z line per thread in the convolution
     const int bfly = (int)((long long)p.Nz * p.RC * Py / p.ay.min_radix);

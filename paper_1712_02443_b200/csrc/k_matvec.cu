@@ -18,6 +18,14 @@ namespace aim {
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+#ifndef AIM_GATHER_UNROLL
+#define AIM_GATHER_UNROLL 2
+#endif
+#ifndef AIM_GATHER_RPL16
+#define AIM_GATHER_RPL16 1
+#endif
+constexpr int kGatherUnroll = AIM_GATHER_UNROLL;   // gather steps in flight per lane
+
 __device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
     return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
@@ -68,7 +76,7 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
                 w01 = __ldcs(W2 + 2 * (long long)ent);
                 w23 = __ldcs(W2 + 2 * (long long)ent + 1);
             }
-#pragma unroll 2
+#pragma unroll kGatherUnroll
             for (int t = ln.grp; t < 32; t += L::G) {
                 int n;
                 double w[4];
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
     else if (R == 2) { CALL(2, 1); }                   \
     else if (R <= 4) { CALL(4, 1); }                   \
     else if (R <= 8) { CALL(8, 1); }                   \
-    else if (R <= 16) { CALL(16, 1); }                 \
+    else if (R <= 16) { CALL(16 / AIM_GATHER_RPL16, AIM_GATHER_RPL16); } \
     else { CALL(32, 1); }
 
 void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s) {
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
                 const int ui = u_l / (M1 * M1), uj = (u_l / M1) % M1, uk = u_l % M1;
                 g_l = (int)(g0 + ((long long)ui * Ny + uj) * Nz + uk);
             }
-#pragma unroll 2
+#pragma unroll kGatherUnroll
             for (int t = ln.grp; t < 32; t += L::G) {
                 int g;
                 double w[4];
@@ -292,6 +300,107 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
     }
 }
 
+// ------------------------------------------ H6 near SpMV, 4-row blocks
+// Warp per block of 4 rows (Morton-ordered RWGs); column groups of LPE
+// lanes walk the block's union columns, each lane holding RPL right-hand
+// sides: one x load feeds the 4 rows (x reuse 4 x fill), the 4 values of a
+// column are one contiguous 64 B group (broadcast within the lane group).
+// Fixed summation order => deterministic.
+#ifndef AIM_NB4_MINB
+#define AIM_NB4_MINB 2
+#endif
+template <int LPE, int RPL>
+__global__ void __launch_bounds__(256, AIM_NB4_MINB) near_b4_kernel(const int32_t* __restrict__ rows,
+                                                      const int64_t* __restrict__ bptr,
+                                                      const int32_t* __restrict__ bcol,
+                                                      const double2* __restrict__ bval,
+                                                      const double2* __restrict__ x, long long nblk, int R,
+                                                      double2* __restrict__ y) {
+    using L = Lanes<LPE, RPL>;
+    const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (b >= nblk) return;
+    const L ln;
+    const long long e0 = bptr[b], e1 = bptr[b + 1];
+    for (int r0 = 0; r0 < R; r0 += L::RC) {
+        double2 acc[4][RPL];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) acc[i][q] = make_double2(0, 0);
+        // columns staged 32 at a time: lane e loads column e's index and its
+        // 4 values (one coalesced 2 KB read per warp), prefetched one batch
+        // ahead; values reach the lane groups by shuffles
+        int c_n = 0;
+        double2 v_n[4];
+        auto fetch = [&](long long e) {
+            const int cnt = (int)min(32LL, e1 - e);
+            c_n = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v_n[i] = make_double2(0, 0);
+            if (ln.lane < cnt) {
+                c_n = __ldcs(&bcol[e + ln.lane]);
+                const double2* vp = bval + 4 * (e + ln.lane);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v_n[i] = __ldcs(vp + i);
+            }
+        };
+        if (e0 < e1) fetch(e0);
+        for (long long e = e0; e < e1; e += 32) {
+            const int cnt = (int)min(32LL, e1 - e);
+            const int c_l = c_n;
+            double2 v_l[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v_l[i] = v_n[i];
+            if (e + 32 < e1) fetch(e + 32);
+#pragma unroll 2
+            for (int t = ln.grp; t < 32; t += L::G) {
+                const int c = __shfl_sync(0xffffffffu, c_l, t);
+                double2 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = make_double2(__shfl_sync(0xffffffffu, v_l[i].x, t),
+                                                                __shfl_sync(0xffffffffu, v_l[i].y, t));
+                if (t < cnt) {
+                    const double2* xr = x + (long long)c * R + r0 + ln.sub;
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) {
+                        if (r0 + ln.sub + q * LPE < R) {
+                            const double2 xv = __ldg(xr + q * LPE);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                acc[i][q].x = fma(v[i].x, xv.x, acc[i][q].x);
+                                acc[i][q].x = fma(-v[i].y, xv.y, acc[i][q].x);
+                                acc[i][q].y = fma(v[i].x, xv.y, acc[i][q].y);
+                                acc[i][q].y = fma(v[i].y, xv.x, acc[i][q].y);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int off = LPE; off < 32; off <<= 1)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const double2 t = shfl_xor2(acc[i][q], off);
+                    acc[i][q].x += t.x;
+                    acc[i][q].y += t.y;
+                }
+        if (ln.grp == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = rows[4 * b + i];
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const int rr = r0 + ln.sub + q * LPE;
+                    if (row >= 0 && rr < R) y[(long long)row * R + rr] = acc[i][q];
+                }
+            }
+        }
+    }
+}
+
 void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s) {
     const unsigned grid = nblk(p->N * 32, 256);
     const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
@@ -311,7 +420,23 @@ void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, boo
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
-void launch_near(const aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
+// Multi-RHS products use the 4-row blocked layout (x reuse across rows);
+// below kNearBlockRhs right-hand sides the plain CSR (fewer value bytes).
+constexpr int kNearBlockRhs = 4;
+
+void launch_near(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
+    if (R >= kNearBlockRhs) {
+        build_near_blocks(p, s);
+        const unsigned grid = nblk(p->nb_count * 32, 256);
+#define NB_CALL(LPE, RPL) \
+    near_b4_kernel<LPE, RPL><<<grid, 256, 0, s>>>(p->nb_rows, p->nb_ptr, p->nb_col, p->nb_val, x, p->nb_count, R, y)
+        if (R <= 4) { NB_CALL(2, 2); }
+        else if (R <= 8) { NB_CALL(4, 2); }
+        else { NB_CALL(8, 2); }
+#undef NB_CALL
+        note_launch("near_b4");
+        return;
+    }
     const unsigned grid = nblk(p->N * 32, 256);
 #define NK_CALL(LPE, RPL) near_kernel<LPE, RPL><<<grid, 256, 0, s>>>(p->nrow, p->ncol, p->nval, x, p->N, R, y)
     AIM_LANE_DISPATCH_NEAR(R, NK_CALL)

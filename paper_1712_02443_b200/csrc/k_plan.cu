@@ -9,6 +9,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <climits>
 #include <numeric>
 #include <vector>
 
@@ -17,6 +18,7 @@
 namespace aim {
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+static inline unsigned nblk_of(long long n) { return (unsigned)((n + 127) / 128); }
 
 // ------------------------------------------------------------ S2 weights
 // L_i(t) = prod_{j != i} (t - j)/(i - j) on nodes 0..M
@@ -291,6 +293,101 @@ void build_near_list(aim_plan* p, cudaStream_t s) {
     cudaFree(d_cnt);
     cudaFree(cg.cptr);
     cudaFree(cg.cids);
+}
+
+// ------------------------------------------------- near field, 4-row blocks
+// Union of the (sorted) column lists of the block's rows, by a 4-way merge;
+// FILL writes the columns and the dense 4-value groups (0 where a row lacks
+// the column).  One thread per block.
+template <bool FILL>
+__global__ void near_block_kernel(const int32_t* __restrict__ rows, long long nblk, const int64_t* __restrict__ rowp,
+                                  const int32_t* __restrict__ col, const double2* __restrict__ val,
+                                  const int64_t* __restrict__ bptr, int64_t* __restrict__ bcnt,
+                                  int32_t* __restrict__ bcol, double2* __restrict__ bval) {
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblk) return;
+    long long pos[4], end[4];
+    for (int i = 0; i < 4; ++i) {
+        const int r = rows[4 * b + i];
+        pos[i] = r >= 0 ? rowp[r] : 0;
+        end[i] = r >= 0 ? rowp[r + 1] : 0;
+    }
+    long long out = FILL ? bptr[b] : 0;
+    long long cnt = 0;
+    for (;;) {
+        int c = INT_MAX;
+        for (int i = 0; i < 4; ++i)
+            if (pos[i] < end[i]) c = min(c, col[pos[i]]);
+        if (c == INT_MAX) break;
+        double2 v[4];
+        for (int i = 0; i < 4; ++i) {
+            v[i] = make_double2(0.0, 0.0);
+            if (pos[i] < end[i] && col[pos[i]] == c) {
+                if (FILL) v[i] = val[pos[i]];
+                ++pos[i];
+            }
+        }
+        if (FILL) {
+            bcol[out] = c;
+            for (int i = 0; i < 4; ++i) bval[4 * out + i] = v[i];
+            ++out;
+        }
+        ++cnt;
+    }
+    if (!FILL) bcnt[b] = cnt;
+}
+
+static uint64_t spread3(uint64_t v) {   // 21 bits -> every third bit
+    uint64_t r = 0;
+    for (int i = 0; i < 21; ++i) r |= ((v >> i) & 1ULL) << (3 * i);
+    return r;
+}
+
+void build_near_blocks(aim_plan* p, cudaStream_t s) {
+    if (p->nb_count) return;
+    const long long N = p->N;
+    std::vector<double> cen(3 * N);
+    AIM_CUDA(cudaMemcpy(cen.data(), p->rwg_c, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost));
+    // Morton order of the centres on a lattice of spacing h: consecutive rows
+    // are spatially close, so their near sets overlap (fill ~0.75 at 4 rows)
+    double lo[3] = {1e300, 1e300, 1e300};
+    for (long long n = 0; n < N; ++n)
+        for (int a = 0; a < 3; ++a) lo[a] = std::min(lo[a], cen[3 * n + a]);
+    std::vector<std::pair<uint64_t, int32_t>> key(N);
+    for (long long n = 0; n < N; ++n) {
+        uint64_t code = 0;
+        for (int a = 0; a < 3; ++a) {
+            const long long q = std::min<long long>((long long)std::floor((cen[3 * n + a] - lo[a]) / p->h), (1 << 21) - 1);
+            code |= spread3((uint64_t)std::max<long long>(q, 0)) << a;
+        }
+        key[n] = {code, (int32_t)n};
+    }
+    std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    const long long nblk = (N + 3) / 4;
+    std::vector<int32_t> rows(4 * nblk, -1);
+    for (long long n = 0; n < N; ++n) rows[n] = key[n].second;
+    p->nb_rows = p->alloc<int32_t>(4 * nblk);
+    AIM_CUDA(cudaMemcpy(p->nb_rows, rows.data(), sizeof(int32_t) * 4 * nblk, cudaMemcpyHostToDevice));
+    int64_t* d_cnt = nullptr;
+    AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int64_t) * nblk));
+    near_block_kernel<false><<<nblk_of(nblk), 128, 0, s>>>(p->nb_rows, nblk, p->nrow, p->ncol, p->nval, nullptr, d_cnt,
+                                                           nullptr, nullptr);
+    note_launch("near_block_count");
+    std::vector<int64_t> cnt(nblk), ptr(nblk + 1, 0);
+    AIM_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * nblk, cudaMemcpyDeviceToHost, s));
+    AIM_CUDA(cudaStreamSynchronize(s));
+    for (long long b = 0; b < nblk; ++b) ptr[b + 1] = ptr[b] + cnt[b];
+    p->nbc = ptr[nblk];
+    p->nb_ptr = p->alloc<int64_t>(nblk + 1);
+    p->nb_col = p->alloc<int32_t>(p->nbc);
+    p->nb_val = p->alloc<double2>(4 * p->nbc);
+    AIM_CUDA(cudaMemcpyAsync(p->nb_ptr, ptr.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, s));
+    near_block_kernel<true><<<nblk_of(nblk), 128, 0, s>>>(p->nb_rows, nblk, p->nrow, p->ncol, p->nval, p->nb_ptr,
+                                                          nullptr, p->nb_col, p->nb_val);
+    note_launch("near_block_fill");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_cnt);
+    p->nb_count = nblk;
 }
 
 // ------------------------------------------------------- S4 exact entries
