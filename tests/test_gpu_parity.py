@@ -140,6 +140,27 @@ def test_matvec_c2_full_size_sampled_rows():
     assert rel(y[rows], ref) <= 1e-10
 
 
+@pytest.mark.parametrize("name", ["c3", "c5", "c4"])
+def test_matvec_full_size_sampled_rows(name):
+    """configs[2], [4], [3] at full size (N = 526,068 / 1,119,744 / 1,843,200;
+    one RHS, the launch configuration of their matvec): 32 sampled rows plus
+    the first and last against the oracle (full projection + its own
+    power-of-two FFT convolution, interpolation and exact near rows for the
+    sampled rows only).  The GPU plan is released before the oracle runs."""
+    from paper_1712_02443_b200 import AimPlan
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    x = make_vectors(mesh.n_rwg, 1, 0)
+    G = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    G.close()
+    from oracle.aim import OraclePlan
+    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    rows = np.unique(np.concatenate([[0, O.N - 1], np.random.default_rng(1).integers(0, O.N, 32)]))
+    ref = O.matvec_rows(x, rows, method="fft")
+    assert rel(y[rows], ref) <= 1e-10
+
+
 def test_planewave_rhs():
     from oracle.excitation import plane_wave_rhs
     G, O = gpu_plan("c1"), oracle_plan("c1")
