@@ -75,6 +75,7 @@ typedef struct aim_info {
                                [(Px/2+1)][(Py/2+1)][(Pz/2+1)];
                                1: planar -- 2-D FFT in x,y and direct Toeplitz
                                product in z, spectrum [(Px/2+1)][(Py/2+1)][Nz]  */
+    int32_t precision;      /* AIM_C128 or AIM_C64                               */
 } aim_info;
 
 /*
@@ -92,7 +93,12 @@ typedef struct aim_info {
  * M          stencil order in [1, 6] ("N_O")
  * near_radius  >= 0; pairs with ||c_m - c_n|| <= near_radius (1 + 1e-9) are
  *            treated exactly (D5)
- * precision  AIM_C128 (AIM_C64 is reserved; returns AIM_E_ARG in this build)
+ * precision  AIM_C128, or AIM_C64 (BASELINE.json configs[4]; reading D16): the
+ *            plan is computed in fp64 and its tables (weights, near values,
+ *            spectrum, twiddles) rounded once to fp32 / complex64; the matvec
+ *            then reads and writes complex64 vectors and runs the FFT and
+ *            all accumulation in fp32.  aim_gmres / aim_planewave_rhs need an
+ *            AIM_C128 plan (AIM_E_ARG otherwise).
  * dist       must be NULL (single-GPU plan); multi-GPU runs shard RHS across
  *            independent plans, see DESIGN.md "Multi-GPU"
  * out        receives the plan
@@ -118,7 +124,8 @@ int aim_plan_info(const aim_plan* plan, aim_info* info);
 /*
  * aim_matvec -- y := Z_eq x for nrhs right-hand sides (PAPER.md:539-559,
  * steps (i)-(iii) plus the precorrected near field).
- * x, y: device complex128 [N][nrhs], must not overlap.  nrhs >= 1.
+ * x, y: device complex128 [N][nrhs] (complex64 for an AIM_C64 plan), must not
+ * overlap.  nrhs >= 1.
  * Stream-ordered on `stream`; workspaces for this nrhs are allocated on the
  * first call (synchronously) and reused afterwards.
  */

@@ -20,7 +20,7 @@ class AimInfo(ctypes.Structure):
         ("n_nodes", ctypes.c_int64), ("nnz_proj", ctypes.c_int64), ("nnz_near", ctypes.c_int64),
         ("k", ctypes.c_double), ("h", ctypes.c_double), ("near_radius", ctypes.c_double),
         ("device_bytes", ctypes.c_int64), ("plan_seconds", ctypes.c_double),
-        ("conv_mode", ctypes.c_int32),
+        ("conv_mode", ctypes.c_int32), ("precision", ctypes.c_int32),
     ]
 
 

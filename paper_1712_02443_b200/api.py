@@ -14,6 +14,7 @@ from . import _lib
 
 STATUS = {0: "AIM_OK", 1: "AIM_NOT_CONVERGED", -1: "AIM_E_ARG", -2: "AIM_E_MESH", -3: "AIM_E_GRID",
           -4: "AIM_E_NOMEM", -5: "AIM_E_CUDA", -6: "AIM_E_NCCL"}
+C128, C64 = 0, 1   # aim_plan_create precision (AIM_C128, AIM_C64)
 EXPORT = {"bases": 0, "weights": 1, "near_rowptr": 2, "near_col": 3, "near_val": 4, "green": 5,
           "proj_rowptr": 6, "proj_ent": 7}
 
@@ -44,10 +45,11 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _dev_ptr(t, n, nrhs):
+def _dev_ptr(t, n, nrhs, dtype=None):
     torch = _torch()
-    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128 and t.is_contiguous()):
-        raise TypeError("expected a contiguous complex128 CUDA tensor")
+    dtype = dtype or torch.complex128
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise TypeError(f"expected a contiguous {dtype} CUDA tensor")
     if t.numel() != n * nrhs:
         raise ValueError(f"expected {n * nrhs} elements, got {t.numel()}")
     return ctypes.c_void_p(t.data_ptr())
@@ -67,11 +69,22 @@ class AimPlan:
                                    float(near_radius), int(precision), None, ctypes.byref(out)))
         self._p = out
         self.N = int(self._r.shape[0])
+        self.precision = int(precision)
         self.info = self.plan_info()
 
     @classmethod
-    def from_mesh(cls, mesh, k, h, M, near_radius):
-        return cls(mesh.vertices, mesh.triangles, mesh.rwg, k, h, M, near_radius)
+    def from_mesh(cls, mesh, k, h, M, near_radius, precision=0):
+        return cls(mesh.vertices, mesh.triangles, mesh.rwg, k, h, M, near_radius, precision)
+
+    @property
+    def dtype(self):
+        """torch dtype of the plan's vectors: complex128 (AIM_C128) or complex64 (AIM_C64)."""
+        torch = _torch()
+        return torch.complex64 if self.precision == C64 else torch.complex128
+
+    @property
+    def np_dtype(self):
+        return np.complex64 if self.precision == C64 else np.complex128
 
     def close(self):
         if getattr(self, "_p", None):
@@ -102,12 +115,12 @@ class AimPlan:
         nrhs = 1 if x.dim() == 1 else x.shape[1]
         if y is None:
             y = torch.empty_like(x)
-        _check(_lib.load().aim_matvec(self._p, _dev_ptr(x, self.N, nrhs), _dev_ptr(y, self.N, nrhs), nrhs,
-                                      _stream()))
+        _check(_lib.load().aim_matvec(self._p, _dev_ptr(x, self.N, nrhs, self.dtype),
+                                      _dev_ptr(y, self.N, nrhs, self.dtype), nrhs, _stream()))
         return y
 
     def matvec_host(self, x: np.ndarray, y: np.ndarray | None = None) -> np.ndarray:
-        x = np.ascontiguousarray(x, dtype=np.complex128)
+        x = np.ascontiguousarray(x, dtype=self.np_dtype)
         nrhs = 1 if x.ndim == 1 else x.shape[1]
         if y is None:
             y = np.empty_like(x)
@@ -142,8 +155,8 @@ class AimPlan:
     def project(self, x):
         torch = _torch()
         nrhs = 1 if x.dim() == 1 else x.shape[1]
-        Q = torch.empty(self.grid_numel(nrhs), dtype=torch.complex128, device=x.device)
-        _check(_lib.load().aim_project(self._p, _dev_ptr(x, self.N, nrhs), ctypes.c_void_p(Q.data_ptr()), nrhs,
+        Q = torch.empty(self.grid_numel(nrhs), dtype=self.dtype, device=x.device)
+        _check(_lib.load().aim_project(self._p, _dev_ptr(x, self.N, nrhs, self.dtype), ctypes.c_void_p(Q.data_ptr()), nrhs,
                                        _stream()))
         return Q.view(4, *self.grid_dims, nrhs)
 
@@ -158,7 +171,7 @@ class AimPlan:
     def interpolate(self, Phi, x=None, add_near=False):
         torch = _torch()
         nrhs = Phi.shape[-1] if Phi is not None else (1 if x.dim() == 1 else x.shape[1])
-        y = torch.empty((self.N, nrhs), dtype=torch.complex128, device="cuda")
+        y = torch.empty((self.N, nrhs), dtype=self.dtype, device="cuda")
         _check(_lib.load().aim_interpolate(self._p, ctypes.c_void_p(Phi.data_ptr()) if Phi is not None else None,
                                            ctypes.c_void_p(x.data_ptr()) if x is not None else None,
                                            ctypes.c_void_p(y.data_ptr()), nrhs, 1 if add_near else 0, _stream()))

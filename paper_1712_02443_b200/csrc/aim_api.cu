@@ -78,8 +78,33 @@ static T* upload(aim_plan* p, const std::vector<T>& h) {
     return d;
 }
 
+// complex64 plans (reading D16): round an fp64 table once at plan creation
+__global__ void round_f32_kernel(const double* __restrict__ a, long long n, float* __restrict__ b) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+static float* rounded_copy(aim_plan* p, const double* a, long long n, cudaStream_t s) {
+    float* b = p->alloc<float>(n);
+    round_f32_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(a, n, b);
+    note_launch("round_f32");
+    return b;
+}
+
+void make_c64_tables(aim_plan* p, cudaStream_t s) {
+    p->W32 = rounded_copy(p, p->W, p->N * p->S * 4, s);
+    p->nval32 = (float2*)rounded_copy(p, (const double*)p->nval, 2 * p->nnzN, s);
+    p->spec32 = (float2*)rounded_copy(p, (const double*)p->spec, 2 * p->spec_len, s);
+}
+
+void make_c64_blocks(aim_plan* p, cudaStream_t s) {
+    if (p->nb_val32 || !p->nb_val) return;
+    p->nb_val32 = (float2*)rounded_copy(p, (const double*)p->nb_val, 8 * p->nbc, s);
+    AIM_CUDA(cudaStreamSynchronize(s));
+}
+
 static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, const int32_t* E, int64_t N, double k,
-                   double h, int M, double r, aim_plan* p) {
+                   double h, int M, double r, int prec, aim_plan* p) {
     const auto t0 = std::chrono::steady_clock::now();
     AIM_CUDA(cudaGetDevice(&p->device));
     AIM_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
@@ -87,6 +112,7 @@ static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, co
     AIM_CUDA(cudaEventCreateWithFlags(&p->ev_x, cudaEventDisableTiming));
     AIM_CUDA(cudaEventCreateWithFlags(&p->ev_n, cudaEventDisableTiming));
     p->N = N; p->nt = nt; p->nv = nv; p->k = k; p->h = h; p->M = M; p->r = r;
+    p->prec = prec;
     p->S = (M + 1) * (M + 1) * (M + 1);
 
     // ---- S0: triangle geometry + quadrature
@@ -196,6 +222,7 @@ static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, co
     build_green_spectrum(p, s);
     build_near_list(p, s);
     build_near_values(p, s);
+    if (p->prec == AIM_C64) make_c64_tables(p, s);
     AIM_CUDA(cudaStreamSynchronize(s));
     p->plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -209,6 +236,8 @@ static void destroy(aim_plan* p) {
     for (auto& a : p->allocs) cudaFree(a.first);
     for (int d = 0; d < 3; ++d)
         if (p->ax[d].tw) cudaFree(p->ax[d].tw);
+    for (int d = 0; d < 3; ++d)
+        if (p->ax[d].tw32) cudaFree(p->ax[d].tw32);
     for (auto e : p->ev_pool) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->side) cudaStreamDestroy(p->side);
@@ -233,11 +262,11 @@ int aim_plan_create(const double* vertices, int64_t nv, const int32_t* triangles
     if (nv < 3 || nt < 2 || n_rwg < 1) return fail(AIM_E_ARG, "empty mesh");
     if (!(k > 0) || !(h > 0) || M < 1 || M > 6 || !(near_radius >= 0))
         return fail(AIM_E_ARG, "k, h > 0, M in [1,6], near_radius >= 0 required");
-    if (precision != AIM_C128) return fail(AIM_E_ARG, "only AIM_C128 is implemented");
+    if (precision != AIM_C128 && precision != AIM_C64) return fail(AIM_E_ARG, "precision must be AIM_C128 or AIM_C64");
     if (dist) return fail(AIM_E_ARG, "dist must be NULL (single-GPU plan)");
     aim_plan* p = new aim_plan();
     const int st = guarded([&] {
-        create(vertices, nv, triangles, nt, rwg_edges, n_rwg, k, h, M, near_radius, p);
+        create(vertices, nv, triangles, nt, rwg_edges, n_rwg, k, h, M, near_radius, precision, p);
         return AIM_OK;
     });
     if (st != AIM_OK) {
@@ -278,6 +307,7 @@ int aim_plan_info(const aim_plan* p, aim_info* info) {
     info->device_bytes = p->device_bytes;
     info->plan_seconds = p->plan_seconds;
     info->conv_mode = p->planar;
+    info->precision = p->prec;
     return AIM_OK;
 }
 
@@ -285,7 +315,7 @@ int aim_matvec(aim_plan* p, const void* x, void* y, int32_t nrhs, void* stream) 
     if (!p || !x || !y || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
     if (x == y) return fail(AIM_E_ARG, "x and y must not overlap");
     return guarded([&] {
-        matvec(p, (const double2*)x, (double2*)y, nrhs, (cudaStream_t)stream);
+        matvec(p, x, y, nrhs, (cudaStream_t)stream);
         return AIM_OK;
     });
 }
@@ -293,7 +323,7 @@ int aim_matvec(aim_plan* p, const void* x, void* y, int32_t nrhs, void* stream) 
 int aim_matvec_host(aim_plan* p, const void* xh, void* yh, int32_t nrhs) {
     if (!p || !xh || !yh || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
-        const size_t bytes = sizeof(double2) * (size_t)p->N * nrhs;
+        const size_t bytes = (p->prec == AIM_C64 ? sizeof(float2) : sizeof(double2)) * (size_t)p->N * nrhs;
         if (p->hs_nrhs < nrhs) {
             p->release(p->hx);
             p->release(p->hy);
@@ -313,6 +343,7 @@ int aim_matvec_host(aim_plan* p, const void* xh, void* yh, int32_t nrhs) {
 int aim_gmres(aim_plan* p, const void* V, void* J, int32_t restart, double tol, int32_t max_iters,
               int32_t fixed_iters, int32_t* iters, double* rel_res) {
     if (!p || !V || !J || restart < 1 || !(tol >= 0)) return fail(AIM_E_ARG, "bad argument");
+    if (p->prec != AIM_C128) return fail(AIM_E_ARG, "aim_gmres needs an AIM_C128 plan");
     return guarded([&] {
         int it = 0;
         double rr = 0;
@@ -326,6 +357,7 @@ int aim_gmres(aim_plan* p, const void* V, void* J, int32_t restart, double tol, 
 int aim_planewave_rhs(aim_plan* p, const double* khat, const double* pol, double E0_re, double E0_im, void* V,
                       void* stream) {
     if (!p || !khat || !pol || !V) return fail(AIM_E_ARG, "bad argument");
+    if (p->prec != AIM_C128) return fail(AIM_E_ARG, "aim_planewave_rhs needs an AIM_C128 plan");
     return guarded([&] {
         launch_planewave(p, khat, pol, make_double2(E0_re, E0_im), (double2*)V, (cudaStream_t)stream);
         return AIM_OK;
@@ -335,7 +367,7 @@ int aim_planewave_rhs(aim_plan* p, const double* khat, const double* pol, double
 int aim_project(aim_plan* p, const void* x, void* Q, int32_t nrhs, void* stream) {
     if (!p || !x || !Q || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
-        launch_project(p, (const double2*)x, (double2*)Q, nrhs, (cudaStream_t)stream);
+        launch_project(p, x, Q, nrhs, (cudaStream_t)stream);
         return AIM_OK;
     });
 }
@@ -344,7 +376,7 @@ int aim_convolve(aim_plan* p, const void* Q, void* Phi, int32_t nrhs, void* stre
     if (!p || !Q || !Phi || nrhs < 1) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
         ensure_workspace(p, nrhs);
-        convolve(p, (const double2*)Q, (double2*)Phi, nrhs, (cudaStream_t)stream);
+        convolve(p, Q, Phi, nrhs, (cudaStream_t)stream);
         return AIM_OK;
     });
 }
@@ -354,8 +386,8 @@ int aim_interpolate(aim_plan* p, const void* Phi, const void* x, void* y, int32_
     if (!p || !y || nrhs < 1 || (add_near && !x) || (!Phi && !add_near)) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
         cudaStream_t s = (cudaStream_t)stream;
-        if (add_near) launch_near(p, (const double2*)x, (double2*)y, nrhs, s);
-        if (Phi) launch_interp(p, (const double2*)Phi, (double2*)y, nrhs, add_near != 0, s);
+        if (add_near) launch_near(p, x, y, nrhs, s);
+        if (Phi) launch_interp(p, Phi, y, nrhs, add_near != 0, s);
         return AIM_OK;
     });
 }

@@ -45,12 +45,16 @@ struct FftAxis {
     unsigned long long nsM[kMaxStages] = {0};  // ceil(2^40 / Ns) of each stage (fast divide)
     int min_radix = 1;                          // smallest stage radix
     double2* tw = nullptr;           // device twiddles exp(-2 pi i e / P), e in [0,P)
+    float2* tw32 = nullptr;          // the same rounded to complex64 (AIM_C64 plans)
 };
 
 // One batched 1-D pass over a tensor viewed as [outer][L][inner].
+// Element type of the pass: prec 0 = complex128 (double2), 1 = complex64
+// (float2); the data pointers are typed by it.
 struct FftPass {
-    const double2* in;
-    double2* out;
+    const void* in;
+    void* out;
+    int prec = 0;
     long long outer;     // number of outer slices
     int Lin;             // input length along the axis (zero-padded to P)
     int Lout;            // output length along the axis (pruned from P)
@@ -59,7 +63,7 @@ struct FftPass {
     int mode;            // 0 forward, 1 inverse, 2 turnaround (fwd, x spectrum, inv)
     FftAxis ax;
     // turnaround only: spectrum octant and the (kx, ky) decoding of `outer`
-    const double2* spec;
+    const void* spec;
     int Px, Py;          // outer = (c Px + kx) Py + ky
     int PyH, PzH;        // octant extents Py/2+1, Pz/2+1
 };
@@ -68,11 +72,12 @@ struct FftPass {
 // 2-D spectrum G2[(Px/2+1)][(Py/2+1)][Nz], y inv; in place on [4][Px][Ny][Nz][R].
 constexpr int kPlanarMaxNz = 16;
 struct PlanarPass {
-    double2* W;
+    void* W;
+    int prec = 0;        // as FftPass::prec
     int Px, Ny, Nz, R, RC;
     int PyH;
     FftAxis ay;
-    const double2* spec;
+    const void* spec;
 };
 
 void launch_fft_pass(const FftPass& p, cudaStream_t s);
@@ -115,6 +120,12 @@ struct aim_plan {
     int64_t* nrow = nullptr;      // [N+1]
     int32_t* ncol = nullptr;      // [nnzN]
     double2* nval = nullptr;      // [nnzN]
+    // complex64 plans (reading D16): the fp64 tables rounded once
+    int prec = AIM_C128;
+    float* W32 = nullptr;         // [N][S][4]
+    float2* nval32 = nullptr;     // [nnzN]
+    float2* spec32 = nullptr;     // spectrum, as spec
+    float2* nb_val32 = nullptr;   // [nbc][4]
     // near field in 4-row blocks (multi-RHS products; built on first use):
     // rows of a block are 4 consecutive RWGs in Morton order of their centres,
     // columns the sorted union of the 4 rows' columns, values dense 4 per column
@@ -192,16 +203,18 @@ void build_near_list(aim_plan* p, cudaStream_t s);
 void build_near_values(aim_plan* p, cudaStream_t s);
 void build_green_spectrum(aim_plan* p, cudaStream_t s);
 void build_near_blocks(aim_plan* p, cudaStream_t s);
+void make_c64_blocks(aim_plan* p, cudaStream_t s);   // rounded nb_val for AIM_C64 plans
 
 // ---- matvec launches (k_matvec.cu)
-void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s);
-void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s);
-void launch_near(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
+// x, y, Q, Phi are complex128 (double2) or complex64 (float2) by plan->prec
+void launch_project(const aim_plan* p, const void* x, void* Q, int R, cudaStream_t s);
+void launch_interp(const aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s);
+void launch_near(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
 void launch_planewave(const aim_plan* p, const double* khat, const double* pol, double2 E0, double2* V,
                       cudaStream_t s);
-void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s);
+void convolve(aim_plan* p, const void* Q, void* Phi, int R, cudaStream_t s);
 void ensure_workspace(aim_plan* p, int R);
-void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s);
+void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
 
 // ---- GMRES (k_gmres.cu)
 int gmres(aim_plan* p, const double2* V, double2* J, int restart, double tol, int max_iters, int fixed_iters,

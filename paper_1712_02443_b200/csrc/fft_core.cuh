@@ -13,17 +13,12 @@
 #include <cuda_runtime.h>
 
 #include "aim_internal.cuh"
+#include "cplx.cuh"
 
 namespace aim {
 #ifdef AIM_BOUNDS_DEBUG
 __device__ int g_aim_dbg = 0;
 #endif
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
 // cos / sin (2 pi (m+1) / R), m = 0 .. (R-3)/2, for the odd radices
 template <int R>
@@ -55,44 +50,46 @@ struct Split {
 };
 
 // b_u = sum_t a_t exp(sign 2 pi i t u / R), in place
-template <int R>
-__device__ __forceinline__ void dft(double2* a, double sign) {
+template <int R, class C>
+__device__ __forceinline__ void dft(C* a, double sign_d) {
+    using T = Real<C>;
+    const T sign = (T)sign_d;
     if constexpr (R == 1) {
     } else if constexpr (R != 2 && R != 3 && R != 4 && R != 5 && R != 7) {
         // decimation in time inside registers: Y_r = DFT_B(a[A m + r]),
         // X[k + B s] = DFT_A over r of W_R^{r k} Y_r[k]
         constexpr int A = Split<R>::A, B = Split<R>::B;
-        double2 y[A][B];
+        C y[A][B];
 #pragma unroll
         for (int r = 0; r < A; ++r) {
 #pragma unroll
             for (int m = 0; m < B; ++m) y[r][m] = a[A * m + r];
-            dft<B>(y[r], sign);
+            dft<B>(y[r], sign_d);
         }
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-            double2 t[A];
+            C t[A];
 #pragma unroll
             for (int r = 0; r < A; ++r) {
                 t[r] = y[r][k];
                 if ((r * k) % R) {
-                    double2 w = c_rtw[rtw_off(R) + (r * k) % R];
+                    C w = cvt<C>(c_rtw[rtw_off(R) + (r * k) % R]);
                     if (sign > 0) w.y = -w.y;
                     t[r] = cmul(t[r], w);
                 }
             }
-            dft<A>(t, sign);
+            dft<A>(t, sign_d);
 #pragma unroll
             for (int q = 0; q < A; ++q) a[k + B * q] = t[q];
         }
     } else if constexpr (R == 2) {
-        const double2 t = a[0];
+        const C t = a[0];
         a[0] = cadd(t, a[1]);
         a[1] = csub(t, a[1]);
     } else if constexpr (R == 4) {
-        const double2 t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
-        const double2 t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
-        const double2 t3 = make_double2(-sign * d.y, sign * d.x);  // d * (sign i)
+        const C t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
+        const C t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
+        const C t3 = mkc<C>(-sign * d.y, sign * d.x);  // d * (sign i)
         a[0] = cadd(t0, t2);
         a[2] = csub(t0, t2);
         a[1] = cadd(t1, t3);
@@ -102,31 +99,31 @@ __device__ __forceinline__ void dft(double2* a, double sign) {
         //   b_u     = a0 + sum_t [cos(th) p_t + i sign sin(th) m_t]
         //   b_{R-u} = a0 + sum_t [cos(th) p_t - i sign sin(th) m_t],  th = 2 pi t u / R
         constexpr int H = (R - 1) / 2;
-        double2 p[H], m[H];
+        C p[H], m[H];
 #pragma unroll
         for (int t = 1; t <= H; ++t) {
             p[t - 1] = cadd(a[t], a[R - t]);
             m[t - 1] = csub(a[t], a[R - t]);
         }
-        const double2 a0 = a[0];
-        double2 s0 = a0;
+        const C a0 = a[0];
+        C s0 = a0;
 #pragma unroll
         for (int t = 0; t < H; ++t) s0 = cadd(s0, p[t]);
 #pragma unroll
         for (int u = 1; u <= H; ++u) {
-            double2 re = a0, im = make_double2(0.0, 0.0);
+            C re = a0, im = mkc<C>(0, 0);
 #pragma unroll
             for (int t = 1; t <= H; ++t) {
                 const int idx = (t * u) % R;
-                const double c = idx <= H ? oc<R>(idx - 1) : oc<R>(R - idx - 1);
-                const double s = idx <= H ? os<R>(idx - 1) : -os<R>(R - idx - 1);
+                const T c = (T)(idx <= H ? oc<R>(idx - 1) : oc<R>(R - idx - 1));
+                const T s = (T)(idx <= H ? os<R>(idx - 1) : -os<R>(R - idx - 1));
                 re.x = fma(c, p[t - 1].x, re.x);
                 re.y = fma(c, p[t - 1].y, re.y);
                 im.x = fma(s, m[t - 1].x, im.x);
                 im.y = fma(s, m[t - 1].y, im.y);
             }
-            a[u] = make_double2(re.x - sign * im.y, re.y + sign * im.x);
-            a[R - u] = make_double2(re.x + sign * im.y, re.y - sign * im.x);
+            a[u] = mkc<C>(re.x - sign * im.y, re.y + sign * im.x);
+            a[R - u] = mkc<C>(re.x + sign * im.y, re.y - sign * im.x);
         }
         a[0] = s0;
     }
@@ -151,9 +148,9 @@ struct LineMap {
 };
 
 // One Stockham stage of radix R over NL lines of length P, src -> dst.
-template <int R>
-__device__ __forceinline__ void stage(const double2* __restrict__ src, double2* __restrict__ dst,
-                                      const double2* __restrict__ tw, int P, int NL, int Ns,
+template <int R, class C>
+__device__ __forceinline__ void stage(const C* __restrict__ src, C* __restrict__ dst,
+                                      const C* __restrict__ tw, int P, int NL, int Ns,
                                       unsigned long long nsM, double sign, const LineMap& lm) {
     if (!lm.active) return;
     const int B = P / R;
@@ -162,13 +159,13 @@ __device__ __forceinline__ void stage(const double2* __restrict__ src, double2* 
     for (int j = lm.js; j < B; j += lm.JS) {
         const int jd = fdiv(j, nsM);
         const int k = j - jd * Ns;
-        double2 a[R];
+        C a[R];
 #pragma unroll
         for (int t = 0; t < R; ++t) a[t] = src[(j + t * B) * NL + l];
         if (k) {
 #pragma unroll
             for (int t = 1; t < R; ++t) {
-                double2 w = tw[t * k * stride];  // exp(-2 pi i e / P)
+                C w = tw[t * k * stride];  // exp(-2 pi i e / P)
                 if (sign > 0) w.y = -w.y;
                 a[t] = cmul(a[t], w);
             }
@@ -182,11 +179,12 @@ __device__ __forceinline__ void stage(const double2* __restrict__ src, double2* 
 
 // Full transform of NL lines (sign -1 forward, +1 inverse, unscaled) between
 // the two buffers; returns the buffer holding the result.
-__device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const double2* tw, const FftAxis& ax, int NL,
+template <class C>
+__device__ __forceinline__ C* fft_lines(C* b0, C* b1, const C* tw, const FftAxis& ax, int NL,
                                               double sign, const LineMap& lm) {
     int Ns = 1;
-    double2* src = b0;
-    double2* dst = b1;
+    C* src = b0;
+    C* dst = b1;
     for (int s = 0; s < ax.nst; ++s) {
         const unsigned long long M = ax.nsM[s];
         switch (ax.radix[s]) {
@@ -197,7 +195,7 @@ __device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const do
         }
         __syncthreads();
         Ns *= ax.radix[s];
-        double2* t = src;
+        C* t = src;
         src = dst;
         dst = t;
     }
@@ -209,14 +207,14 @@ __device__ __forceinline__ double2* fft_lines(double2* b0, double2* b1, const do
 // load-to-registers, barrier, compute, store -- a single shared buffer.
 // One fixed register array serves every radix (kept out of the switch so it
 // stays in registers across the barrier).
-template <int R>
-__device__ __forceinline__ void ip_load(double2* a, const double2* __restrict__ buf, int B, int NL, int j, int l) {
+template <int R, class C>
+__device__ __forceinline__ void ip_load(C* a, const C* __restrict__ buf, int B, int NL, int j, int l) {
 #pragma unroll
     for (int t = 0; t < R; ++t) a[t] = buf[(j + t * B) * NL + l];
 }
 
-template <int R>
-__device__ __forceinline__ void ip_store(double2* a, double2* __restrict__ buf, const double2* __restrict__ tw, int P,
+template <int R, class C>
+__device__ __forceinline__ void ip_store(C* a, C* __restrict__ buf, const C* __restrict__ tw, int P,
                                          int NL, int Ns, unsigned long long nsM, double sign, int j, int l) {
     const int stride = P / (Ns * R);
     const int jd = fdiv(j, nsM);
@@ -224,7 +222,7 @@ __device__ __forceinline__ void ip_store(double2* a, double2* __restrict__ buf, 
     if (k) {
 #pragma unroll
         for (int t = 1; t < R; ++t) {
-            double2 w = tw[t * k * stride];
+            C w = tw[t * k * stride];
             if (sign > 0) w.y = -w.y;
             a[t] = cmul(a[t], w);
         }
@@ -237,7 +235,8 @@ __device__ __forceinline__ void ip_store(double2* a, double2* __restrict__ buf, 
 
 // In-place transform with runtime radices (fallback for sizes without a
 // compile-time plan): every thread owns at most ONE butterfly per stage.
-__device__ __forceinline__ void fft_lines_inplace(double2* buf, const double2* tw, const FftAxis& ax, int NL,
+template <class C>
+__device__ __forceinline__ void fft_lines_inplace(C* buf, const C* tw, const FftAxis& ax, int NL,
                                                   double sign, const LineMap& lm) {
     int Ns = 1;
     for (int s = 0; s < ax.nst; ++s) {
@@ -245,7 +244,7 @@ __device__ __forceinline__ void fft_lines_inplace(double2* buf, const double2* t
         const int B = ax.P / R;
         const int j = lm.js;
         const bool mine = lm.active && j < B;
-        double2 a[16];
+        C a[16];
         if (mine) {
             switch (R) {
 #define AIM_LD(RR) case RR: ip_load<RR>(a, buf, B, NL, j, lm.l); break;
@@ -280,9 +279,9 @@ struct MinOf<R, Rs...> { static constexpr int v = R < MinOf<Rs...>::v ? R : MinO
 // Stockham stage src -> dst with compile-time P, Ns, R, line count NL and
 // thread count T: each thread walks butterflies j = tid/NL, += T/NL (one
 // butterfly live at a time: no register array survives a barrier).
-template <int P, int Ns, int R, int SIGN, int NL, int T>
-__device__ __forceinline__ void ctp_stage(const double2* src, double2* dst, const double2* tw) {
-    constexpr double sign = SIGN;
+template <int P, int Ns, int R, int SIGN, int NL, int T, class C>
+__device__ __forceinline__ void ctp_stage(const C* src, C* dst, const C* tw) {
+    constexpr Real<C> sign = SIGN;
     constexpr int B = P / R;
     constexpr int stride = P / (Ns * R);
     constexpr int JS = T / NL;
@@ -291,8 +290,8 @@ __device__ __forceinline__ void ctp_stage(const double2* src, double2* dst, cons
     if (j < JS) {
 #pragma unroll 1
         for (; j < B; j += JS) {
-            double2 a[R];
-            const double2* sp = src + j * NL + l;   // + t * B * NL
+            C a[R];
+            const C* sp = src + j * NL + l;   // + t * B * NL
 #pragma unroll
             for (int t = 0; t < R; ++t) a[t] = sp[t * B * NL];
 #ifdef AIM_BOUNDS_DEBUG
@@ -303,13 +302,13 @@ __device__ __forceinline__ void ctp_stage(const double2* src, double2* dst, cons
             if (Ns > 1 && k) {
 #pragma unroll
                 for (int t = 1; t < R; ++t) {
-                    double2 w = tw[t * k * stride];   // exp(-2 pi i t k stride / P)
+                    C w = tw[t * k * stride];   // exp(-2 pi i t k stride / P)
                     if (sign > 0) w.y = -w.y;
                     a[t] = cmul(a[t], w);
                 }
             }
             dft<R>(a, sign);
-            double2* dp = dst + (jd * Ns * R + k) * NL + l;   // + u * Ns * NL
+            C* dp = dst + (jd * Ns * R + k) * NL + l;   // + u * Ns * NL
 #ifdef AIM_BOUNDS_DEBUG
             if (!((jd * Ns * R + k + (R - 1) * Ns) * NL + l < P * NL)) atomicCAS(&g_aim_dbg, 0, 202);
             if (Ns > 1 && k && !((R - 1) * k * stride < P)) atomicCAS(&g_aim_dbg, 0, 203);
@@ -322,8 +321,8 @@ __device__ __forceinline__ void ctp_stage(const double2* src, double2* dst, cons
 }
 
 // Stages alternate a -> b -> a ...; returns the buffer holding the result.
-template <int SIGN, int NL, int T, int P, int Ns, int R, int... Rs>
-__device__ __forceinline__ double2* ctp_fft(double2* a, double2* b, const double2* tw) {
+template <int SIGN, int NL, int T, int P, int Ns, int R, int... Rs, class C>
+__device__ __forceinline__ C* ctp_fft(C* a, C* b, const C* tw) {
     ctp_stage<P, Ns, R, SIGN, NL, T>(a, b, tw);
     if constexpr (sizeof...(Rs) > 0) return ctp_fft<SIGN, NL, T, P, Ns * R, Rs...>(b, a, tw);
     else return b;
@@ -335,8 +334,8 @@ struct CtpPlan {
     static constexpr int NL = NL_;
     static constexpr int T = T_;
     static constexpr int min_radix = MinOf<Rs...>::v;
-    template <int SIGN>
-    __device__ __forceinline__ static double2* run(double2* a, double2* b, const double2* tw) {
+    template <int SIGN, class C>
+    __device__ __forceinline__ static C* run(C* a, C* b, const C* tw) {
         return ctp_fft<SIGN, NL, T, P, 1, Rs...>(a, b, tw);
     }
 };

@@ -35,6 +35,22 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool va
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 16 : 0)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+// one complex element (16 B complex128 / 8 B complex64), zero-filled if !valid
+template <class C>
+__device__ __forceinline__ void cp_async_c(C* sdst, const C* gsrc, bool valid) {
+    if constexpr (sizeof(C) == 16) cp_async16(sdst, gsrc, valid);
+    else cp_async8(sdst, gsrc, valid);
+}
+template <class C>
+__device__ __forceinline__ const C* tw_of(const FftAxis& ax) {
+    if constexpr (sizeof(C) == 16) return (const C*)ax.tw;
+    else return (const C*)ax.tw32;
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
@@ -44,8 +60,8 @@ struct RtPlan {
     static constexpr int P = 0;
     static constexpr int NL = 0;
     static constexpr bool compile_time = false;
-    template <int SIGN>
-    __device__ __forceinline__ static void run(double2* buf, const double2* tw, const FftAxis& ax, int NL) {
+    template <int SIGN, class C>
+    __device__ __forceinline__ static void run(C* buf, const C* tw, const FftAxis& ax, int NL) {
         const LineMap lm(NL);
         fft_lines_inplace(buf, tw, ax, NL, (double)SIGN, lm);
     }
@@ -72,34 +88,35 @@ using Ct24z7 = CtpPlan<7, 64, 24, 6, 4>;          // planar y/z of C1, one RHS p
 // transformed in place (one butterfly per thread per stage) and stored.
 // Tile indices are 32-bit and advanced incrementally (no 64-bit divides:
 // their call sequences pin registers and cause spills).
-template <class F, int MODE, int MAXT, int MINB>
+template <class F, int MODE, int MAXT, int MINB, class C>
 __global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int tiles) {
-    extern __shared__ double2 sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw);
     const int P = F::compile_time ? F::P : p.ax.P;
     const int TO = p.TO, TI = p.TI, NL = F::compile_time ? F::NL : TO * TI;
-    double2* tw = sm;
-    double2* const buf0 = sm + P;
-    double2* const buf1 = sm + P + (size_t)P * NL;
+    C* tw = sm;
+    C* const buf0 = sm + P;
+    C* const buf1 = sm + P + (size_t)P * NL;
     const int outer = (int)p.outer, inner = (int)p.inner;
     const int tilesI = (inner + TI - 1) / TI;
     const LineMap lm(NL);
     const int o = lm.l / TI, i = lm.l - (lm.l / TI) * TI;
-    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = p.ax.tw[e];
+    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = tw_of<C>(p.ax)[e];
     int t0, t1;
     tile_range(tiles, t0, t1);
     if (t0 >= t1) return;
 
     // (ot, it) = tile coordinates of the tile being loaded
     int ot = t0 / tilesI, itl = t0 - (t0 / tilesI) * tilesI;
-    auto issue = [&](double2* buf) {
+    auto issue = [&](C* buf) {
         if (!lm.active) return;
         const int oo = ot * TO + o, ii = itl * TI + i;
         const bool live = oo < outer && ii < inner;
-        const double2* src = p.in + (live ? (long long)oo * p.Lin * inner + ii : 0);
+        const C* src = ((const C*)p.in) + (live ? (long long)oo * p.Lin * inner + ii : 0);
 #pragma unroll 4
         for (int j = lm.js; j < P; j += lm.JS) {
             const bool v = live && j < p.Lin;
-            cp_async16(&buf[j * NL + lm.l], v ? src + (long long)j * inner : p.in, v);
+            cp_async_c(&buf[j * NL + lm.l], v ? src + (long long)j * inner : (const C*)p.in, v);
         }
     };
     auto advance = [&]() {
@@ -111,7 +128,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int til
     advance();
     for (int t = t0; t < t1; ++t) {
         const bool odd = (t - t0) & 1;
-        double2* buf = odd ? buf1 : buf0;
+        C* buf = odd ? buf1 : buf0;
         if (t + 1 < t1) issue(odd ? buf0 : buf1);
         cp_commit();
         cp_wait_prev();
@@ -127,7 +144,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int til
                     const int ky = og % p.Py;
                     const int kx = (og / p.Py) % p.Px;
                     const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
-                    const double2* g = p.spec + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                    const C* g = ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
                     for (int j = lm.js; j < P; j += lm.JS)
                         buf[j * NL + lm.l] = cmul(buf[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
                 }
@@ -138,7 +155,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int til
         // tile store with fused pruning
         const int oo = cur_o * TO + o, ii = cur_i * TI + i;
         if (lm.active && oo < outer && ii < inner) {
-            double2* dst = p.out + (long long)oo * p.Lout * inner + ii;
+            C* dst = ((C*)p.out) + (long long)oo * p.Lout * inner + ii;
 #pragma unroll 4
             for (int j = lm.js; j < p.Lout; j += lm.JS) __stcs(dst + (long long)j * inner, buf[j * NL + lm.l]);
         }
@@ -152,28 +169,28 @@ __global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int til
 // z step of the planar pass: out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'] for
 // every (ky, rl), one line per thread, all indices compile-time (inputs in
 // registers), symmetric Toeplitz: out[z] = g0 in[z] + sum_{d>0} g_d (in[z-d] + in[z+d]).
-template <int NZ>
-__device__ __forceinline__ void planar_toeplitz(double2* buf, const double2* g2, int Py, int RC, int NL) {
+template <int NZ, class C>
+__device__ __forceinline__ void planar_toeplitz(C* buf, const C* g2, int Py, int RC, int NL) {
 #pragma unroll 1
     for (int line = threadIdx.x; line < Py * RC; line += blockDim.x) {
         const int ky = line / RC, rr = line - (line / RC) * RC;
         const int ay = min(ky, Py - ky);
-        const double2* g = g2 + ay * NZ;
-        double2* row = buf + ky * NL + rr;   // + zz * RC
-        double2 gk[NZ], in[NZ];
+        const C* g = g2 + ay * NZ;
+        C* row = buf + ky * NL + rr;   // + zz * RC
+        C gk[NZ], in[NZ];
 #pragma unroll
         for (int d = 0; d < NZ; ++d) gk[d] = __ldg(&g[d]);
 #pragma unroll
         for (int zz = 0; zz < NZ; ++zz) in[zz] = row[zz * RC];
 #pragma unroll
         for (int zz = 0; zz < NZ; ++zz) {
-            double2 acc = cmul(gk[0], in[zz]);
+            C acc = cmul(gk[0], in[zz]);
 #pragma unroll
             for (int d = 1; d < NZ; ++d) {
                 if (zz - d < 0 && zz + d >= NZ) continue;
-                double2 sum = zz - d >= 0 ? in[zz - d] : make_double2(0.0, 0.0);
+                C sum = zz - d >= 0 ? in[zz - d] : mkc<C>(0, 0);
                 if (zz + d < NZ) sum = zz - d >= 0 ? cadd(sum, in[zz + d]) : in[zz + d];
-                const double2 gd = gk[d];
+                const C gd = gk[d];
                 acc.x = fma(gd.x, sum.x, fma(-gd.y, sum.y, acc.x));
                 acc.y = fma(gd.x, sum.y, fma(gd.y, sum.x, acc.y));
             }
@@ -186,34 +203,35 @@ __device__ __forceinline__ void planar_toeplitz(double2* buf, const double2* g2,
 // Persistent CTAs, three tile buffers: X holds the tile being transformed, Y
 // is the ping-pong scratch, Z receives the next tile by cp.async; X and Z
 // swap after every tile.  All sizes compile-time (F::P, F::NL, F::T).
-template <class F, int MODE, int MINB>
+template <class F, int MODE, int MINB, class C>
 __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles) {
     constexpr int P = F::P, NL = F::NL, T = F::T, JS = T / NL;
-    extern __shared__ double2 sm[];
-    double2* tw = sm;
-    double2* X = sm + P;
-    double2* Y = X + P * NL;
-    double2* Z = Y + P * NL;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw);
+    C* tw = sm;
+    C* X = sm + P;
+    C* Y = X + P * NL;
+    C* Z = Y + P * NL;
     const int TI = p.TI;
     const int outer = (int)p.outer, inner = (int)p.inner;
     const int tilesI = (inner + TI - 1) / TI;
     const int l = threadIdx.x % NL, js = threadIdx.x / NL;
     const bool act = js < JS;
     const int o = l / TI, i = l - (l / TI) * TI;
-    for (int e = threadIdx.x; e < P; e += T) tw[e] = p.ax.tw[e];
+    for (int e = threadIdx.x; e < P; e += T) tw[e] = tw_of<C>(p.ax)[e];
     int t0, t1;
     tile_range(tiles, t0, t1);
     if (t0 >= t1) return;
     int ot = t0 / tilesI, itl = t0 - (t0 / tilesI) * tilesI;
-    auto issue = [&](double2* buf) {
+    auto issue = [&](C* buf) {
         if (!act) return;
         const int oo = ot * (NL / TI) + o, ii = itl * TI + i;
         const bool live = oo < outer && ii < inner;
-        const double2* src = p.in + (live ? (long long)oo * p.Lin * inner + ii : 0);
+        const C* src = ((const C*)p.in) + (live ? (long long)oo * p.Lin * inner + ii : 0);
 #pragma unroll 2
         for (int j = js; j < P; j += JS) {
             const bool v = live && j < p.Lin;
-            cp_async16(&buf[j * NL + l], v ? src + (long long)j * inner : p.in, v);
+            cp_async_c(&buf[j * NL + l], v ? src + (long long)j * inner : (const C*)p.in, v);
         }
     };
     auto advance = [&]() {
@@ -228,7 +246,7 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
         cp_commit();
         cp_wait_prev();
         __syncthreads();
-        double2* res;
+        C* res;
         if constexpr (MODE == 1) {
             res = F::template run<+1>(X, Y, tw);
         } else {
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
                     const int ky = og % p.Py;
                     const int kx = (og / p.Py) % p.Px;
                     const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
-                    const double2* g = p.spec + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                    const C* g = ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
                     for (int j = js; j < P; j += JS) res[j * NL + l] = cmul(res[j * NL + l], __ldg(&g[min(j, P - j)]));
                 }
                 __syncthreads();
@@ -248,14 +266,14 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
         }
         const int oo = cur_o * (NL / TI) + o, ii = cur_i * TI + i;
         if (act && oo < outer && ii < inner) {
-            double2* dst = p.out + (long long)oo * p.Lout * inner + ii;
+            C* dst = ((C*)p.out) + (long long)oo * p.Lout * inner + ii;
 #pragma unroll 2
             for (int j = js; j < p.Lout; j += JS) __stcs(dst + (long long)j * inner, res[j * NL + l]);
         }
         cur_o = ot;
         cur_i = itl;
         advance();
-        double2* tmp = X;
+        C* tmp = X;
         X = Z;
         Z = tmp;
         __syncthreads();
@@ -266,15 +284,16 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
 // buffers (X being transformed, Y ping-pong scratch, Z receiving the next
 // tile by cp.async); the twiddles and the G2 slice are read through L1
 // (__ldg) so two CTAs fit per SM (barrier stalls of one overlap the other).
-template <int NZ, class F, int MINB>
+template <int NZ, class F, int MINB, class C>
 __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int tiles) {
     constexpr int Py = F::P, NL = F::NL, T = F::T, JS = T / NL;
     static_assert(NL == NZ, "one RHS per tile");
-    extern __shared__ double2 sm[];
-    double2* X = sm;
-    double2* Y = X + Py * NL;
-    double2* Z = Y + Py * NL;
-    const double2* tw = p.ay.tw;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw);
+    C* X = sm;
+    C* Y = X + Py * NL;
+    C* Z = Y + Py * NL;
+    const C* tw = tw_of<C>(p.ay);
     const int nchunk = p.R;
     const int l = threadIdx.x % NL, js = threadIdx.x / NL;   // l = z
     const bool act = js < JS;
@@ -283,17 +302,17 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
     tile_range(tiles, t0, t1);
     if (t0 >= t1) return;
     int lkx = t0 / (4 * nchunk), lc = (t0 / nchunk) % 4, lch = t0 % nchunk;
-    auto base_of = [&](int kx, int c, int r) -> double2* {
+    auto base_of = [&](int kx, int c, int r) -> C* {
         const long long plane = (long long)c * p.Px + kx;
-        return p.W + plane * p.Ny * ystride + l * p.R + r;   // + y * ystride
+        return ((C*)p.W) + plane * p.Ny * ystride + l * p.R + r;   // + y * ystride
     };
-    auto issue = [&](double2* buf) {
+    auto issue = [&](C* buf) {
         if (!act) return;
-        const double2* src = base_of(lkx, lc, lch);
+        const C* src = base_of(lkx, lc, lch);
 #pragma unroll 2
         for (int y = js; y < Py; y += JS) {
             const bool v = y < p.Ny;
-            cp_async16(&buf[y * NL + l], v ? src + y * ystride : p.W, v);
+            cp_async_c(&buf[y * NL + l], v ? src + y * ystride : (const C*)p.W, v);
         }
     };
     auto advance = [&]() {
@@ -312,19 +331,19 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
         cp_wait_prev();
         __syncthreads();
         const int ax_ = min(ckx, p.Px - ckx);
-        const double2* g2 = p.spec + (long long)ax_ * p.PyH * NZ;
-        double2* res = F::template run<-1>(X, Y, tw);
+        const C* g2 = ((const C*)p.spec) + (long long)ax_ * p.PyH * NZ;
+        C* res = F::template run<-1>(X, Y, tw);
         planar_toeplitz<NZ>(res, g2, Py, 1, NL);
         __syncthreads();
         res = F::template run<+1>(res, res == X ? Y : X, tw);
         if (act) {
-            double2* dst = base_of(ckx, cc, cch);
+            C* dst = base_of(ckx, cc, cch);
 #pragma unroll 2
             for (int y = js; y < p.Ny; y += JS) __stcs(dst + y * ystride, res[y * NL + l]);
         }
         ckx = lkx; cc = lc; cch = lch;
         advance();
-        double2* tmp = X;
+        C* tmp = X;
         X = Z;
         Z = tmp;
         __syncthreads();
@@ -333,14 +352,16 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
 
 // Ping-pong fallback (lines too long for one butterfly per thread): one tile
 // per CTA, two buffers.
+template <class C>
 __global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
-    extern __shared__ double2 sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw);
     const int P = p.ax.P;
     const int TO = p.TO, TI = p.TI;
     const int NL = TO * TI;
-    double2* buf = sm;
-    double2* alt = sm + (size_t)P * NL;
-    double2* tw = sm + (size_t)2 * P * NL;
+    C* buf = sm;
+    C* alt = sm + (size_t)P * NL;
+    C* tw = sm + (size_t)2 * P * NL;
 
     const long long tilesI = (p.inner + TI - 1) / TI;
     const long long o0 = (long long)(blockIdx.x / tilesI) * TO;
@@ -350,19 +371,19 @@ __global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
     const LineMap lm(NL);
     const int o = lm.l / TI, i = lm.l - (lm.l / TI) * TI;
     const bool live = lm.active && o < to_n && i < ti_n;
-    const double2* src = p.in + (o0 + o) * p.Lin * p.inner + i0 + i;
+    const C* src = ((const C*)p.in) + (o0 + o) * p.Lin * p.inner + i0 + i;
 
-    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = p.ax.tw[e];
+    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = tw_of<C>(p.ax)[e];
     if (lm.active)
         for (int j = lm.js; j < P; j += lm.JS) {
             const bool v = live && j < p.Lin;
-            cp_async16(&buf[j * NL + lm.l], v ? src + (long long)j * p.inner : p.in, v);
+            cp_async_c(&buf[j * NL + lm.l], v ? src + (long long)j * p.inner : (const C*)p.in, v);
         }
     cp_commit();
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
 
-    double2* res = buf;
+    C* res = buf;
     if (p.mode == 1) {
         res = fft_lines(buf, alt, tw, p.ax, NL, +1.0, lm);
     } else {
@@ -373,7 +394,7 @@ __global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
                 const int ky = (int)(og % p.Py);
                 const int kx = (int)((og / p.Py) % p.Px);
                 const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
-                const double2* g = p.spec + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                const C* g = ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
                 for (int j = lm.js; j < P; j += lm.JS) res[j * NL + lm.l] = cmul(res[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
             }
             __syncthreads();
@@ -381,7 +402,7 @@ __global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
         }
     }
     if (live) {
-        double2* dst = p.out + (o0 + o) * p.Lout * p.inner + i0 + i;
+        C* dst = ((C*)p.out) + (o0 + o) * p.Lout * p.inner + i0 + i;
         for (int j = lm.js; j < p.Lout; j += lm.JS) __stcs(dst + (long long)j * p.inner, res[j * NL + lm.l]);
     }
 }
@@ -392,40 +413,41 @@ constexpr int kPlanarThreads = 256;   // max; launched with >= one butterfly per
 // ordered kx-major (a CTA's tile range touches the G2 slices of one or two kx,
 // read through L1).  smem: twiddles [Py], two tile buffers [Py][NZ*RC]
 // (y lines indexed by l = z*RC + rl).
-template <int NZ, class F, int MAXT, int MINB>
+template <int NZ, class F, int MAXT, int MINB, class C>
 __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int tiles) {
-    extern __shared__ double2 sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw);
     const int Py = F::compile_time ? F::P : p.ay.P;
     const int RC = F::compile_time ? 1 : p.RC;
     const int NL = NZ * RC;
-    double2* tw = sm;
-    double2* const buf0 = sm + Py;
-    double2* const buf1 = buf0 + (size_t)Py * NL;
+    C* tw = sm;
+    C* const buf0 = sm + Py;
+    C* const buf1 = buf0 + (size_t)Py * NL;
     const int nchunk = (p.R + RC - 1) / RC;
     const LineMap lm(NL);
     const int z = lm.l / RC, rl = lm.l - (lm.l / RC) * RC;
     const int ystride = NZ * p.R;
-    for (int e = threadIdx.x; e < Py; e += blockDim.x) tw[e] = p.ay.tw[e];
+    for (int e = threadIdx.x; e < Py; e += blockDim.x) tw[e] = tw_of<C>(p.ay)[e];
     int t0, t1;
     tile_range(tiles, t0, t1);
     if (t0 >= t1) return;
 
     // tile t -> (kx, c, chunk) = (t / (4 nchunk), (t / nchunk) % 4, t % nchunk); advanced incrementally
     int lkx = t0 / (4 * nchunk), lc = (t0 / nchunk) % 4, lch = t0 % nchunk;
-    auto base_of = [&](int kx, int c, int ch, bool& live) -> double2* {
+    auto base_of = [&](int kx, int c, int ch, bool& live) -> C* {
         const int r0 = ch * RC;
         live = lm.active && r0 + rl < p.R;
         const long long plane = (long long)c * p.Px + kx;
-        return p.W + plane * p.Ny * ystride + z * p.R + r0 + rl;   // + y * ystride
+        return ((C*)p.W) + plane * p.Ny * ystride + z * p.R + r0 + rl;   // + y * ystride
     };
-    auto issue = [&](double2* buf) {
+    auto issue = [&](C* buf) {
         if (!lm.active) return;
         bool live;
-        const double2* src = base_of(lkx, lc, lch, live);
+        const C* src = base_of(lkx, lc, lch, live);
 #pragma unroll 4
         for (int y = lm.js; y < Py; y += lm.JS) {
             const bool v = live && y < p.Ny;
-            cp_async16(&buf[y * NL + lm.l], v ? src + y * ystride : p.W, v);
+            cp_async_c(&buf[y * NL + lm.l], v ? src + y * ystride : (const C*)p.W, v);
         }
     };
     auto advance = [&]() {
@@ -440,19 +462,19 @@ __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int
     advance();
     for (int t = t0; t < t1; ++t) {
         const bool odd = (t - t0) & 1;
-        double2* buf = odd ? buf1 : buf0;
+        C* buf = odd ? buf1 : buf0;
         if (t + 1 < t1) issue(odd ? buf0 : buf1);
         cp_commit();
         cp_wait_prev();
         const int ax_ = min(ckx, p.Px - ckx);
-        const double2* g2 = p.spec + (long long)ax_ * p.PyH * NZ;   // G2 slice of this kx (read through L1)
+        const C* g2 = ((const C*)p.spec) + (long long)ax_ * p.PyH * NZ;   // G2 slice of this kx (read through L1)
         __syncthreads();
         F::template run<-1>(buf, tw, p.ay, NL);
         planar_toeplitz<NZ>(buf, g2, Py, RC, NL);
         __syncthreads();
         F::template run<+1>(buf, tw, p.ay, NL);
         bool live;
-        double2* dst = base_of(ckx, cc, cch, live);
+        C* dst = base_of(ckx, cc, cch, live);
         if (live) {
 #pragma unroll 4
             for (int y = lm.js; y < p.Ny; y += lm.JS) __stcs(dst + y * ystride, buf[y * NL + lm.l]);
@@ -539,6 +561,10 @@ void make_fft_axis(int P, FftAxis& ax) {
     }
     AIM_CUDA(cudaMalloc(&ax.tw, sizeof(double2) * P));
     AIM_CUDA(cudaMemcpy(ax.tw, h.data(), sizeof(double2) * P, cudaMemcpyHostToDevice));
+    std::vector<float2> h32(P);
+    for (int e = 0; e < P; ++e) h32[e] = make_float2((float)h[e].x, (float)h[e].y);
+    AIM_CUDA(cudaMalloc(&ax.tw32, sizeof(float2) * P));
+    AIM_CUDA(cudaMemcpy(ax.tw32, h32.data(), sizeof(float2) * P, cudaMemcpyHostToDevice));
 }
 
 static constexpr int kFftThreads = 256;
@@ -585,12 +611,12 @@ static void tile_shape(FftPass& p, int nl) {
     p.TO = std::min(p.TO, std::max(1, nl / p.TI));
 }
 
-template <class K>
+template <class C, class K>
 static void launch_pipe(K kern, const FftPass& p, int threads, cudaStream_t s) {
     const int P = p.ax.P;
     const long long tiles = ((p.inner + p.TI - 1) / p.TI) * ((p.outer + p.TO - 1) / p.TO);
     if (tiles <= 0) return;
-    const size_t smem = sizeof(double2) * ((size_t)2 * P * p.TO * p.TI + P);
+    const size_t smem = sizeof(C) * ((size_t)2 * P * p.TO * p.TI + P);
     if (smem > 227 * 1024) throw Error(AIM_E_GRID, "FFT length exceeds the shared-memory tile capacity");
     ensure_smem_attr(kern);
     const long long grid = persistent_grid(kern, threads, smem, tiles);
@@ -602,7 +628,7 @@ static void launch_pipe(K kern, const FftPass& p, int threads, cudaStream_t s) {
                                     " smem=" + std::to_string(smem) + ": " + cudaGetErrorString(e));
 }
 
-template <class F, int MINB>
+template <class C, class F, int MINB>
 static bool try_ct_pass(FftPass p, cudaStream_t s) {
     if (p.ax.P != F::P || p.TI > 0) return false;
     // F::NL lines: TI = the largest power of two <= inner dividing NL, TO = NL / TI
@@ -612,7 +638,7 @@ static bool try_ct_pass(FftPass p, cudaStream_t s) {
     p.TI = ti;
     p.TO = F::NL / ti;
     const long long tiles = ((p.inner + p.TI - 1) / p.TI) * ((p.outer + p.TO - 1) / p.TO);
-    const size_t smem = sizeof(double2) * ((size_t)3 * F::P * F::NL + F::P);
+    const size_t smem = sizeof(C) * ((size_t)3 * F::P * F::NL + F::P);
     auto go = [&](auto kern) {
         ensure_smem_attr(kern);
         const long long grid = persistent_grid(kern, F::T, smem, tiles);
@@ -621,54 +647,56 @@ static bool try_ct_pass(FftPass p, cudaStream_t s) {
         if (e != cudaSuccess)
             throw Error(AIM_E_CUDA, "fft_ct_kernel P=" + std::to_string(F::P) + ": " + cudaGetErrorString(e));
     };
-    if (p.mode == 0) go(fft_ct_kernel<F, 0, MINB>);
-    else if (p.mode == 1) go(fft_ct_kernel<F, 1, MINB>);
-    else go(fft_ct_kernel<F, 2, MINB>);
+    if (p.mode == 0) go(fft_ct_kernel<F, 0, MINB, C>);
+    else if (p.mode == 1) go(fft_ct_kernel<F, 1, MINB, C>);
+    else go(fft_ct_kernel<F, 2, MINB, C>);
     return true;
 }
 
-void launch_fft_pass(const FftPass& p0, cudaStream_t s) {
-    FftPass p = p0;
+template <class C>
+static void launch_fft_pass_t(FftPass p, cudaStream_t s) {
     const int P = p.ax.P;
-    if (p.outer <= 0 || p.inner <= 0) return;
-    if (try_ct_pass<Ct210, 2>(p, s) || try_ct_pass<Ct24, 2>(p, s)) {
-        note_launch("fft_pass");
-        return;
-    }
+    if (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s)) return;
     // runtime radices: in place when one butterfly per thread per stage suffices for >= 2 lines
     const int nl_inplace = kFftThreads * p.ax.min_radix / P;
     const bool inplace = nl_inplace >= 2;
     const int cap = std::max(fft_tile_capacity(), P);
     if (p.TI <= 0) tile_shape(p, inplace ? nl_inplace : std::max(1, cap / P));
     if (inplace) {
-        if (p.mode == 0) launch_pipe(fft_pipe_kernel<RtPlan, 0, kFftThreads, 2>, p, kFftThreads, s);
-        else if (p.mode == 1) launch_pipe(fft_pipe_kernel<RtPlan, 1, kFftThreads, 2>, p, kFftThreads, s);
-        else launch_pipe(fft_pipe_kernel<RtPlan, 2, kFftThreads, 2>, p, kFftThreads, s);
+        if (p.mode == 0) launch_pipe<C>(fft_pipe_kernel<RtPlan, 0, kFftThreads, 2, C>, p, kFftThreads, s);
+        else if (p.mode == 1) launch_pipe<C>(fft_pipe_kernel<RtPlan, 1, kFftThreads, 2, C>, p, kFftThreads, s);
+        else launch_pipe<C>(fft_pipe_kernel<RtPlan, 2, kFftThreads, 2, C>, p, kFftThreads, s);
     } else {
         const long long tiles = ((p.inner + p.TI - 1) / p.TI) * ((p.outer + p.TO - 1) / p.TO);
-        const size_t smem = sizeof(double2) * ((size_t)2 * P * p.TO * p.TI + P);
+        const size_t smem = sizeof(C) * ((size_t)2 * P * p.TO * p.TI + P);
         if (smem > 227 * 1024) throw Error(AIM_E_GRID, "FFT length exceeds the shared-memory tile capacity");
-        ensure_smem_attr(fft_pp_kernel);
-        fft_pp_kernel<<<(unsigned)tiles, kFftThreads, smem, s>>>(p);
+        ensure_smem_attr(fft_pp_kernel<C>);
+        fft_pp_kernel<C><<<(unsigned)tiles, kFftThreads, smem, s>>>(p);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess)
             throw Error(AIM_E_CUDA, "fft_pp_kernel P=" + std::to_string(P) + " tiles=" + std::to_string(tiles) +
                                         " smem=" + std::to_string(smem) + ": " + cudaGetErrorString(e));
     }
+}
+
+void launch_fft_pass(const FftPass& p, cudaStream_t s) {
+    if (p.outer <= 0 || p.inner <= 0) return;
+    if (p.prec == 1) launch_fft_pass_t<float2>(p, s);
+    else launch_fft_pass_t<double2>(p, s);
     note_launch("fft_pass");
 }
 
 // planar pass: one CTA holds a (Py x Nz) plane in place, one butterfly per thread per stage
 bool planar_supported(int Py, int Nz, int min_radix) {
-    const size_t smem = sizeof(double2) * ((size_t)2 * Py * Nz + (size_t)(Py / 2 + 1) * Nz + Py);
+    const size_t smem = sizeof(double2) * ((size_t)2 * Py * Nz + Py);
     return Nz <= kPlanarMaxNz && (long long)Nz * Py / min_radix <= kPlanarThreads && smem <= 200 * 1024;
 }
 
-template <class K>
+template <class C, class K>
 static void launch_planar(K kern, const PlanarPass& p, int threads, cudaStream_t s) {
     const int Py = p.ay.P;
     const long long tiles = 4LL * p.Px * ((p.R + p.RC - 1) / p.RC);
-    const size_t smem = sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py);
+    const size_t smem = sizeof(C) * ((size_t)2 * Py * p.Nz * p.RC + Py);
     ensure_smem_attr(kern);
     const long long grid = persistent_grid(kern, threads, smem, tiles);
     kern<<<(unsigned)grid, threads, smem, s>>>(p, (int)tiles);
@@ -679,50 +707,43 @@ static void launch_planar(K kern, const PlanarPass& p, int threads, cudaStream_t
                                     " smem=" + std::to_string(smem) + ": " + cudaGetErrorString(e));
 }
 
-template <int NZ, class F, int MINB>
+template <class C, int NZ, class F, int MINB>
 static bool try_ct_planar(PlanarPass p, cudaStream_t s) {
     if (p.ay.P != F::P || p.Nz != NZ || p.PyH != F::P / 2 + 1) return false;
     p.RC = 1;
     const long long tiles = 4LL * p.Px * p.R;
-    const size_t smem = sizeof(double2) * ((size_t)3 * F::P * NZ);
-    auto kern = planar_ct_kernel<NZ, F, MINB>;
+    const size_t smem = sizeof(C) * ((size_t)3 * F::P * NZ);
+    auto kern = planar_ct_kernel<NZ, F, MINB, C>;
     ensure_smem_attr(kern);
     const long long grid = persistent_grid(kern, F::T, smem, tiles);
     kern<<<(unsigned)grid, F::T, smem, s>>>(p, (int)tiles);
-#ifdef AIM_BOUNDS_DEBUG
-    {
-        cudaDeviceSynchronize();
-        int flag = 0;
-        cudaMemcpyFromSymbol(&flag, g_aim_dbg, sizeof(int));
-        if (flag) throw Error(AIM_E_CUDA, "planar_ct_kernel bounds check " + std::to_string(flag));
-    }
-#endif
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         throw Error(AIM_E_CUDA, "planar_ct_kernel Py=" + std::to_string(F::P) + ": " + cudaGetErrorString(e));
     return true;
 }
 
-void launch_planar_yz(const PlanarPass& p0, cudaStream_t s) {
-    PlanarPass p = p0;
-    if (try_ct_planar<11, Ct210z11, 2>(p, s) || try_ct_planar<7, Ct24z7, 2>(p, s)) {
-        note_launch("planar_yz");
-        return;
-    }
+template <class C>
+static void launch_planar_yz_t(PlanarPass p, cudaStream_t s) {
+    if (try_ct_planar<C, 11, Ct210z11, 2>(p, s) || try_ct_planar<C, 7, Ct24z7, 2>(p, s)) return;
     const int Py = p.ay.P;
     const int rc_fft = (int)(kPlanarThreads * (long long)p.ay.min_radix / ((long long)Py * p.Nz));
     p.RC = std::max(1, std::min({p.R, rc_fft, kPlanarThreads / p.Nz}));
-    while (p.RC > 1 && sizeof(double2) * ((size_t)2 * Py * p.Nz * p.RC + Py) > 110 * 1024)
-        --p.RC;
+    while (p.RC > 1 && sizeof(C) * ((size_t)2 * Py * p.Nz * p.RC + Py) > 110 * 1024) --p.RC;
     // one butterfly per thread per FFT stage; one (ky, rhs) z line per thread in the convolution
     const int bfly = (int)((long long)p.Nz * p.RC * Py / p.ay.min_radix);
     const int threads = std::min(kPlanarThreads, 32 * ((std::max({bfly, Py * p.RC, p.Nz * p.RC}) + 31) / 32));
     switch (p.Nz) {
-#define PZ(NZ) case NZ: launch_planar(planar_yz_kernel<NZ, RtPlan, kPlanarThreads, 2>, p, threads, s); break;
+#define PZ(NZ) case NZ: launch_planar<C>(planar_yz_kernel<NZ, RtPlan, kPlanarThreads, 2, C>, p, threads, s); break;
         PZ(1) PZ(2) PZ(3) PZ(4) PZ(5) PZ(6) PZ(7) PZ(8) PZ(9) PZ(10) PZ(11) PZ(12) PZ(13) PZ(14) PZ(15) PZ(16)
 #undef PZ
         default: throw Error(AIM_E_GRID, "planar pass: Nz out of range");
     }
+}
+
+void launch_planar_yz(const PlanarPass& p, cudaStream_t s) {
+    if (p.prec == 1) launch_planar_yz_t<float2>(p, s);
+    else launch_planar_yz_t<double2>(p, s);
     note_launch("planar_yz");
 }
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include "aim_internal.cuh"
+#include "cplx.cuh"
 
 namespace aim {
 
@@ -26,9 +27,6 @@ static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) 
 #endif
 constexpr int kGatherUnroll = AIM_GATHER_UNROLL;   // gather steps in flight per lane
 
-__device__ __forceinline__ double2 shfl_xor2(double2 v, int m) {
-    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
-}
 
 // Lane layout of the gather kernels: LPE lanes share one CSR entry and each
 // holds RPL right-hand sides (r = r0 + sub + q*LPE), so a warp consumes
@@ -49,27 +47,27 @@ struct Lanes {
 
 // ------------------------------------------------------------ H1 projection
 // Q^psi[u,r] = sum_{n in col(u)} w^psi_{n,u} x[n,r]; warp per grid node.
-template <int M, int LPE, int RPL>
+template <int M, int LPE, int RPL, class C>
 __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict__ prow,
                                                       const int32_t* __restrict__ pent,
-                                                      const double* __restrict__ W, const double2* __restrict__ x,
-                                                      long long Ng, int R, double2* __restrict__ Q) {
+                                                      const Real<C>* __restrict__ W, const C* __restrict__ x,
+                                                      long long Ng, int R, C* __restrict__ Q) {
     constexpr int S = (M + 1) * (M + 1) * (M + 1);
     using L = Lanes<LPE, RPL>;
     const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (g >= Ng) return;
     const L ln;
     const int e0 = prow[g], e1 = prow[g + 1];
-    const double2* W2 = reinterpret_cast<const double2*>(W);
+    const C* W2 = reinterpret_cast<const C*>(W);
     for (int r0 = 0; r0 < R; r0 += L::RC) {
-        double2 a[4][RPL];
+        C a[4][RPL];
 #pragma unroll
         for (int q = 0; q < RPL; ++q)
-            for (int c = 0; c < 4; ++c) a[c][q] = make_double2(0, 0);
+            for (int c = 0; c < 4; ++c) a[c][q] = mkc<C>(0, 0);
         for (int b = e0; b < e1; b += 32) {
             const int cnt = min(32, e1 - b);
             int n_l = 0;
-            double2 w01 = make_double2(0, 0), w23 = w01;
+            C w01 = mkc<C>(0, 0), w23 = w01;
             if (ln.lane < cnt) {
                 const int ent = __ldg(&pent[b + ln.lane]);
                 n_l = ent / S;
@@ -79,7 +77,7 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
 #pragma unroll kGatherUnroll
             for (int t = ln.grp; t < 32; t += L::G) {
                 int n;
-                double w[4];
+                Real<C> w[4];
                 if (LPE == 1) {
                     n = n_l; w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
                 } else {
@@ -88,11 +86,11 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
                     w[2] = __shfl_sync(0xffffffffu, w23.x, t); w[3] = __shfl_sync(0xffffffffu, w23.y, t);
                 }
                 if (t < cnt) {
-                    const double2* xr = x + (long long)n * R + r0 + ln.sub;
+                    const C* xr = x + (long long)n * R + r0 + ln.sub;
 #pragma unroll
                     for (int q = 0; q < RPL; ++q) {
                         if (r0 + ln.sub + q * LPE < R) {
-                            const double2 xv = __ldg(xr + q * LPE);
+                            const C xv = __ldg(xr + q * LPE);
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
                                 a[c][q].x = fma(w[c], xv.x, a[c][q].x);
@@ -109,7 +107,7 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
             for (int c = 0; c < 4; ++c)
 #pragma unroll
                 for (int q = 0; q < RPL; ++q) {
-                    const double2 t = shfl_xor2(a[c][q], off);
+                    const C t = shfl_xor2(a[c][q], off);
                     a[c][q].x += t.x; a[c][q].y += t.y;
                 }
         if (ln.grp == 0) {
@@ -141,14 +139,15 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
     else if (R <= 16) { CALL(16 / AIM_GATHER_RPL16, AIM_GATHER_RPL16); } \
     else { CALL(32, 1); }
 
-void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cudaStream_t s) {
+template <class C>
+static void launch_project_t(const aim_plan* p, const C* x, C* Q, int R, cudaStream_t s) {
     const unsigned grid = nblk(p->Ng * 32, 256);
-#define PJ_CALL(LPE, RPL) project_kernel<MM, LPE, RPL><<<grid, 256, 0, s>>>(p->prow, p->pent, p->W, x, p->Ng, R, Q)
+    const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->W : (const void*)p->W32);
+#define PJ_CALL(LPE, RPL) project_kernel<MM, LPE, RPL, C><<<grid, 256, 0, s>>>(p->prow, p->pent, W, x, p->Ng, R, Q)
 #define PJ_M(MMV)                                   \
     if (p->M == MMV) {                              \
         constexpr int MM = MMV;                     \
-        AIM_LANE_DISPATCH_GATHER(R, PJ_CALL)               \
-        note_launch("project");                     \
+        AIM_LANE_DISPATCH_GATHER(R, PJ_CALL)        \
         return;                                     \
     }
     PJ_M(1) PJ_M(2) PJ_M(3) PJ_M(4) PJ_M(5) PJ_M(6)
@@ -157,30 +156,36 @@ void launch_project(const aim_plan* p, const double2* x, double2* Q, int R, cuda
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
+void launch_project(const aim_plan* p, const void* x, void* Q, int R, cudaStream_t s) {
+    if (p->prec == AIM_C64) launch_project_t(p, (const float2*)x, (float2*)Q, R, s);
+    else launch_project_t(p, (const double2*)x, (double2*)Q, R, s);
+    note_launch("project");
+}
+
 // ------------------------------------------------------ H5 interpolation
 // y[m,r] (+)= j k eta0 [sum_xyz sum_u w_{m,u} Phi[u,r] - k^-2 sum_u w^phi_{m,u} Phi^phi[u,r]]
 // Warp per RWG row: lane u loads w_{m,u} (contiguous) and its node index, then
 // the rhs lanes gather the stencil's potentials (weights broadcast by shuffles).
-template <int M, int LPE, int RPL>
-__global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__ Phi, const double* __restrict__ W,
+template <int M, int LPE, int RPL, class C>
+__global__ void __launch_bounds__(256) interp_kernel(const C* __restrict__ Phi, const Real<C>* __restrict__ W,
                                                      const int32_t* __restrict__ node0, long long Ng, int Ny, int Nz,
                                                      long long N, int R, double keta, double ik2, int accumulate,
-                                                     double2* __restrict__ y) {
+                                                     C* __restrict__ y) {
     constexpr int M1 = M + 1, S = M1 * M1 * M1;
     using L = Lanes<LPE, RPL>;
     const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (m >= N) return;
     const L ln;
     const long long g0 = node0[m];
-    const double2* W2 = reinterpret_cast<const double2*>(W) + 2 * m * S;
+    const C* W2 = reinterpret_cast<const C*>(W) + 2 * m * S;
     for (int r0 = 0; r0 < R; r0 += L::RC) {
-        double2 aA[RPL], aP[RPL];
+        C aA[RPL], aP[RPL];
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) aA[q] = aP[q] = make_double2(0, 0);
+        for (int q = 0; q < RPL; ++q) aA[q] = aP[q] = mkc<C>(0, 0);
         for (int ub = 0; ub < S; ub += 32) {
             const int u_l = ub + ln.lane;
             const int cnt = min(32, S - ub);
-            double2 w01 = make_double2(0, 0), w23 = w01;
+            C w01 = mkc<C>(0, 0), w23 = w01;
             int g_l = 0;
             if (ln.lane < cnt) {
                 w01 = __ldcs(W2 + 2 * u_l);
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
 #pragma unroll kGatherUnroll
             for (int t = ln.grp; t < 32; t += L::G) {
                 int g;
-                double w[4];
+                Real<C> w[4];
                 if (LPE == 1) {
                     g = g_l; w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
                 } else {
@@ -204,10 +209,10 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
                     for (int q = 0; q < RPL; ++q) {
                         const int rr = r0 + ln.sub + q * LPE;
                         if (rr < R) {
-                            const double2 f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
-                            const double2 f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
-                            const double2 f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
-                            const double2 f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
+                            const C f0 = __ldg(&Phi[(0 * Ng + g) * R + rr]);
+                            const C f1 = __ldg(&Phi[(1 * Ng + g) * R + rr]);
+                            const C f2 = __ldg(&Phi[(2 * Ng + g) * R + rr]);
+                            const C f3 = __ldg(&Phi[(3 * Ng + g) * R + rr]);
                             aA[q].x = fma(w[0], f0.x, aA[q].x); aA[q].y = fma(w[0], f0.y, aA[q].y);
                             aA[q].x = fma(w[1], f1.x, aA[q].x); aA[q].y = fma(w[1], f1.y, aA[q].y);
                             aA[q].x = fma(w[2], f2.x, aA[q].x); aA[q].y = fma(w[2], f2.y, aA[q].y);
@@ -220,17 +225,17 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
             // far = j k eta0 (aA - aP / k^2)
-            const double2 f = make_double2(aA[q].x - aP[q].x * ik2, aA[q].y - aP[q].y * ik2);
-            double2 tot = make_double2(-keta * f.y, keta * f.x);
+            const C f = mkc<C>(aA[q].x - aP[q].x * (Real<C>)ik2, aA[q].y - aP[q].y * (Real<C>)ik2);
+            C tot = mkc<C>(-(Real<C>)keta * f.y, (Real<C>)keta * f.x);
 #pragma unroll
             for (int off = LPE; off < 32; off <<= 1) {
-                const double2 t = shfl_xor2(tot, off);
+                const C t = shfl_xor2(tot, off);
                 tot.x += t.x; tot.y += t.y;
             }
             const int rr = r0 + ln.sub + q * LPE;
             if (ln.grp == 0 && rr < R) {
                 if (accumulate) {
-                    const double2 o = y[m * R + rr];
+                    const C o = y[m * R + rr];
                     tot.x += o.x; tot.y += o.y;
                 }
                 y[m * R + rr] = tot;
@@ -242,22 +247,22 @@ __global__ void __launch_bounds__(256) interp_kernel(const double2* __restrict__
 // ------------------------------------------------------- H6 near SpMV
 // y[m,r] = sum_{n in near(m)} Z_corr[m,n] x[n,r]; warp per row, entries
 // staged 32 at a time (values streamed past L1), fixed-order reduction.
-template <int LPE, int RPL>
+template <int LPE, int RPL, class C>
 __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ rowp, const int32_t* __restrict__ col,
-                                                   const double2* __restrict__ val, const double2* __restrict__ x,
-                                                   long long N, int R, double2* __restrict__ y) {
+                                                   const C* __restrict__ val, const C* __restrict__ x,
+                                                   long long N, int R, C* __restrict__ y) {
     using L = Lanes<LPE, RPL>;
     const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (m >= N) return;
     const L ln;
     const long long e0 = rowp[m], e1 = rowp[m + 1];
     for (int r0 = 0; r0 < R; r0 += L::RC) {
-        double2 acc[RPL];
+        C acc[RPL];
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) acc[q] = make_double2(0, 0);
+        for (int q = 0; q < RPL; ++q) acc[q] = mkc<C>(0, 0);
         for (long long b = e0; b < e1; b += 32) {
             const int cnt = (int)min(32LL, e1 - b);
-            double2 z_l = make_double2(0, 0);
+            C z_l = mkc<C>(0, 0);
             int n_l = 0;
             if (ln.lane < cnt) {
                 z_l = __ldcs(&val[b + ln.lane]);
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
 #pragma unroll 4
             for (int t = ln.grp; t < 32; t += L::G) {
                 int n;
-                double zx, zy;
+                Real<C> zx, zy;
                 if (LPE == 1) {
                     n = n_l; zx = z_l.x; zy = z_l.y;
                 } else {
@@ -275,11 +280,11 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
                     zy = __shfl_sync(0xffffffffu, z_l.y, t);
                 }
                 if (t < cnt) {
-                    const double2* xr = x + (long long)n * R + r0 + ln.sub;
+                    const C* xr = x + (long long)n * R + r0 + ln.sub;
 #pragma unroll
                     for (int q = 0; q < RPL; ++q) {
                         if (r0 + ln.sub + q * LPE < R) {
-                            const double2 xv = __ldg(xr + q * LPE);
+                            const C xv = __ldg(xr + q * LPE);
                             acc[q].x = fma(zx, xv.x, acc[q].x); acc[q].x = fma(-zy, xv.y, acc[q].x);
                             acc[q].y = fma(zx, xv.y, acc[q].y); acc[q].y = fma(zy, xv.x, acc[q].y);
                         }
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
         for (int q = 0; q < RPL; ++q) {
 #pragma unroll
             for (int off = LPE; off < 32; off <<= 1) {
-                const double2 t = shfl_xor2(acc[q], off);
+                const C t = shfl_xor2(acc[q], off);
                 acc[q].x += t.x; acc[q].y += t.y;
             }
             const int rr = r0 + ln.sub + q * LPE;
@@ -309,37 +314,37 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
 #ifndef AIM_NB4_MINB
 #define AIM_NB4_MINB 2
 #endif
-template <int LPE, int RPL>
+template <int LPE, int RPL, class C>
 __global__ void __launch_bounds__(256, AIM_NB4_MINB) near_b4_kernel(const int32_t* __restrict__ rows,
                                                       const int64_t* __restrict__ bptr,
                                                       const int32_t* __restrict__ bcol,
-                                                      const double2* __restrict__ bval,
-                                                      const double2* __restrict__ x, long long nblk, int R,
-                                                      double2* __restrict__ y) {
+                                                      const C* __restrict__ bval,
+                                                      const C* __restrict__ x, long long nblk, int R,
+                                                      C* __restrict__ y) {
     using L = Lanes<LPE, RPL>;
     const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (b >= nblk) return;
     const L ln;
     const long long e0 = bptr[b], e1 = bptr[b + 1];
     for (int r0 = 0; r0 < R; r0 += L::RC) {
-        double2 acc[4][RPL];
+        C acc[4][RPL];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < RPL; ++q) acc[i][q] = make_double2(0, 0);
+            for (int q = 0; q < RPL; ++q) acc[i][q] = mkc<C>(0, 0);
         // columns staged 32 at a time: lane e loads column e's index and its
         // 4 values (one coalesced 2 KB read per warp), prefetched one batch
         // ahead; values reach the lane groups by shuffles
         int c_n = 0;
-        double2 v_n[4];
+        C v_n[4];
         auto fetch = [&](long long e) {
             const int cnt = (int)min(32LL, e1 - e);
             c_n = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) v_n[i] = make_double2(0, 0);
+            for (int i = 0; i < 4; ++i) v_n[i] = mkc<C>(0, 0);
             if (ln.lane < cnt) {
                 c_n = __ldcs(&bcol[e + ln.lane]);
-                const double2* vp = bval + 4 * (e + ln.lane);
+                const C* vp = bval + 4 * (e + ln.lane);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) v_n[i] = __ldcs(vp + i);
             }
@@ -348,23 +353,22 @@ __global__ void __launch_bounds__(256, AIM_NB4_MINB) near_b4_kernel(const int32_
         for (long long e = e0; e < e1; e += 32) {
             const int cnt = (int)min(32LL, e1 - e);
             const int c_l = c_n;
-            double2 v_l[4];
+            C v_l[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) v_l[i] = v_n[i];
             if (e + 32 < e1) fetch(e + 32);
 #pragma unroll 2
             for (int t = ln.grp; t < 32; t += L::G) {
                 const int c = __shfl_sync(0xffffffffu, c_l, t);
-                double2 v[4];
+                C v[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) v[i] = make_double2(__shfl_sync(0xffffffffu, v_l[i].x, t),
-                                                                __shfl_sync(0xffffffffu, v_l[i].y, t));
+                for (int i = 0; i < 4; ++i) v[i] = shfl_c(v_l[i], t);
                 if (t < cnt) {
-                    const double2* xr = x + (long long)c * R + r0 + ln.sub;
+                    const C* xr = x + (long long)c * R + r0 + ln.sub;
 #pragma unroll
                     for (int q = 0; q < RPL; ++q) {
                         if (r0 + ln.sub + q * LPE < R) {
-                            const double2 xv = __ldg(xr + q * LPE);
+                            const C xv = __ldg(xr + q * LPE);
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
                                 acc[i][q].x = fma(v[i].x, xv.x, acc[i][q].x);
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(256, AIM_NB4_MINB) near_b4_kernel(const int32_
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int q = 0; q < RPL; ++q) {
-                    const double2 t = shfl_xor2(acc[i][q], off);
+                    const C t = shfl_xor2(acc[i][q], off);
                     acc[i][q].x += t.x;
                     acc[i][q].y += t.y;
                 }
@@ -401,18 +405,19 @@ __global__ void __launch_bounds__(256, AIM_NB4_MINB) near_b4_kernel(const int32_
     }
 }
 
-void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, bool accumulate, cudaStream_t s) {
+template <class C>
+static void launch_interp_t(const aim_plan* p, const C* Phi, C* y, int R, bool accumulate, cudaStream_t s) {
     const unsigned grid = nblk(p->N * 32, 256);
     const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
-#define IN_CALL(LPE, RPL)                                                                                     \
-    interp_kernel<MM, LPE, RPL><<<grid, 256, 0, s>>>(Phi, p->W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, R, \
-                                                     keta, ik2, accumulate ? 1 : 0, y)
-#define IN_M(MMV)                     \
-    if (p->M == MMV) {                \
-        constexpr int MM = MMV;       \
+    const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->W : (const void*)p->W32);
+#define IN_CALL(LPE, RPL)                                                                                       \
+    interp_kernel<MM, LPE, RPL, C><<<grid, 256, 0, s>>>(Phi, W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, R, \
+                                                        keta, ik2, accumulate ? 1 : 0, y)
+#define IN_M(MMV)                            \
+    if (p->M == MMV) {                       \
+        constexpr int MM = MMV;              \
         AIM_LANE_DISPATCH_GATHER(R, IN_CALL) \
-        note_launch("interp");        \
-        return;                       \
+        return;                              \
     }
     IN_M(1) IN_M(2) IN_M(3) IN_M(4) IN_M(5) IN_M(6)
 #undef IN_M
@@ -420,27 +425,41 @@ void launch_interp(const aim_plan* p, const double2* Phi, double2* y, int R, boo
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
+void launch_interp(const aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s) {
+    if (p->prec == AIM_C64) launch_interp_t(p, (const float2*)Phi, (float2*)y, R, accumulate, s);
+    else launch_interp_t(p, (const double2*)Phi, (double2*)y, R, accumulate, s);
+    note_launch("interp");
+}
+
 // Multi-RHS products use the 4-row blocked layout (x reuse across rows);
 // below kNearBlockRhs right-hand sides the plain CSR (fewer value bytes).
 constexpr int kNearBlockRhs = 4;
 
-void launch_near(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
+template <class C>
+static void launch_near_t(aim_plan* p, const C* x, C* y, int R, cudaStream_t s) {
+    const bool c64 = sizeof(C) == 8;
     if (R >= kNearBlockRhs) {
         build_near_blocks(p, s);
         const unsigned grid = nblk(p->nb_count * 32, 256);
+        const C* bval = (const C*)(c64 ? (const void*)p->nb_val32 : (const void*)p->nb_val);
 #define NB_CALL(LPE, RPL) \
-    near_b4_kernel<LPE, RPL><<<grid, 256, 0, s>>>(p->nb_rows, p->nb_ptr, p->nb_col, p->nb_val, x, p->nb_count, R, y)
+    near_b4_kernel<LPE, RPL, C><<<grid, 256, 0, s>>>(p->nb_rows, p->nb_ptr, p->nb_col, bval, x, p->nb_count, R, y)
         if (R <= 4) { NB_CALL(2, 2); }
         else if (R <= 8) { NB_CALL(4, 2); }
         else { NB_CALL(8, 2); }
 #undef NB_CALL
-        note_launch("near_b4");
         return;
     }
     const unsigned grid = nblk(p->N * 32, 256);
-#define NK_CALL(LPE, RPL) near_kernel<LPE, RPL><<<grid, 256, 0, s>>>(p->nrow, p->ncol, p->nval, x, p->N, R, y)
+    const C* val = (const C*)(c64 ? (const void*)p->nval32 : (const void*)p->nval);
+#define NK_CALL(LPE, RPL) near_kernel<LPE, RPL, C><<<grid, 256, 0, s>>>(p->nrow, p->ncol, val, x, p->N, R, y)
     AIM_LANE_DISPATCH_NEAR(R, NK_CALL)
 #undef NK_CALL
+}
+
+void launch_near(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
+    if (p->prec == AIM_C64) launch_near_t(p, (const float2*)x, (float2*)y, R, s);
+    else launch_near_t(p, (const double2*)x, (double2*)y, R, s);
     note_launch("near");
 }
 
@@ -487,9 +506,11 @@ void ensure_workspace(aim_plan* p, int R) {
     p->W2 = nullptr;
     const long long Nx = p->dims[0], Ny = p->dims[1], Nz = p->dims[2];
     const long long Px = p->pads[0], Py = p->pads[1];
-    p->Q = p->alloc<double2>(4 * Nx * Ny * Nz * R);
-    p->W1 = p->alloc<double2>(4 * Px * Ny * Nz * R);
-    if (!p->planar) p->W2 = p->alloc<double2>(4 * Px * Py * Nz * R);
+    // complex64 plans use the same buffers at half the size (float2 elements)
+    const long long es = p->prec == AIM_C64 ? 1 : 2;   // element size in 8-byte units
+    p->Q = (double2*)p->alloc<float2>(es * 4 * Nx * Ny * Nz * R);
+    p->W1 = (double2*)p->alloc<float2>(es * 4 * Px * Ny * Nz * R);
+    if (!p->planar) p->W2 = (double2*)p->alloc<float2>(es * 4 * Px * Py * Nz * R);
     p->ws_nrhs = R;
 }
 
@@ -512,10 +533,12 @@ struct Prof {
     }
 };
 
-static void convolve_impl(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s, Prof* pr) {
+static void convolve_impl(aim_plan* p, const void* Q, void* Phi, int R, cudaStream_t s, Prof* pr) {
     const long long Nx = p->dims[0], Ny = p->dims[1], Nz = p->dims[2];
     const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2];
     FftPass f{};
+    f.prec = p->prec;
+    const void* spec = p->prec == AIM_C64 ? (const void*)p->spec32 : (const void*)p->spec;
     // x forward, [4][Nx -> Px][Ny Nz R]
     f.in = Q; f.out = p->W1; f.outer = 4; f.Lin = (int)Nx; f.Lout = Px; f.inner = Ny * Nz * R;
     f.mode = 0; f.ax = p->ax[0]; f.TO = f.TI = 0;
@@ -523,8 +546,9 @@ static void convolve_impl(aim_plan* p, const double2* Q, double2* Phi, int R, cu
     if (pr) pr->mark(2, s);
     if (p->planar) {
         PlanarPass q{};
+        q.prec = p->prec;
         q.W = p->W1; q.Px = Px; q.Ny = (int)Ny; q.Nz = (int)Nz; q.R = R; q.PyH = Py / 2 + 1; q.ay = p->ax[1];
-        q.spec = p->spec;
+        q.spec = spec;
         launch_planar_yz(q, s);
     } else {
         // y forward, [4 Px][Ny -> Py][Nz R]
@@ -534,7 +558,7 @@ static void convolve_impl(aim_plan* p, const double2* Q, double2* Phi, int R, cu
         // z turnaround in place, [4 Px Py][Nz -> Pz -> Nz][R]
         f.in = p->W2; f.out = p->W2; f.outer = 4LL * Px * Py; f.Lin = (int)Nz; f.Lout = (int)Nz; f.inner = R;
         f.mode = 2; f.ax = p->ax[2]; f.TO = f.TI = 0;
-        f.spec = p->spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
+        f.spec = spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
         launch_fft_pass(f, s);
         // y inverse, [4 Px][Py -> Ny][Nz R]
         f.in = p->W2; f.out = p->W1; f.outer = 4LL * Px; f.Lin = Py; f.Lout = (int)Ny; f.inner = Nz * R;
@@ -549,7 +573,7 @@ static void convolve_impl(aim_plan* p, const double2* Q, double2* Phi, int R, cu
     if (pr) pr->mark(4, s);
 }
 
-void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s) {
+void convolve(aim_plan* p, const void* Q, void* Phi, int R, cudaStream_t s) {
     convolve_impl(p, Q, Phi, R, s, nullptr);
 }
 
@@ -558,7 +582,7 @@ void convolve(aim_plan* p, const double2* Q, double2* Phi, int R, cudaStream_t s
 // interpolation, which accumulates the far field into y.  (Running the SpMV
 // on a side stream bought nothing: its 14k CTAs occupy every SM and the
 // persistent FFT CTAs queue behind them.)
-void matvec(aim_plan* p, const double2* x, double2* y, int R, cudaStream_t s) {
+void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
     ensure_workspace(p, R);
     Prof pr(p);
     pr.mark(0, s);

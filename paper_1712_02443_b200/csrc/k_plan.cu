@@ -388,6 +388,7 @@ void build_near_blocks(aim_plan* p, cudaStream_t s) {
     AIM_CUDA(cudaStreamSynchronize(s));
     cudaFree(d_cnt);
     p->nb_count = nblk;
+    if (p->prec == AIM_C64) make_c64_blocks(p, s);
 }
 
 // ------------------------------------------------------- S4 exact entries

@@ -161,6 +161,43 @@ def test_matvec_full_size_sampled_rows(name):
     assert rel(y[rows], ref) <= 1e-10
 
 
+@pytest.mark.parametrize("name,nrhs", [("c1", 1), ("c1", 16), ("t_vol", 1), ("t_m3", 2), ("t_dissim", 5)])
+def test_matvec_c64(name, nrhs):
+    """AIM_C64 plans (reading D16: fp64 plan rounded to fp32, fp32 FFT and
+    accumulation) against the complex128 oracle: <= 1e-4 relative L2."""
+    from paper_1712_02443_b200 import AimPlan
+    from paper_1712_02443_b200.api import C64
+    cfg = get_config(name)
+    O = oracle_plan(name)
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius, precision=C64)
+    assert G.info["precision"] == C64
+    x = make_vectors(O.N, nrhs, 0)
+    y = G.matvec(torch.from_numpy(x.astype(np.complex64)).cuda()).cpu().numpy()
+    assert y.dtype == np.complex64
+    assert rel(y, O.matvec(x)) <= 1e-4
+    yh = G.matvec_host(x.astype(np.complex64))
+    assert np.array_equal(yh, y)
+    G.close()
+
+
+def test_matvec_c5_c64_full_size_sampled_rows():
+    """configs[4] in complex64 at full size (N = 1,119,744): sampled rows
+    against the complex128 oracle, <= 1e-4 (BASELINE.json configs[4])."""
+    from paper_1712_02443_b200 import AimPlan
+    from paper_1712_02443_b200.api import C64
+    from oracle.aim import OraclePlan
+    cfg = get_config("c5")
+    mesh = make_mesh(cfg)
+    x = make_vectors(mesh.n_rwg, 1, 0)
+    G = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, precision=C64)
+    y = G.matvec(torch.from_numpy(x.astype(np.complex64)).cuda()).cpu().numpy()
+    G.close()
+    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    rows = np.unique(np.concatenate([[0, O.N - 1], np.random.default_rng(2).integers(0, O.N, 32)]))
+    ref = O.matvec_rows(x, rows, method="fft")
+    assert rel(y[rows], ref) <= 1e-4
+
+
 def test_planewave_rhs():
     from oracle.excitation import plane_wave_rhs
     G, O = gpu_plan("c1"), oracle_plan("c1")
