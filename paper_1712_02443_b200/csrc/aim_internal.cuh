@@ -135,6 +135,18 @@ struct aim_plan {
     int64_t* nb_ptr = nullptr;    // [nb_count+1]
     int32_t* nb_col = nullptr;    // [nbc]
     double2* nb_val = nullptr;    // [nbc][4]
+    // near field in 8- or 16-row blocks for the FP64 tensor-core SpMM (complex128,
+    // R >= 8; built on first use): chunks of 4 union columns, a 32-bit
+    // row x column presence mask per chunk, values packed (exactly nnzN)
+    int64_t nm_count = 0;         // number of blocks (0 = not built)
+    int64_t nm_chunks = 0;
+    int nm_mt = 1;                // m-tiles per block (8 * nm_mt rows)
+    int32_t* nm_rows = nullptr;   // [nm_count][8 nm_mt] row ids, -1 = padding
+    int64_t* nm_cptr = nullptr;   // [nm_count+1] chunk ranges
+    int64_t* nm_vptr = nullptr;   // [nm_count+1] packed value ranges
+    uint32_t* nm_mask = nullptr;  // [nm_chunks][nm_mt]
+    int32_t* nm_col = nullptr;    // [nm_chunks][4]
+    double2* nm_val = nullptr;    // [nnzN]
     int planar = 0;               // 1: z handled by direct convolution (spec = G2)
     double2* spec = nullptr;      // 3-D: [(Px/2+1)(Py/2+1)(Pz/2+1)]; planar: [(Px/2+1)(Py/2+1)][Nz]
     int64_t spec_len = 0;
@@ -203,6 +215,7 @@ void build_near_list(aim_plan* p, cudaStream_t s);
 void build_near_values(aim_plan* p, cudaStream_t s);
 void build_green_spectrum(aim_plan* p, cudaStream_t s);
 void build_near_blocks(aim_plan* p, cudaStream_t s);
+void build_near_mma(aim_plan* p, cudaStream_t s);
 void make_c64_blocks(aim_plan* p, cudaStream_t s);   // rounded nb_val for AIM_C64 plans
 
 // ---- matvec launches (k_matvec.cu)

@@ -11,6 +11,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "aim_internal.cuh"
 #include "cplx.cuh"
@@ -405,6 +407,162 @@ __global__ void __launch_bounds__(256, AIM_NB4_MINB) near_b4_kernel(const int32_
     }
 }
 
+// ------------------------------ H6 near SpMM on the FP64 tensor cores
+// Warp per block of 8*MT rows (build_near_mma): each chunk of 4 union columns
+// is one k-step of mma.m8n8k4.f64 per m-tile, with A = the m-tile's 8x4
+// values (lane l holds row l/4, column l%4: bit l of the chunk's mask word,
+// packed value popc(mask below l)) and B = x[4 columns][8 RHS] (lane l:
+// column l%4, RHS l/4).  C fragment: lane l holds row l/4, RHS 2(l%4) + {0,1}.
+// Complex product with three real MMAs per 8-RHS tile (Gauss):
+//   T1 = Zr Xr,  T2 = Zi Xi,  T3 = (Zr + Zi)(Xr + Xi);  re = T1 - T2, im = T3 - T1 - T2.
+// The masks and columns of a window of 8 chunks are one coalesced load per
+// lane (prefetched two windows ahead, handed out by shuffles).
+// Fixed order => deterministic.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+// The operands are staged through shared memory by cp.async: every lane owns
+// a private ring of D chunk slots (its MT A values and its NT x values per
+// chunk), so D chunks per warp are in flight while the MMAs of the oldest
+// run, and no register arrays are held across the wait.  Absent values and
+// padding columns are zero-filled by plain shared stores.  Chunk j lives in
+// slot j % D; after consuming chunk c the lane issues chunk c + D into the
+// freed slot, so exactly D - 1 newer copy groups are pending at every wait.
+// Blocks of 16 rows (MT = 2) share each x fragment between two m-tiles.
+// values stream past L1 (.cg); x rows are re-read by neighbouring blocks of
+// the same CTA, so they are cached in L1 (.ca)
+__device__ __forceinline__ void cpa16_cg(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa16_ca(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+#ifndef AIM_NM_DEPTH
+#define AIM_NM_DEPTH 4
+#endif
+constexpr int kNmWarps = 4;               // warps per CTA of near_mma_kernel
+constexpr int kNmDepth = AIM_NM_DEPTH;    // ring depth (chunks in flight per warp), <= 8
+template <int MT, int NT>
+constexpr size_t near_mma_smem() { return sizeof(double2) * kNmWarps * kNmDepth * (MT + NT) * 32; }
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(32 * kNmWarps) near_mma_kernel(const int32_t* __restrict__ rows,
+                                                              const int64_t* __restrict__ cptr,
+                                                              const int64_t* __restrict__ vptr,
+                                                              const uint32_t* __restrict__ cmask,
+                                                              const int32_t* __restrict__ ccol,
+                                                              const double2* __restrict__ val,
+                                                              const double2* __restrict__ x, long long nblk, int R,
+                                                              double2* __restrict__ y) {
+    // ring depth D; metadata windows of W = 8 chunks (one column per lane)
+    constexpr int D = kNmDepth, W = 8, SL = (MT + NT) * 32;   // SL: slot stride (double2)
+    static_assert(D >= 1 && D <= W, "ring depth");
+    extern __shared__ __align__(16) double2 nm_sm[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const long long b = (long long)blockIdx.x * kNmWarps + wid;
+    if (b >= nblk) return;
+    // this lane's slot u: A of m-tile q at ring[u*SL + q*32], x tile n at ring[u*SL + (MT+n)*32]
+    double2* ring = nm_sm + (size_t)wid * D * SL + lane;
+    const uint32_t below = (1u << lane) - 1u;
+    // 32-bit offsets: nnzN < 2^31 (plan check) and N R < 2^31 (launch check)
+    const int c0 = (int)cptr[b], c1 = (int)cptr[b + 1];
+    auto meta = [&](int w, int& colw, uint32_t& mw) {
+        colw = (4 * w + lane < 4 * c1) ? __ldcs(&ccol[4 * w + lane]) : -1;
+        mw = (lane < W * MT && MT * w + lane < MT * c1) ? __ldcs(&cmask[MT * w + lane]) : 0u;
+    };
+    for (int r0 = 0; r0 < R; r0 += 8 * NT) {
+        const double2* xr0 = x + r0 + g;
+        int vo = (int)vptr[b];
+        // issue the chunk at position j of the window described by (colw, mw) into slot s
+        auto issue = [&](int colw, uint32_t mw, int j, int slot) {
+            const int col = __shfl_sync(0xffffffffu, colw, 4 * j + t);
+            double2* sl = ring + slot * SL;
+#pragma unroll
+            for (int q = 0; q < MT; ++q) {
+                const uint32_t m = __shfl_sync(0xffffffffu, mw, MT * j + q);
+                if (m >> lane & 1u) cpa16_cg(sl + q * 32, val + vo + __popc(m & below));
+                else sl[q * 32] = make_double2(0.0, 0.0);
+                vo += __popc(m);
+            }
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                if (col >= 0 && r0 + 8 * n + g < R) cpa16_ca(sl + (MT + n) * 32, xr0 + (col * R + 8 * n));
+                else sl[(MT + n) * 32] = make_double2(0.0, 0.0);
+            }
+            cpa_commit();
+        };
+        double T1[MT][NT][2], T2[MT][NT][2], T3[MT][NT][2];
+#pragma unroll
+        for (int q = 0; q < MT; ++q)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) T1[q][n][i] = T2[q][n][i] = T3[q][n][i] = 0.0;
+        int colw, colw_n;
+        uint32_t mw, mw_n;
+        meta(c0, colw, mw);
+        meta(c0 + W, colw_n, mw_n);
+#pragma unroll
+        for (int u = 0; u < D; ++u) issue(colw, mw, u, u);
+        for (int w = c0; w < c1; w += W) {
+            int colw_nn;
+            uint32_t mw_nn;
+            meta(w + 2 * W, colw_nn, mw_nn);
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                // chunk w + u sits in slot u % D; chunk w + u + D replaces it
+                cpa_wait<D - 1>();
+                const double2* sl = ring + (u % D) * SL;
+                double2 a[MT], xv[NT];
+#pragma unroll
+                for (int q = 0; q < MT; ++q) a[q] = sl[q * 32];
+#pragma unroll
+                for (int n = 0; n < NT; ++n) xv[n] = sl[(MT + n) * 32];
+                if (u + D < W) issue(colw, mw, u + D, u % D);   // zero-filled past c1
+                else issue(colw_n, mw_n, u + D - W, u % D);
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const double xs = xv[n].x + xv[n].y;
+#pragma unroll
+                    for (int q = 0; q < MT; ++q) {
+                        dmma(T1[q][n][0], T1[q][n][1], a[q].x, xv[n].x);
+                        dmma(T2[q][n][0], T2[q][n][1], a[q].y, xv[n].y);
+                        dmma(T3[q][n][0], T3[q][n][1], a[q].x + a[q].y, xs);
+                    }
+                }
+            }
+            colw = colw_n;
+            mw = mw_n;
+            colw_n = colw_nn;
+            mw_n = mw_nn;
+        }
+        cpa_wait<0>();
+#pragma unroll
+        for (int q = 0; q < MT; ++q) {
+            const int row = rows[8 * MT * b + 8 * q + g];
+            if (row < 0) continue;
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int rr = r0 + 8 * n + 2 * t + i;
+                    if (rr < R)
+                        y[(long long)row * R + rr] = make_double2(T1[q][n][i] - T2[q][n][i],
+                                                                  T3[q][n][i] - T1[q][n][i] - T2[q][n][i]);
+                }
+        }
+    }
+}
+
 template <class C>
 static void launch_interp_t(const aim_plan* p, const C* Phi, C* y, int R, bool accumulate, cudaStream_t s) {
     const unsigned grid = nblk(p->N * 32, 256);
@@ -435,10 +593,47 @@ void launch_interp(const aim_plan* p, const void* Phi, void* y, int R, bool accu
 // below kNearBlockRhs right-hand sides the plain CSR (fewer value bytes).
 constexpr int kNearBlockRhs = 4;
 
+// complex128 products with >= kNearMmaRhs right-hand sides use the FP64
+// tensor-core kernel (8-row blocks, packed values).  AIM_NEAR_KERNEL=b4|csr
+// in the environment forces another kernel (A/B timing only).
+constexpr int kNearMmaRhs = 8;
+static int near_override() {
+    const char* e = getenv("AIM_NEAR_KERNEL");
+    return !e ? 0 : !strcmp(e, "b4") ? 1 : !strcmp(e, "csr") ? 2 : 0;
+}
+
 template <class C>
 static void launch_near_t(aim_plan* p, const C* x, C* y, int R, cudaStream_t s) {
     const bool c64 = sizeof(C) == 8;
-    if (R >= kNearBlockRhs) {
+    const int ov = near_override();
+    if constexpr (sizeof(C) == 16) {
+        if (R >= kNearMmaRhs && ov == 0) {
+            build_near_mma(p, s);
+            if (p->N * (long long)R >= (1LL << 31)) throw Error(AIM_E_ARG, "near_mma: N * nrhs exceeds 2^31");
+#define NM_CALL(MT, NT)                                                                                        \
+    {                                                                                                          \
+        static bool attr = false;                                                                              \
+        if (!attr) {                                                                                           \
+            AIM_CUDA(cudaFuncSetAttribute(near_mma_kernel<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                          (int)near_mma_smem<MT, NT>()));                                      \
+            attr = true;                                                                                       \
+        }                                                                                                      \
+        near_mma_kernel<MT, NT><<<nblk(p->nm_count, kNmWarps), 32 * kNmWarps, near_mma_smem<MT, NT>(), s>>>(   \
+            p->nm_rows, p->nm_cptr, p->nm_vptr, p->nm_mask, p->nm_col, p->nm_val, (const double2*)x,           \
+            p->nm_count, R, (double2*)y);                                                                      \
+    }
+            if (p->nm_mt == 1) {
+                if (R <= 8) NM_CALL(1, 1)
+                else NM_CALL(1, 2)
+            } else {
+                if (R <= 8) NM_CALL(2, 1)
+                else NM_CALL(2, 2)
+            }
+#undef NM_CALL
+            return;
+        }
+    }
+    if (R >= kNearBlockRhs && ov != 2) {
         build_near_blocks(p, s);
         const unsigned grid = nblk(p->nb_count * 32, 256);
         const C* bval = (const C*)(c64 ? (const void*)p->nb_val32 : (const void*)p->nb_val);

@@ -9,6 +9,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <numeric>
 #include <vector>
@@ -343,13 +344,13 @@ static uint64_t spread3(uint64_t v) {   // 21 bits -> every third bit
     return r;
 }
 
-void build_near_blocks(aim_plan* p, cudaStream_t s) {
-    if (p->nb_count) return;
+// RWG ids in Morton order of their centres on a lattice of spacing h, padded
+// with -1 to a multiple of B: consecutive rows are spatially close, so the
+// near sets of a block of B rows overlap (fill ~0.75 at 4 rows).
+static std::vector<int32_t> morton_rows(const aim_plan* p, int B) {
     const long long N = p->N;
     std::vector<double> cen(3 * N);
     AIM_CUDA(cudaMemcpy(cen.data(), p->rwg_c, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost));
-    // Morton order of the centres on a lattice of spacing h: consecutive rows
-    // are spatially close, so their near sets overlap (fill ~0.75 at 4 rows)
     double lo[3] = {1e300, 1e300, 1e300};
     for (long long n = 0; n < N; ++n)
         for (int a = 0; a < 3; ++a) lo[a] = std::min(lo[a], cen[3 * n + a]);
@@ -363,9 +364,134 @@ void build_near_blocks(aim_plan* p, cudaStream_t s) {
         key[n] = {code, (int32_t)n};
     }
     std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    const long long nblk = (N + 3) / 4;
-    std::vector<int32_t> rows(4 * nblk, -1);
+    const long long nblk = (N + B - 1) / B;
+    std::vector<int32_t> rows(B * nblk, -1);
     for (long long n = 0; n < N; ++n) rows[n] = key[n].second;
+    return rows;
+}
+
+// ------------------------- near field, 8*MT-row blocks for FP64 MMA
+// Block = 8*MT Morton-consecutive rows (MT m-tiles of mma.m8n8k4); its
+// columns = the sorted union of the rows' columns, cut into chunks of 4 (the
+// k extent).  Chunk c stores col[4c..4c+3] (-1 = padding) and MT 32-bit masks:
+// bit 4*i + k of word q says row 8q + i has column k.  The values present are
+// packed in (word, bit) order, so exactly the nnzN near values are stored (no
+// fill).  One thread per block.
+template <bool FILL, int MT>
+__global__ void near_mma_build_kernel(const int32_t* __restrict__ rows, long long nblk,
+                                      const int64_t* __restrict__ rowp, const int32_t* __restrict__ col,
+                                      const double2* __restrict__ val, const int64_t* __restrict__ cptr,
+                                      const int64_t* __restrict__ vptr, int64_t* __restrict__ ccnt,
+                                      uint32_t* __restrict__ cmask, int32_t* __restrict__ ccol,
+                                      double2* __restrict__ cval) {
+    constexpr int RB = 8 * MT;
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblk) return;
+    long long pos[RB], end[RB];
+    for (int i = 0; i < RB; ++i) {
+        const int r = rows[RB * b + i];
+        pos[i] = r >= 0 ? rowp[r] : 0;
+        end[i] = r >= 0 ? rowp[r + 1] : 0;
+    }
+    long long ch = FILL ? cptr[b] : 0, vo = FILL ? vptr[b] : 0;
+    long long nun = 0;
+    uint32_t mask[MT];
+    for (int q = 0; q < MT; ++q) mask[q] = 0;
+    int k = 0;
+    long long src[32 * MT];   // value index of (word q, bit 4i+k) (FILL)
+    for (;;) {
+        int c = INT_MAX;
+        for (int i = 0; i < RB; ++i)
+            if (pos[i] < end[i]) c = min(c, col[pos[i]]);
+        if (c != INT_MAX) {
+            for (int i = 0; i < RB; ++i)
+                if (pos[i] < end[i] && col[pos[i]] == c) {
+                    const int q = i / 8, bit = 4 * (i % 8) + k;
+                    mask[q] |= 1u << bit;
+                    src[32 * q + bit] = pos[i];
+                    ++pos[i];
+                }
+            if (FILL) ccol[4 * ch + k] = c;
+            ++k;
+            ++nun;
+        }
+        if (k == 4 || (c == INT_MAX && k > 0)) {
+            if (FILL) {
+                for (int kk = k; kk < 4; ++kk) ccol[4 * ch + kk] = -1;
+                for (int q = 0; q < MT; ++q) {
+                    cmask[MT * ch + q] = mask[q];
+                    for (int bit = 0; bit < 32; ++bit)
+                        if (mask[q] >> bit & 1u) cval[vo++] = val[src[32 * q + bit]];
+                }
+            }
+            ++ch;
+            for (int q = 0; q < MT; ++q) mask[q] = 0;
+            k = 0;
+        }
+        if (c == INT_MAX) break;
+    }
+    if (!FILL) ccnt[b] = (nun + 3) / 4;
+}
+
+void build_near_mma(aim_plan* p, cudaStream_t s) {
+    if (p->nm_count) return;
+    const long long N = p->N;
+    const char* e = getenv("AIM_NEAR_RB");
+    const int MT = (e && atoi(e) == 8) ? 1 : 2;   // 16-row blocks unless overridden (A/B timing)
+    const int RB = 8 * MT;
+    const std::vector<int32_t> rows = morton_rows(p, RB);
+    const long long nblk = (long long)rows.size() / RB;
+    p->nm_rows = p->alloc<int32_t>(RB * nblk);
+    AIM_CUDA(cudaMemcpy(p->nm_rows, rows.data(), sizeof(int32_t) * RB * nblk, cudaMemcpyHostToDevice));
+    int64_t* d_cnt = nullptr;
+    AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int64_t) * nblk));
+    if (MT == 1)
+        near_mma_build_kernel<false, 1><<<nblk_of(nblk), 128, 0, s>>>(p->nm_rows, nblk, p->nrow, p->ncol, p->nval,
+                                                                      nullptr, nullptr, d_cnt, nullptr, nullptr, nullptr);
+    else
+        near_mma_build_kernel<false, 2><<<nblk_of(nblk), 128, 0, s>>>(p->nm_rows, nblk, p->nrow, p->ncol, p->nval,
+                                                                      nullptr, nullptr, d_cnt, nullptr, nullptr, nullptr);
+    note_launch("near_mma_count");
+    std::vector<int64_t> cnt(nblk), cptr(nblk + 1, 0), vptr(nblk + 1, 0), rowp(N + 1);
+    AIM_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * nblk, cudaMemcpyDeviceToHost, s));
+    AIM_CUDA(cudaMemcpyAsync(rowp.data(), p->nrow, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost, s));
+    AIM_CUDA(cudaStreamSynchronize(s));
+    for (long long b = 0; b < nblk; ++b) {
+        cptr[b + 1] = cptr[b] + cnt[b];
+        long long nz = 0;
+        for (int i = 0; i < RB; ++i) {
+            const int r = rows[RB * b + i];
+            if (r >= 0) nz += rowp[r + 1] - rowp[r];
+        }
+        vptr[b + 1] = vptr[b] + nz;
+    }
+    p->nm_chunks = cptr[nblk];
+    p->nm_mt = MT;
+    p->nm_cptr = p->alloc<int64_t>(nblk + 1);
+    p->nm_vptr = p->alloc<int64_t>(nblk + 1);
+    p->nm_mask = p->alloc<uint32_t>(MT * p->nm_chunks);
+    p->nm_col = p->alloc<int32_t>(4 * p->nm_chunks);
+    p->nm_val = p->alloc<double2>(p->nnzN);
+    AIM_CUDA(cudaMemcpyAsync(p->nm_cptr, cptr.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, s));
+    AIM_CUDA(cudaMemcpyAsync(p->nm_vptr, vptr.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, s));
+    if (MT == 1)
+        near_mma_build_kernel<true, 1><<<nblk_of(nblk), 128, 0, s>>>(p->nm_rows, nblk, p->nrow, p->ncol, p->nval,
+                                                                     p->nm_cptr, p->nm_vptr, nullptr, p->nm_mask,
+                                                                     p->nm_col, p->nm_val);
+    else
+        near_mma_build_kernel<true, 2><<<nblk_of(nblk), 128, 0, s>>>(p->nm_rows, nblk, p->nrow, p->ncol, p->nval,
+                                                                     p->nm_cptr, p->nm_vptr, nullptr, p->nm_mask,
+                                                                     p->nm_col, p->nm_val);
+    note_launch("near_mma_fill");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_cnt);
+    p->nm_count = nblk;
+}
+
+void build_near_blocks(aim_plan* p, cudaStream_t s) {
+    if (p->nb_count) return;
+    const std::vector<int32_t> rows = morton_rows(p, 4);
+    const long long nblk = (long long)rows.size() / 4;
     p->nb_rows = p->alloc<int32_t>(4 * nblk);
     AIM_CUDA(cudaMemcpy(p->nb_rows, rows.data(), sizeof(int32_t) * 4 * nblk, cudaMemcpyHostToDevice));
     int64_t* d_cnt = nullptr;

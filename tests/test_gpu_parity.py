@@ -261,3 +261,29 @@ def test_degenerate_cases():
         y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
         assert rel(y, O.matvec(x)) <= 1e-10
         G.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "t_dissim"])
+@pytest.mark.parametrize("rb", [8, 16])
+def test_near_kernels_all_rhs_counts(name, rb, monkeypatch):
+    """H6 near SpMV: the FP64 tensor-core kernel (complex128, R >= 8; blocks
+    of 8 or 16 rows), the 4-row block kernel and the plain CSR kernel each
+    match the oracle's Z_corr x, over RHS counts with ragged 8-RHS tiles."""
+    from paper_1712_02443_b200 import AimPlan
+    cfg = get_config(name)
+    O = oracle_plan(name)
+    monkeypatch.setenv("AIM_NEAR_RB", str(rb))
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    Z = O.near_full()
+    for nrhs in (4, 7, 8, 9, 16, 24, 33):
+        x = make_vectors(O.N, nrhs, 11)
+        xt = torch.from_numpy(x).cuda()
+        ref = Z @ x
+        outs = {}
+        for kern in ("mma", "b4", "csr"):
+            monkeypatch.setenv("AIM_NEAR_KERNEL", kern)
+            outs[kern] = G.interpolate(None, xt, add_near=True).cpu().numpy()
+            assert rel(outs[kern], ref) <= 1e-13, (kern, nrhs)
+        monkeypatch.delenv("AIM_NEAR_KERNEL")
+        assert rel(outs["mma"], outs["csr"]) <= 1e-14
+    G.close()
