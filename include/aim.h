@@ -52,7 +52,7 @@ typedef enum aim_status {
     AIM_E_GRID = -3,       /* grid or index space exceeds 32-bit addressing    */
     AIM_E_NOMEM = -4,      /* device allocation failed                         */
     AIM_E_CUDA = -5,       /* CUDA runtime / launch error                      */
-    AIM_E_NCCL = -6        /* reserved for the slab-decomposed multi-GPU path  */
+    AIM_E_NCCL = -6        /* NCCL failure (slab-decomposed multi-GPU path)     */
 } aim_status;
 
 enum { AIM_C128 = 0, AIM_C64 = 1 };
@@ -99,8 +99,8 @@ typedef struct aim_info {
  *            then reads and writes complex64 vectors and runs the FFT and
  *            all accumulation in fp32.  aim_gmres / aim_planewave_rhs need an
  *            AIM_C128 plan (AIM_E_ARG otherwise).
- * dist       must be NULL (single-GPU plan); multi-GPU runs shard RHS across
- *            independent plans, see DESIGN.md "Multi-GPU"
+ * dist       must be NULL (single-GPU plan); the slab-decomposed multi-GPU
+ *            operator is aim_slab_create below
  * out        receives the plan
  *
  * Errors: AIM_E_ARG (k <= 0, h <= 0, M outside [1,6], near_radius < 0,
@@ -208,6 +208,65 @@ int aim_profile(aim_plan* plan, int32_t enable);
  * stage into ms[AIM_NUM_STAGES] and the number of profiled matvecs into *count;
  * resets the accumulators. */
 int aim_profile_read(aim_plan* plan, double* ms, int64_t* count);
+
+/* ---- slab-decomposed multi-GPU product ---------------- */
+/* BASELINE.json north_star: "the grid is slab-decomposed along x, the 3D FFT
+ * transposes run as NCCL all-to-all over NVLink, basis functions and
+ * precorrection rows are partitioned by owning slab with stencil halos".
+ * The unpadded grid's x planes are cut into `world` contiguous slabs
+ * [X[r], X[r+1]), balanced by the number of RWGs whose stencil base x index
+ * (D3) lies in them, each at least M planes wide; rank r owns those RWGs
+ * (near rows, weights) and the grid planes [X[r], X[r+1] + M).  Planar grids
+ * (aim_info.conv_mode == 1) only. */
+typedef struct aim_slab aim_slab; /* opaque */
+
+/* Host only (no device work): the partition of `world` slabs.
+ * X: host int32 [world+1] plane bounds (0 = first grid plane, X[world] = Nx);
+ * owner: host int32 [N] owning rank of each RWG, or NULL; grid_nx: host int32
+ * (Nx), or NULL.  Errors: AIM_E_ARG (world * M > Nx, bad scalars),
+ * AIM_E_MESH (index out of range). */
+int aim_slab_partition(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt,
+                       const int32_t* rwg_edges, int64_t n_rwg, double h, int32_t M, int32_t world,
+                       int32_t* X, int32_t* owner, int32_t* grid_nx);
+
+/* Fill `id` (host, `bytes` == NCCL_UNIQUE_ID_BYTES = 128) with a fresh NCCL
+ * unique id (rank 0 calls this and broadcasts it).  libnccl.so.2 is loaded at
+ * run time; AIM_E_NCCL if it cannot be. */
+int aim_nccl_unique_id(void* id, int64_t bytes);
+
+/*
+ * aim_slab_create -- build the slab-decomposed operator (complex128).
+ * Mesh and scalars as aim_plan_create.  Every rank passes the full mesh; the
+ * whole operator is built once per rank and each rank keeps its own rows.
+ * rank in [0, world) with nccl_id (host, 128 bytes, the same on every rank):
+ *   one process per GPU, exchanges over NCCL (grouped send/recv; halos to
+ *   the neighbouring ranks, two all-to-all FFT transposes, a broadcast
+ *   gather of y).  Collective: every rank must call it.
+ * rank < 0 (nccl_id ignored): all `world` slabs on the current GPU in this
+ *   process, exchanges as device copies with the same packing (checks the
+ *   decomposition on one device).
+ * Errors: as aim_plan_create; AIM_E_ARG also for a non-planar grid or
+ * world * M > Nx; AIM_E_NCCL.  Synchronous.
+ */
+int aim_slab_create(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt,
+                    const int32_t* rwg_edges, int64_t n_rwg, double k, double h, int32_t M,
+                    double near_radius, int32_t world, int32_t rank, const void* nccl_id,
+                    aim_slab** out);
+
+/* y := Z_eq x, x and y device complex128 [N][nrhs] in the caller's RWG order,
+ * replicated on every rank (x must be identical on every rank; every rank
+ * receives all of y).  Stream-ordered on `stream`; with NCCL every rank must
+ * call it (collective). */
+int aim_slab_matvec(aim_slab* slab, const void* x, void* y, int32_t nrhs, void* stream);
+
+/* Host: out[10] = {X[r], X[r+1], KY[r], KY[r+1] (owned ky range of the
+ * x-pencil phase), n0, n1 (rank r's rows in the permuted order), local near
+ * nnz (-1 if rank r is not held here), all-to-all bytes per RHS and matvec
+ * (max over ranks, out + in), halo bytes per RHS and matvec, world}. */
+int aim_slab_query(const aim_slab* slab, int32_t rank, int64_t* out);
+
+/* Release everything (NCCL communicator included).  NULL is accepted. */
+int aim_slab_destroy(aim_slab* slab);
 
 /* Thread-local message for the last non-OK status ("" if none). */
 const char* aim_last_error(void);

@@ -4,4 +4,4 @@ Thin Python binding over the C ABI in include/aim.h (libaim_b200.so, built
 in-tree for sm_100a).  PyTorch is used for device memory and streams only;
 every step of the operator runs in the library's CUDA kernels.
 """
-from .api import AimPlan, AimError, launch_count, EXPORT  # noqa: F401
+from .api import AimPlan, AimSlabPlan, AimError, launch_count, slab_partition, nccl_unique_id, EXPORT  # noqa: F401

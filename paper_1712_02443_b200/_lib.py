@@ -43,6 +43,12 @@ SIGNATURES = [
     ("aim_plan_export", I32, [P, I32, P, I64]),
     ("aim_profile", I32, [P, I32]),
     ("aim_profile_read", I32, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
+    ("aim_slab_partition", I32, [P, I64, P, I64, P, I64, D, I32, I32, P, P, P]),
+    ("aim_nccl_unique_id", I32, [P, I64]),
+    ("aim_slab_create", I32, [P, I64, P, I64, P, I64, D, D, I32, D, I32, I32, P, ctypes.POINTER(P)]),
+    ("aim_slab_matvec", I32, [P, P, P, I32, P]),
+    ("aim_slab_query", I32, [P, I32, P]),
+    ("aim_slab_destroy", I32, [P]),
     ("aim_last_error", ctypes.c_char_p, []),
     ("aim_launch_count", I64, [I32]),
 ]

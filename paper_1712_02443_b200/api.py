@@ -206,3 +206,91 @@ class AimPlan:
         out = np.empty(sh, dtype=dt)
         _check(_lib.load().aim_plan_export(self._p, EXPORT[what], out.ctypes.data, out.nbytes))
         return out
+
+
+def slab_partition(mesh_or_arrays, h, M, world):
+    """aim_slab_partition (host only): slab plane bounds X[world+1], the owning
+    rank of every RWG and the grid's x extent Nx."""
+    if hasattr(mesh_or_arrays, "vertices"):
+        v, t, r = mesh_or_arrays.vertices, mesh_or_arrays.triangles, mesh_or_arrays.rwg
+    else:
+        v, t, r = mesh_or_arrays
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.int32)
+    r = np.ascontiguousarray(r, dtype=np.int32)
+    X = np.empty(world + 1, dtype=np.int32)
+    owner = np.empty(r.shape[0], dtype=np.int32)
+    nx = ctypes.c_int32()
+    _check(_lib.load().aim_slab_partition(v.ctypes.data, v.shape[0], t.ctypes.data, t.shape[0], r.ctypes.data,
+                                          r.shape[0], float(h), int(M), int(world), X.ctypes.data,
+                                          owner.ctypes.data, ctypes.byref(nx)))
+    return X, owner, int(nx.value)
+
+
+def nccl_unique_id() -> bytes:
+    """aim_nccl_unique_id: 128 bytes for aim_slab_create (rank 0 makes it, all ranks use it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.load().aim_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+class AimSlabPlan:
+    """aim_slab_create(...) wrapper: the slab-decomposed operator.
+    rank=None: all `world` slabs on the current GPU (device-copy exchanges);
+    rank=r with nccl_id: one slab per process/GPU, NCCL exchanges."""
+
+    QUERY = ("X0", "X1", "KY0", "KY1", "n0", "n1", "nnz_near", "a2a_bytes_per_rhs", "halo_bytes_per_rhs", "world")
+
+    def __init__(self, vertices, triangles, rwg, k, h, M, near_radius, world, rank=None, nccl_id=None):
+        lib = _lib.load()
+        self._v = np.ascontiguousarray(vertices, dtype=np.float64)
+        self._t = np.ascontiguousarray(triangles, dtype=np.int32)
+        self._r = np.ascontiguousarray(rwg, dtype=np.int32)
+        out = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(lib.aim_slab_create(self._v.ctypes.data, self._v.shape[0], self._t.ctypes.data, self._t.shape[0],
+                                   self._r.ctypes.data, self._r.shape[0], float(k), float(h), int(M),
+                                   float(near_radius), int(world), -1 if rank is None else int(rank), idbuf,
+                                   ctypes.byref(out)))
+        self._p = out
+        self.N = int(self._r.shape[0])
+        self.world = int(world)
+        self.rank = rank
+
+    @classmethod
+    def from_mesh(cls, mesh, k, h, M, near_radius, world, rank=None, nccl_id=None):
+        return cls(mesh.vertices, mesh.triangles, mesh.rwg, k, h, M, near_radius, world, rank, nccl_id)
+
+    def query(self, rank: int) -> dict:
+        out = np.empty(10, dtype=np.int64)
+        _check(_lib.load().aim_slab_query(self._p, int(rank), out.ctypes.data))
+        return dict(zip(self.QUERY, (int(v) for v in out)))
+
+    def matvec(self, x, y=None):
+        torch = _torch()
+        nrhs = 1 if x.dim() == 1 else x.shape[1]
+        if y is None:
+            y = torch.empty_like(x)
+        _check(_lib.load().aim_slab_matvec(self._p, _dev_ptr(x, self.N, nrhs), _dev_ptr(y, self.N, nrhs), nrhs,
+                                           _stream()))
+        return y
+
+    def close(self):
+        if getattr(self, "_p", None):
+            _lib.load().aim_slab_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_nccl_id(group=None) -> bytes:
+    """Rank 0 of the torch.distributed group makes an NCCL unique id and every
+    rank receives it (host-side plumbing of aim_slab_create with NCCL)."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]

@@ -23,6 +23,8 @@ namespace aim {
 static thread_local std::string g_err;
 static thread_local long long g_launches = 0;
 
+std::string& last_error() { return g_err; }
+
 void note_launch(const char* name) {
     ++g_launches;
     cudaError_t e = cudaGetLastError();
@@ -32,25 +34,6 @@ void note_launch(const char* name) {
     if (sync_debug) {
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) throw Error(AIM_E_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
-    }
-}
-
-static int fail(int status, const std::string& msg) {
-    g_err = msg;
-    return status;
-}
-
-template <class F>
-static int guarded(F&& f) {
-    try {
-        g_err.clear();
-        return f();
-    } catch (const Error& e) {
-        return fail(e.status, e.what());
-    } catch (const std::bad_alloc&) {
-        return fail(AIM_E_NOMEM, "host allocation failed");
-    } catch (const std::exception& e) {
-        return fail(AIM_E_CUDA, e.what());
     }
 }
 
@@ -103,8 +86,8 @@ void make_c64_blocks(aim_plan* p, cudaStream_t s) {
     AIM_CUDA(cudaStreamSynchronize(s));
 }
 
-static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, const int32_t* E, int64_t N, double k,
-                   double h, int M, double r, int prec, aim_plan* p) {
+void create_plan(const double* V, int64_t nv, const int32_t* T, int64_t nt, const int32_t* E, int64_t N, double k,
+                 double h, int M, double r, int prec, aim_plan* p) {
     const auto t0 = std::chrono::steady_clock::now();
     AIM_CUDA(cudaGetDevice(&p->device));
     AIM_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
@@ -227,7 +210,7 @@ static void create(const double* V, int64_t nv, const int32_t* T, int64_t nt, co
     p->plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-static void destroy(aim_plan* p) {
+void destroy_plan(aim_plan* p) {
     if (!p) return;
     int cur = 0;
     cudaGetDevice(&cur);
@@ -266,12 +249,12 @@ int aim_plan_create(const double* vertices, int64_t nv, const int32_t* triangles
     if (dist) return fail(AIM_E_ARG, "dist must be NULL (single-GPU plan)");
     aim_plan* p = new aim_plan();
     const int st = guarded([&] {
-        create(vertices, nv, triangles, nt, rwg_edges, n_rwg, k, h, M, near_radius, precision, p);
+        create_plan(vertices, nv, triangles, nt, rwg_edges, n_rwg, k, h, M, near_radius, precision, p);
         return AIM_OK;
     });
     if (st != AIM_OK) {
         const std::string msg = g_err;
-        destroy(p);
+        destroy_plan(p);
         g_err = msg;
         return st;
     }
@@ -281,7 +264,7 @@ int aim_plan_create(const double* vertices, int64_t nv, const int32_t* triangles
 
 int aim_plan_destroy(aim_plan* plan) {
     return guarded([&] {
-        destroy(plan);
+        destroy_plan(plan);
         return AIM_OK;
     });
 }

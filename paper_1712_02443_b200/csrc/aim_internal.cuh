@@ -30,6 +30,27 @@ struct Error : std::runtime_error {
     } while (0)
 
 void note_launch(const char* name);  // counts launches, checks launch errors
+std::string& last_error();           // thread-local message behind aim_last_error()
+
+inline int fail(int status, const std::string& msg) {
+    last_error() = msg;
+    return status;
+}
+
+// run an API body, mapping exceptions to aim_status codes
+template <class F>
+int guarded(F&& f) {
+    try {
+        last_error().clear();
+        return f();
+    } catch (const Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(AIM_E_NOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(AIM_E_CUDA, e.what());
+    }
+}
 
 // eta0 = mu0 c with mu0 = 4 pi 1e-7 (reading D1; one fixed value).
 constexpr double kPi = 3.14159265358979323846;
@@ -71,13 +92,17 @@ struct FftPass {
 // Fused planar y/z pass (planar arrays): y fwd, direct z convolution with the
 // 2-D spectrum G2[(Px/2+1)][(Py/2+1)][Nz], y inv; in place on [4][Px][Ny][Nz][R].
 constexpr int kPlanarMaxNz = 16;
+// The same kernel serves the slab-decomposed path with the roles of x and y
+// swapped (outer = a local range of ky starting at `off`, lines along x).
 struct PlanarPass {
     void* W;
     int prec = 0;        // as FftPass::prec
-    int Px, Ny, Nz, R, RC;
+    int Px, Ny, Nz, R, RC;   // Px: number of outer planes per component in W
     int PyH;
     FftAxis ay;
-    const void* spec;
+    const void* spec;    // [(Pfold/2+1)][PyH][Nz]
+    int off = 0;         // global index of outer plane 0
+    int Pfold = 0;       // period of the outer axis (min-image fold of the spectrum index)
 };
 
 void launch_fft_pass(const FftPass& p, cudaStream_t s);
@@ -207,6 +232,11 @@ struct aim_plan {
 namespace aim {
 
 constexpr int kProfEvents = 9;
+
+// ---- whole-plan construction / teardown (aim_api.cu)
+void create_plan(const double* V, int64_t nv, const int32_t* T, int64_t nt, const int32_t* E, int64_t N, double k,
+                 double h, int M, double r, int prec, aim_plan* p);
+void destroy_plan(aim_plan* p);
 
 // ---- plan-building launches (k_plan.cu)
 void build_weights(aim_plan* p, cudaStream_t s);

@@ -330,7 +330,8 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
         cp_commit();
         cp_wait_prev();
         __syncthreads();
-        const int ax_ = min(ckx, p.Px - ckx);
+        const int kg = ckx + p.off;   // global index of the outer (spectral) axis
+        const int ax_ = min(kg, p.Pfold - kg);
         const C* g2 = ((const C*)p.spec) + (long long)ax_ * p.PyH * NZ;
         C* res = F::template run<-1>(X, Y, tw);
         planar_toeplitz<NZ>(res, g2, Py, 1, NL);
@@ -466,7 +467,8 @@ __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int
         if (t + 1 < t1) issue(odd ? buf0 : buf1);
         cp_commit();
         cp_wait_prev();
-        const int ax_ = min(ckx, p.Px - ckx);
+        const int kg = ckx + p.off;   // global index of the outer (spectral) axis
+        const int ax_ = min(kg, p.Pfold - kg);
         const C* g2 = ((const C*)p.spec) + (long long)ax_ * p.PyH * NZ;   // G2 slice of this kx (read through L1)
         __syncthreads();
         F::template run<-1>(buf, tw, p.ay, NL);

@@ -743,6 +743,7 @@ static void convolve_impl(aim_plan* p, const void* Q, void* Phi, int R, cudaStre
         PlanarPass q{};
         q.prec = p->prec;
         q.W = p->W1; q.Px = Px; q.Ny = (int)Ny; q.Nz = (int)Nz; q.R = R; q.PyH = Py / 2 + 1; q.ay = p->ax[1];
+        q.off = 0; q.Pfold = Px;
         q.spec = spec;
         launch_planar_yz(q, s);
     } else {

@@ -1,0 +1,151 @@
+"""Slab-decomposed product: the host partition on CPU
+(including a world_size-2 gloo run of the multi-process plumbing), and on the
+GPU the G-slab operator with device-copy exchanges vs the single-GPU plan
+(<= 1e-13) and the oracle (<= 1e-10)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from workloads import get_config, make_mesh, make_vectors
+
+
+def _oracle_bases(mesh, h, M):
+    from oracle.aim import grid_box, stencil_bases
+    from oracle.geometry import rwg_geometry
+    geo = rwg_geometry(mesh.vertices, mesh.triangles, mesh.rwg)
+    b = stencil_bases(geo["centre"], h, M)
+    return b, grid_box(b, M)
+
+
+@pytest.mark.parametrize("name", ["c1", "t_m3", "t_dissim", "c2"])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_partition(name, world):
+    from paper_1712_02443_b200 import AimError, slab_partition
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    b, (origin, dims) = _oracle_bases(mesh, cfg.h, cfg.M)
+    if world * cfg.M > dims[0]:
+        with pytest.raises(AimError):
+            slab_partition(mesh, cfg.h, cfg.M, world)
+        return
+    X, owner, nx = slab_partition(mesh, cfg.h, cfg.M, world)
+    assert nx == dims[0]
+    assert X[0] == 0 and X[-1] == nx
+    assert np.all(np.diff(X) >= cfg.M)                      # halo reaches one neighbour only
+    bx = b[:, 0] - origin[0]                                 # D3 bases (oracle)
+    assert np.array_equal(owner, np.searchsorted(X, bx, side="right") - 1)
+    cnt = np.bincount(owner, minlength=world)
+    per_plane = np.bincount(bx, minlength=nx).max()
+    assert cnt.max() <= mesh.n_rwg / world + per_plane      # balanced to one plane
+
+
+def test_partition_rejects_too_many_slabs():
+    from paper_1712_02443_b200 import AimError, slab_partition
+    cfg = get_config("c1")
+    with pytest.raises(AimError):
+        slab_partition(make_mesh(cfg), cfg.h, cfg.M, 12)     # 12 * M > Nx = 12
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, name, q):
+    import torch
+    import torch.distributed as dist
+    from paper_1712_02443_b200 import slab_partition
+    from paper_1712_02443_b200.api import slab_nccl_id
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    nid = slab_nccl_id()                                     # rank 0 makes it, all receive it
+    X, owner, nx = slab_partition(mesh, cfg.h, cfg.M, world)
+    mine = torch.tensor([int((owner == rank).sum())], dtype=torch.int64)
+    counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(counts, mine)
+    xs = [torch.zeros(world + 1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(xs, torch.from_numpy(X.astype(np.int64)))
+    ids = [None] * world
+    dist.all_gather_object(ids, nid)
+    # max-over-ranks timing reduction as bench.py does it
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    q.put((rank, [int(c) for c in counts], [x.tolist() for x in xs], len(set(ids)), len(nid), float(t)))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_partition_and_plumbing():
+    import torch.multiprocessing as mp
+    world, name = 2, "c2"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gloo_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N = make_mesh(get_config(name)).n_rwg
+    for rank, counts, xs, nids, idlen, tmax in res:
+        assert sum(counts) == N                              # every RWG owned exactly once
+        assert xs[0] == xs[1]                                # identical partition on every rank
+        assert nids == 1 and idlen == 128                    # one NCCL id, broadcast
+        assert tmax == float(world)
+    assert res[0][1] == res[1][1]
+
+
+# ------------------------------------------------------------------ GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,world,nrhs", [("c1", 2, 1), ("c1", 3, 5), ("c1", 6, 16), ("t_m3", 2, 2),
+                                             ("t_dissim", 3, 9)])
+def test_slab_matvec_vs_single_and_oracle(name, world, nrhs):
+    import torch
+    from conftest import oracle_plan
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    if single.info["conv_mode"] != 1:
+        pytest.skip("slab mode needs a planar grid")
+    slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
+    q = [slab.query(r) for r in range(world)]
+    assert q[0]["n0"] == 0 and q[-1]["n1"] == mesh.n_rwg
+    assert sum(d["nnz_near"] for d in q) == single.info["nnz_near"]
+    x = make_vectors(mesh.n_rwg, nrhs, 3)
+    xt = torch.from_numpy(x).cuda()
+    y1 = single.matvec(xt).cpu().numpy()
+    yg = slab.matvec(xt).cpu().numpy()
+    assert np.linalg.norm(yg - y1) / np.linalg.norm(y1) <= 1e-13
+    ref = oracle_plan(name).matvec(x)
+    assert np.linalg.norm(yg - ref) / np.linalg.norm(ref) <= 1e-10
+    assert np.array_equal(slab.matvec(xt).cpu().numpy(), yg)     # deterministic
+    slab.close()
+    single.close()
+
+
+@pytest.mark.gpu
+def test_slab_matvec_c2_full_size():
+    """C2 at full size over 4 and 8 slabs (device-copy exchanges): equal to the
+    single-GPU plan to 1e-13 on all 16 RHS."""
+    import torch
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan
+    cfg = get_config("c2")
+    mesh = make_mesh(cfg)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    x = torch.from_numpy(make_vectors(mesh.n_rwg, cfg.nrhs, 0)).cuda()
+    y1 = single.matvec(x)
+    single.close()
+    for world in (4, 8):
+        slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
+        yg = slab.matvec(x)
+        assert float((yg - y1).norm() / y1.norm()) <= 1e-13
+        slab.close()
