@@ -57,7 +57,7 @@ static void dunavant7(double bary[7][3], double w[7]) {
 template <class T>
 static T* upload(aim_plan* p, const std::vector<T>& h) {
     T* d = p->alloc<T>(h.size());
-    AIM_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    h2d(d, h.data(), sizeof(T) * h.size(), p->stream);
     return d;
 }
 

@@ -29,6 +29,14 @@ struct Error : std::runtime_error {
         }                                                                               \
     } while (0)
 
+// Host -> device copy ordered on stream `s` and complete on return.  (A plain
+// cudaMemcpy from pageable memory may return before its DMA has landed, and
+// kernels on a non-blocking stream do not wait for the legacy stream.)
+inline void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+    AIM_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+    AIM_CUDA(cudaStreamSynchronize(s));
+}
+
 void note_launch(const char* name);  // counts launches, checks launch errors
 std::string& last_error();           // thread-local message behind aim_last_error()
 

@@ -562,11 +562,11 @@ void make_fft_axis(int P, FftAxis& ax) {
         h[e] = make_double2((double)cosl(a), (double)sinl(a));
     }
     AIM_CUDA(cudaMalloc(&ax.tw, sizeof(double2) * P));
-    AIM_CUDA(cudaMemcpy(ax.tw, h.data(), sizeof(double2) * P, cudaMemcpyHostToDevice));
+    h2d(ax.tw, h.data(), sizeof(double2) * P, 0);
     std::vector<float2> h32(P);
     for (int e = 0; e < P; ++e) h32[e] = make_float2((float)h[e].x, (float)h[e].y);
     AIM_CUDA(cudaMalloc(&ax.tw32, sizeof(float2) * P));
-    AIM_CUDA(cudaMemcpy(ax.tw32, h32.data(), sizeof(float2) * P, cudaMemcpyHostToDevice));
+    h2d(ax.tw32, h32.data(), sizeof(float2) * P, 0);
 }
 
 static constexpr int kFftThreads = 256;

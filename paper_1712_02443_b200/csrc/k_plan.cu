@@ -266,8 +266,8 @@ void build_near_list(aim_plan* p, cudaStream_t s) {
     }
     AIM_CUDA(cudaMalloc(&cg.cptr, sizeof(int32_t) * (ncells + 1)));
     AIM_CUDA(cudaMalloc(&cg.cids, sizeof(int32_t) * N));
-    AIM_CUDA(cudaMemcpy(cg.cptr, cptr.data(), sizeof(int32_t) * (ncells + 1), cudaMemcpyHostToDevice));
-    AIM_CUDA(cudaMemcpy(cg.cids, cids.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    h2d(cg.cptr, cptr.data(), sizeof(int32_t) * (ncells + 1), s);
+    h2d(cg.cids, cids.data(), sizeof(int32_t) * N, s);
     int32_t* d_cnt = nullptr;
     AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int32_t) * N));
     near_scan_kernel<false><<<nblk(N, 256), 256, 0, s>>>(p->rwg_c, N, cg, lim, nullptr, d_cnt, nullptr);
@@ -442,7 +442,7 @@ void build_near_mma(aim_plan* p, cudaStream_t s) {
     const std::vector<int32_t> rows = morton_rows(p, RB);
     const long long nblk = (long long)rows.size() / RB;
     p->nm_rows = p->alloc<int32_t>(RB * nblk);
-    AIM_CUDA(cudaMemcpy(p->nm_rows, rows.data(), sizeof(int32_t) * RB * nblk, cudaMemcpyHostToDevice));
+    h2d(p->nm_rows, rows.data(), sizeof(int32_t) * RB * nblk, s);
     int64_t* d_cnt = nullptr;
     AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int64_t) * nblk));
     if (MT == 1)
@@ -493,7 +493,7 @@ void build_near_blocks(aim_plan* p, cudaStream_t s) {
     const std::vector<int32_t> rows = morton_rows(p, 4);
     const long long nblk = (long long)rows.size() / 4;
     p->nb_rows = p->alloc<int32_t>(4 * nblk);
-    AIM_CUDA(cudaMemcpy(p->nb_rows, rows.data(), sizeof(int32_t) * 4 * nblk, cudaMemcpyHostToDevice));
+    h2d(p->nb_rows, rows.data(), sizeof(int32_t) * 4 * nblk, s);
     int64_t* d_cnt = nullptr;
     AIM_CUDA(cudaMalloc(&d_cnt, sizeof(int64_t) * nblk));
     near_block_kernel<false><<<nblk_of(nblk), 128, 0, s>>>(p->nb_rows, nblk, p->nrow, p->ncol, p->nval, nullptr, d_cnt,

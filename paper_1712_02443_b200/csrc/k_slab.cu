@@ -150,11 +150,17 @@ __global__ void slab_near_rows_kernel(const int32_t* __restrict__ perm, long lon
                                       const int64_t* __restrict__ growp, const int32_t* __restrict__ gcol,
                                       const double2* __restrict__ gval, const int32_t* __restrict__ iperm,
                                       const int32_t* __restrict__ owner, const int64_t* __restrict__ lrowp,
-                                      int32_t* __restrict__ lcol, double2* __restrict__ lval) {
+                                      int32_t* __restrict__ lcol, double2* __restrict__ lval, long long N,
+                                      long long gnnz, long long* __restrict__ err) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nloc) return;
     const int g = perm[n0 + i];
+    if (g < 0 || g >= N) { atomicCAS((unsigned long long*)err, 0ULL, (unsigned long long)(1000000000LL + i)); return; }
     const long long e0 = growp[g], e1 = growp[g + 1];
+    if (e0 < 0 || e1 > gnnz || e1 < e0) { atomicCAS((unsigned long long*)err, 0ULL, (unsigned long long)(2000000000LL + i)); return; }
+    for (long long e = e0; e < e1; ++e)
+        if (gcol[e] < 0 || gcol[e] >= N) { atomicCAS((unsigned long long*)err, 0ULL, (unsigned long long)(3000000000LL + e)); return; }
+    if (lrowp[i + 1] - lrowp[i] != e1 - e0) { atomicCAS((unsigned long long*)err, 0ULL, (unsigned long long)(4000000000LL + i)); return; }
     long long o = lrowp[i];
     int cur = -1;
     for (;;) {
@@ -337,7 +343,7 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
         for (int ky = S->KY[w]; ky < S->KY[w + 1]; ++ky) kyown[ky] = w;
     auto up = [&](const std::vector<int32_t>& v) {
         int32_t* d = S->alloc<int32_t>(v.size());
-        AIM_CUDA(cudaMemcpy(d, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice));
+        h2d(d, v.data(), sizeof(int32_t) * v.size(), s);
         return d;
     };
     S->perm = up(perm);
@@ -394,7 +400,7 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
             node0[i] = (int32_t)(((long long)lx * S->Ny + ly) * S->Nz + lz);
         }
         q->node0 = q->alloc<int32_t>(std::max<long long>(nl, 1));
-        if (nl) AIM_CUDA(cudaMemcpy(q->node0, node0.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
+        if (nl) h2d(q->node0, node0.data(), sizeof(int32_t) * nl, s);
         build_projection_csr(q, node0, s);
         // near rows: columns renumbered and re-sorted
         std::vector<int64_t> lrowp(nl + 1, 0);
@@ -406,11 +412,22 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
         q->nrow = q->alloc<int64_t>(nl + 1);
         q->ncol = q->alloc<int32_t>(q->nnzN);
         q->nval = q->alloc<double2>(q->nnzN);
-        AIM_CUDA(cudaMemcpy(q->nrow, lrowp.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice));
+        h2d(q->nrow, lrowp.data(), sizeof(int64_t) * (nl + 1), s);
         if (nl) {
+            long long* d_err = nullptr;
+            AIM_CUDA(cudaMalloc(&d_err, sizeof(long long)));
+            AIM_CUDA(cudaMemsetAsync(d_err, 0, sizeof(long long), s));
             slab_near_rows_kernel<<<nblk(nl, 128), 128, 0, s>>>(S->perm, R.n0, nl, B->nrow, B->ncol, B->nval, d_iperm,
-                                                                d_owner, q->nrow, q->ncol, q->nval);
+                                                                d_owner, q->nrow, q->ncol, q->nval, N, B->nnzN, d_err);
             note_launch("slab_near_rows");
+            long long herr = 0;
+            AIM_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(long long), cudaMemcpyDeviceToHost, s));
+            AIM_CUDA(cudaStreamSynchronize(s));
+            cudaFree(d_err);
+            if (herr)
+                throw Error(AIM_E_GRID, "slab near rows: bad index code " + std::to_string(herr) + " rank " +
+                                            std::to_string(w) + " nl " + std::to_string(nl) + " nnz " +
+                                            std::to_string(q->nnzN) + " gnnz " + std::to_string(B->nnzN));
         }
         AIM_CUDA(cudaStreamSynchronize(s));
         S->ranks.push_back(R);
@@ -459,7 +476,7 @@ static void slab_workspace(aim_slab* S, int R) {
         std::vector<long long> off(S->world + 1, 0);
         for (int w = 0; w < S->world; ++w) off[w + 1] = off[w] + 4LL * (S->KY[w + 1] - S->KY[w]) * Rk.Xl * NzR;
         Rk.d_off1 = S->alloc<long long>(S->world + 1);
-        AIM_CUDA(cudaMemcpy(Rk.d_off1, off.data(), sizeof(long long) * (S->world + 1), cudaMemcpyHostToDevice));
+        h2d(Rk.d_off1, off.data(), sizeof(long long) * (S->world + 1), S->stream);
     }
     S->ws_nrhs = R;
 }
