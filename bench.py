@@ -2,7 +2,7 @@
 """Benchmark of the AIM matvec hot path (BASELINE.json metric: AIM matvecs/sec,
 complex128, and fraction of the HBM roofline).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference] [--slab]
 
 Workload (default): BASELINE.json configs[1] = "c2", the 10x10 array of
 0.4-lambda cubes (N = 115,200 RWG unknowns), h = 0.05, M = 2, near radius 0.2,
@@ -11,7 +11,9 @@ aim_matvec on the 16-RHS batch (projection, 5 FFT passes, interpolation +
 near-field SpMV).  `value` counts single-RHS matvecs per second over all
 ranks.  N > 1: one process per GPU, each rank runs an independent replica
 plan on its own 16-RHS batch (RHS sharding, no data-path collective, weak
-scaling; DESIGN.md "Multi-GPU").
+scaling).  --slab: the slab-decomposed operator
+(default config c4, the 1.8M-unknown array): the ranks cooperate on every
+product (x-slabs, NCCL all-to-all FFT transposes, strong scaling).
 
 Timing: CUDA events on the launching stream, W warm-up steps, barrier +
 synchronize on both sides, max over ranks.  The working set (near matrix
@@ -69,13 +71,30 @@ def alg_bytes(info, R):
     return matvec, stages
 
 
+def fp64_peak():
+    """FP64 FMA peak derived from the unit counts and clock (B200: 148 SMs x 64
+    FP64 lanes per clock x 2 flop x 1.965 GHz max SM clock).
+    tools/fp64_peak.cu measured 34.2 TFLOP/s for a DFMA loop (profiles/fp64_peak.txt)."""
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 lanes x 2 x 1.965 GHz"
+
+
+def planar_flops(info, R):
+    """Algorithmic flops of one planar y/z launch: forward + inverse y FFTs of
+    length Py over 4 Px Nz R lines (5 P log2 P each) and the direct z Toeplitz
+    product, 8 Nz^2 flops per (component, kx, ky, rhs) column."""
+    Px, Py, _ = info["fft_dims"]
+    Nz = info["grid_dims"][2]
+    lines = 4 * Px * Nz * R
+    return 2 * lines * 5 * Py * math.log2(Py) + 4 * Px * Py * R * 8 * Nz * Nz
+
+
 KERNEL_NAMES = {
-    "near": "near_kernel (H6 precorrected near-field SpMV, side stream)",
+    "near": "near_mma_kernel (H6 precorrected near-field SpMM, FP64 tensor cores)",
     "project": "project_kernel (H1 projection gather)",
     "interp": "interp_kernel (H5 interpolation)",
-    "fft_x": "fft_pass_kernel (x forward, zero-pad fused)",
-    "fft_yz": "planar_yz_kernel / fft_pass_kernel x3 (y fwd, z convolution, y inv)",
-    "ifft_x": "fft_pass_kernel (x inverse, pruned)",
+    "fft_x": "fft_ct_kernel (x forward, zero-pad fused)",
+    "fft_yz": "planar_ct_kernel (y fwd FFT, z Toeplitz x G2, y inv FFT, fused)",
+    "ifft_x": "fft_ct_kernel (x inverse, pruned)",
 }
 
 
@@ -191,6 +210,97 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args, ws, rank, local):
+    """--slab: the slab-decomposed operator (aim_slab_*), one rank per GPU over
+    NCCL (at N = 1 a one-rank communicator), strong scaling of one product."""
+    import numpy as np
+    import torch
+    from paper_1712_02443_b200 import AimSlabPlan, launch_count, nccl_unique_id
+    from paper_1712_02443_b200.api import slab_nccl_id
+    from workloads import get_config, make_mesh, make_vectors
+
+    torch.cuda.set_device(local)
+    cfg = get_config(args.config)
+    mesh = make_mesh(cfg)
+    R = cfg.nrhs
+    nid = slab_nccl_id() if ws > 1 else nccl_unique_id()
+    t0 = time.perf_counter()
+    plan = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, ws, rank, nid)
+    plan_s = time.perf_counter() - t0
+    q = plan.query(rank)
+    xh = make_vectors(mesh.n_rwg, R, seed=0)          # x replicated on every rank
+    x = torch.from_numpy(xh).cuda()
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        plan.matvec(x, y)
+    torch.cuda.synchronize()
+    barrier()
+    clk = ClockSampler(local) if rank == 0 else None
+    time.sleep(0.15 if clk else 0)
+    torch.cuda.synchronize()
+    barrier()
+    launch_count(reset=True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        plan.matvec(x, y)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = launch_count()
+    clocks = clk.stop() if clk else None
+    t = ev0.elapsed_time(ev1) / 1e3
+    if ws > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    value = args.steps * R / t                        # one product per step for the whole job
+    # end to end: pinned host x -> device, product, y -> pinned host, every step
+    xp = torch.from_numpy(xh).pin_memory()
+    yp = torch.empty_like(xp).pin_memory()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        x.copy_(xp, non_blocking=True)
+        plan.matvec(x, y)
+        yp.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+    te = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        te = float(tt.item())
+    ms_step = 1e3 * t / args.steps
+    peak, peak_src = load_peaks()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded cube-array mesh per BASELINE.json, N(0,1) complex vectors)",
+        "config": {"workload": f"{cfg.name}: slab-decomposed product (N={mesh.n_rwg}, {R} RHS)",
+                   "N": mesh.n_rwg, "nrhs": R, "parallelism": f"x-slabs x{ws} (NCCL all-to-all FFT transposes)",
+                   "slab_rank0": q, "l2": "working set > 126 MB L2 (no flush needed)"},
+        "nvlink": {"a2a_bytes_per_rank_per_step": q["a2a_bytes_per_rhs"] * R,
+                   "halo_bytes_per_rank_per_step": q["halo_bytes_per_rhs"] * R},
+        "e2e": {"value": args.e2e_steps * R / te, "unit": UNIT, "h2d_bytes_per_step": int(xh.nbytes),
+                "d2h_bytes_per_step": int(xh.nbytes), "steps": args.e2e_steps,
+                "timer": "host wall clock around copy + product + copy"},
+        "gpu_launches": int(launches), "clocks": clocks, "plan_seconds": plan_s, "peak_hbm_gbs": peak,
+        "peak_source": peak_src,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -200,11 +310,18 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--slab", action="store_true",
+                    help="slab-decomposed operator over the ranks (default config c4) instead of RHS replicas")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.slab and "--config" not in sys.argv:
+        args.config = "c4"
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if args.slab:
+        run_slab(args, ws, rank, local)
         return
 
     import numpy as np
@@ -282,11 +399,21 @@ def main():
     dom = max(b_stage, key=lambda k: stage_ms.get(k, 0.0))
     ach = stage_gbs[dom]
     traffic = load_traffic(dom)
-    roof = {"kernel": KERNEL_NAMES[dom], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-            "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": b_stage[dom],
-            "ms_per_launch": stage_ms[dom], "peak_source": peak_src,
-            "timing": "CUDA events recorded by the library around the kernel on its launch stream, "
-                      "averaged over the timed region"}
+    timing = ("CUDA events recorded by the library around the kernel on its launch stream, "
+              "averaged over the timed region")
+    if dom == "fft_yz" and info["conv_mode"] == 1:
+        # the fused planar y/z kernel is FP64-ALU bound (ncu: fp64 pipe busiest, DRAM ~10%)
+        fl = planar_flops(info, R)
+        pk, pk_src = fp64_peak()
+        tf = fl / (stage_ms[dom] / 1e3) / 1e12
+        roof = {"kernel": KERNEL_NAMES[dom], "bound": "alu", "achieved": tf, "peak": pk, "unit": "TFLOP/s",
+                "frac": tf / pk, "traffic": traffic, "alg_flops_per_launch": fl,
+                "alg_bytes_per_launch": b_stage[dom], "hbm_frac": ach / peak,
+                "ms_per_launch": stage_ms[dom], "peak_source": pk_src, "timing": timing}
+    else:
+        roof = {"kernel": KERNEL_NAMES[dom], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": b_stage[dom],
+                "ms_per_launch": stage_ms[dom], "peak_source": peak_src, "timing": timing}
     ms_step = 1e3 * t / args.steps
     mv_ach = b_mv / (ms_step / 1e3) / 1e9
     line = {

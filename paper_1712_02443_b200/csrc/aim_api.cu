@@ -197,6 +197,8 @@ void create_plan(const double* V, int64_t nv, const int32_t* T, int64_t nt, cons
     p->node0 = upload(p, node0);
     for (int d = 0; d < 3; ++d) make_fft_axis(p->pads[d], p->ax[d]);
     p->planar = planar_supported(p->pads[1], p->dims[2], p->ax[1].min_radix) ? 1 : 0;
+    // AIM_CONV_MODE=0 in the environment forces the 3-D FFT convolution (tests of that path on small grids)
+    if (getenv("AIM_CONV_MODE") && getenv("AIM_CONV_MODE")[0] == '0') p->planar = 0;
 
     // ---- device setup S2-S4
     cudaStream_t s = p->stream;

@@ -95,6 +95,11 @@ struct FftPass {
     const void* spec;
     int Px, Py;          // outer = (c Px + kx) Py + ky
     int PyH, PzH;        // octant extents Py/2+1, Pz/2+1
+    // spec_mode 1 (x-line turnaround of the slab path): outer = c nky + kyl with
+    // ky = off + kyl, inner = kz Rin + r, spectrum transposed [ay][az][ax]
+    int spec_mode = 0;
+    int Pz = 0, PxH = 0;
+    int off = 0, nky = 1, Rin = 1;
 };
 
 // Fused planar y/z pass (planar arrays): y fwd, direct z convolution with the

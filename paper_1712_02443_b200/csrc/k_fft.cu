@@ -51,6 +51,24 @@ __device__ __forceinline__ const C* tw_of(const FftAxis& ax) {
     if constexpr (sizeof(C) == 16) return (const C*)ax.tw;
     else return (const C*)ax.tw32;
 }
+// Spectrum line of a turnaround pass (mode 2) for the line (outer og, inner ii):
+//   spec_mode 0 (z lines): og = (c Px + kx) Py + ky, octant [ax][ay][az], line index kz;
+//   spec_mode 1 (x lines of the slab path): og = c nky + kyl, ky = off + kyl,
+//     kz = ii / Rin, transposed octant [ay][az][ax], line index kx.
+template <class C>
+__device__ __forceinline__ const C* spec_line(const FftPass& p, long long og, long long ii) {
+    if (p.spec_mode == 0) {
+        const int ky = (int)(og % p.Py);
+        const int kx = (int)((og / p.Py) % p.Px);
+        const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
+        return ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
+    }
+    const int ky = p.off + (int)(og % p.nky);
+    const int kz = (int)(ii / p.Rin);
+    const int ay = min(ky, p.Py - ky), az = min(kz, p.Pz - kz);
+    return ((const C*)p.spec) + ((long long)ay * p.PzH + az) * p.PxH;
+}
+
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
@@ -141,10 +159,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fft_pipe_kernel(FftPass p, int til
                 // x spectrum: line (o, i) belongs to outer og = (c Px + kx) Py + ky; kz = j
                 if (lm.active) {
                     const int og = min(cur_o * TO + o, outer - 1);
-                    const int ky = og % p.Py;
-                    const int kx = (og / p.Py) % p.Px;
-                    const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
-                    const C* g = ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                    const C* g = spec_line<C>(p, og, min(cur_i * TI + i, inner - 1));
                     for (int j = lm.js; j < P; j += lm.JS)
                         buf[j * NL + lm.l] = cmul(buf[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
                 }
@@ -254,10 +269,7 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
             if constexpr (MODE == 2) {
                 if (act) {
                     const int og = min(cur_o * (NL / TI) + o, outer - 1);
-                    const int ky = og % p.Py;
-                    const int kx = (og / p.Py) % p.Px;
-                    const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
-                    const C* g = ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                    const C* g = spec_line<C>(p, og, min(cur_i * TI + i, inner - 1));
                     for (int j = js; j < P; j += JS) res[j * NL + l] = cmul(res[j * NL + l], __ldg(&g[min(j, P - j)]));
                 }
                 __syncthreads();
@@ -392,10 +404,7 @@ __global__ void __launch_bounds__(256, 2) fft_pp_kernel(FftPass p) {
         if (p.mode == 2) {
             if (lm.active) {
                 const long long og = o0 + min(o, to_n - 1);
-                const int ky = (int)(og % p.Py);
-                const int kx = (int)((og / p.Py) % p.Px);
-                const int ax_ = min(kx, p.Px - kx), ay = min(ky, p.Py - ky);
-                const C* g = ((const C*)p.spec) + ((long long)ax_ * p.PyH + ay) * p.PzH;
+                const C* g = spec_line<C>(p, og, i0 + min(i, ti_n - 1));
                 for (int j = lm.js; j < P; j += lm.JS) res[j * NL + lm.l] = cmul(res[j * NL + lm.l], __ldg(&g[min(j, P - j)]));
             }
             __syncthreads();

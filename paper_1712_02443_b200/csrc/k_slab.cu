@@ -11,14 +11,15 @@
 // renumbered so each rank's rows are contiguous (permuted order = by owner,
 // then by id); x is replicated, y is gathered back to every rank.
 //
-// One product (planar grids, conv_mode 1):
+// One product (planar grids, conv_mode 1; 3-D grids add the z passes):
 //   near rows + projection of the owned RWGs  -> Q on [X_r, X_{r+1} + M)
 //   halo reduce: planes [X_{r+1}, X_{r+1} + M) are added into rank r+1
-//   y forward FFT (pad Ny -> Py) on the owned planes
+//   y forward FFT (pad Ny -> Py) on the owned planes [3-D: then z forward, pad Nz -> Pz]
 //   all-to-all #1: x-slabs -> ky-slabs [KY_s, KY_{s+1}) with every x
-//   x forward FFT (pad Nx -> Px), z Toeplitz x G2, x inverse (prune) -- the
-//     planar kernel with the roles of x and y swapped (transposed spectrum)
-//   all-to-all #2 back to x-slabs, y inverse FFT (prune Py -> Ny)
+//   planar: x forward FFT (pad Nx -> Px), z Toeplitz x G2, x inverse (prune) --
+//     the planar kernel with the roles of x and y swapped (transposed spectrum);
+//   3-D: x turnaround (pad, forward, x G^ octant transposed to [ky][kz][kx], inverse, prune)
+//   all-to-all #2 back to x-slabs [3-D: z inverse], y inverse FFT (prune Py -> Ny)
 //   halo copy: planes [X_{r+1}, X_{r+1} + M) of Phi from rank r+1
 //   interpolation of the owned RWGs (accumulates onto the near rows)
 //   gather of y (every rank gets all rows), un-permute.
@@ -180,14 +181,16 @@ __global__ void slab_near_rows_kernel(const int32_t* __restrict__ perm, long lon
     }
 }
 
-// spectrum [(Px/2+1)][(Py/2+1)][Nz] -> [(Py/2+1)][(Px/2+1)][Nz]
-__global__ void spec_transpose_kernel(const double2* __restrict__ a, int AX, int AY, int Nz, double2* __restrict__ b) {
+// spectrum a[AX][AY][AZ] -> planar: b[AY][AX][AZ] (kx <-> ky), 3-D: b[AY][AZ][AX]
+template <bool PLANAR>
+__global__ void spec_transpose_kernel(const double2* __restrict__ a, int AX, int AY, int AZ, double2* __restrict__ b) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (long long)AX * AY * Nz) return;
-    const int z = (int)(t % Nz);
-    const long long xy = t / Nz;
+    if (t >= (long long)AX * AY * AZ) return;
+    const int z = (int)(t % AZ);
+    const long long xy = t / AZ;
     const int y = (int)(xy % AY), x = (int)(xy / AY);
-    b[((long long)y * AX + x) * Nz + z] = a[t];
+    if (PLANAR) b[((long long)y * AX + x) * AZ + z] = a[t];
+    else b[((long long)y * AZ + z) * AX + x] = a[t];
 }
 
 // All-to-all #1 pack / #2 unpack on rank r:
@@ -232,8 +235,9 @@ struct aim_slab_rank {
     aim_plan* sub = nullptr;              // local tables (N = n1 - n0, grid Xh x Ny x Nz)
     // workspaces (complex128), sized for ws_nrhs
     double2* Qh = nullptr;    // [4][Xh][Ny][Nz][R]   projection (+halo) / Phi (+halo)
-    double2* Wy = nullptr;    // [4][Xl][Py][Nz][R]   after the y forward pass
-    double2* T = nullptr;     // [4][KYl][Nx][Nz][R]  x pencils
+    double2* Wy = nullptr;    // [4][Xl][Py][Zc][R]   after the y (3-D: and z) forward pass
+    double2* Wy1 = nullptr;   // [4][Xl][Py][Nz][R]   3-D only: between the y and z passes
+    double2* T = nullptr;     // [4][KYl][Nx][Zc][R]  x pencils
     double2* sb = nullptr;    // send blocks  (max of the two all-to-alls)
     double2* rb = nullptr;    // receive blocks
     double2* hb = nullptr;    // halo staging [4][M][Ny][Nz][R]
@@ -244,7 +248,9 @@ struct aim_slab {
     int world = 1, rank = -1;             // rank < 0: all slabs in this process
     bool virt = true;
     aim_plan* base = nullptr;             // full single-GPU plan (spectrum, FFT axes, grid dims)
-    int Nx = 0, Ny = 0, Nz = 0, Px = 0, Py = 0, M = 0;
+    int Nx = 0, Ny = 0, Nz = 0, Px = 0, Py = 0, Pz = 0, M = 0;
+    int planar = 1;
+    int Zc = 0;                           // z extent of the exchanged layout: Nz (planar) or Pz (3-D)
     int64_t N = 0;
     std::vector<int> X, KY;
     std::vector<int64_t> nstart;
@@ -252,7 +258,7 @@ struct aim_slab {
     int32_t* perm = nullptr;              // [N] permuted row -> RWG id
     int32_t* kyown = nullptr;             // [Py] owner of ky
     int32_t* d_KY = nullptr;              // [world+1]
-    double2* g2t = nullptr;               // transposed planar spectrum
+    double2* g2t = nullptr;               // transposed spectrum (planar [ay][ax][dz], 3-D [ay][az][ax])
     double2* xp = nullptr;                // [N][R] permuted x
     double2* yp = nullptr;                // [N][R] permuted y
     int ws_nrhs = 0;
@@ -312,10 +318,12 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     S->base = new aim_plan();
     create_plan(V, nv, T, nt, E, N, k, h, M, r, AIM_C128, S->base);
     aim_plan* B = S->base;
-    if (!B->planar || !planar_supported(B->pads[0], B->dims[2], B->ax[0].min_radix))
-        throw Error(AIM_E_ARG, "slab decomposition needs a planar grid (conv_mode 1) in both x and y");
+    S->planar = B->planar;
+    if (S->planar && !planar_supported(B->pads[0], B->dims[2], B->ax[0].min_radix))
+        throw Error(AIM_E_ARG, "planar slab pass: the x lines do not fit the planar kernel");
     S->Nx = B->dims[0]; S->Ny = B->dims[1]; S->Nz = B->dims[2];
-    S->Px = B->pads[0]; S->Py = B->pads[1];
+    S->Px = B->pads[0]; S->Py = B->pads[1]; S->Pz = B->pads[2];
+    S->Zc = S->planar ? S->Nz : S->Pz;
     // partition (host formula, checked against the plan's own stencil bases)
     std::vector<int> bx;
     int Nx = 0;
@@ -351,10 +359,13 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     S->d_KY = up(std::vector<int32_t>(S->KY.begin(), S->KY.end()));
     int32_t* d_iperm = up(iperm);
     int32_t* d_owner = up(owner);
-    // transposed planar spectrum for the x-pencil pass
-    const int AX = S->Px / 2 + 1, AY = S->Py / 2 + 1;
-    S->g2t = S->alloc<double2>((size_t)AX * AY * S->Nz);
-    spec_transpose_kernel<<<nblk((long long)AX * AY * S->Nz, 256), 256, 0, s>>>(B->spec, AX, AY, S->Nz, S->g2t);
+    // transposed spectrum for the x-pencil pass
+    const int AX = S->Px / 2 + 1, AY = S->Py / 2 + 1, AZ = S->planar ? S->Nz : S->Pz / 2 + 1;
+    S->g2t = S->alloc<double2>((size_t)AX * AY * AZ);
+    if (S->planar)
+        spec_transpose_kernel<true><<<nblk((long long)AX * AY * AZ, 256), 256, 0, s>>>(B->spec, AX, AY, AZ, S->g2t);
+    else
+        spec_transpose_kernel<false><<<nblk((long long)AX * AY * AZ, 256), 256, 0, s>>>(B->spec, AX, AY, AZ, S->g2t);
     note_launch("slab_spec_transpose");
     std::vector<int64_t> growp(N + 1);
     AIM_CUDA(cudaMemcpy(growp.data(), B->nrow, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost));
@@ -447,7 +458,7 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     // exchange volume per RHS (max over ranks): all-to-all out + in, halos
     for (int w = 0; w < world; ++w) {
         const long long Xl = S->X[w + 1] - S->X[w], kys = S->KY[w + 1] - S->KY[w];
-        const long long out = 4 * Xl * (S->Py - kys) * S->Nz * 16, in = 4 * kys * (S->Nx - Xl) * S->Nz * 16;
+        const long long out = 4 * Xl * (S->Py - kys) * S->Zc * 16, in = 4 * kys * (S->Nx - Xl) * S->Zc * 16;
         S->bytes_a2a = std::max<int64_t>(S->bytes_a2a, 2 * (out + in));
     }
     S->bytes_halo = 2LL * 4 * M * S->Ny * S->Nz * 16 * (world > 1 ? 2 : 0);
@@ -460,21 +471,23 @@ static void slab_workspace(aim_slab* S, int R) {
     S->release(S->yp);
     S->xp = S->alloc<double2>((size_t)S->N * R);
     S->yp = S->alloc<double2>((size_t)S->N * R);
-    const long long NzR = (long long)S->Nz * R;
+    const long long NzR = (long long)S->Nz * R, ZR = (long long)S->Zc * R;
     for (auto& Rk : S->ranks) {
-        for (void* ptr : {(void*)Rk.Qh, (void*)Rk.Wy, (void*)Rk.T, (void*)Rk.sb, (void*)Rk.rb, (void*)Rk.hb,
-                          (void*)Rk.d_off1})
+        for (void* ptr : {(void*)Rk.Qh, (void*)Rk.Wy, (void*)Rk.Wy1, (void*)Rk.T, (void*)Rk.sb, (void*)Rk.rb,
+                          (void*)Rk.hb, (void*)Rk.d_off1})
             S->release(ptr);
+        Rk.Wy1 = nullptr;
         const long long kyl = Rk.KY1 - Rk.KY0;
         Rk.Qh = S->alloc<double2>(4LL * Rk.Xh * S->Ny * NzR);
-        Rk.Wy = S->alloc<double2>(4LL * Rk.Xl * S->Py * NzR);
-        Rk.T = S->alloc<double2>(4LL * kyl * S->Nx * NzR);
-        const long long blk = std::max(4LL * Rk.Xl * S->Py * NzR, 4LL * kyl * S->Nx * NzR);
+        Rk.Wy = S->alloc<double2>(4LL * Rk.Xl * S->Py * ZR);
+        if (!S->planar) Rk.Wy1 = S->alloc<double2>(4LL * Rk.Xl * S->Py * NzR);
+        Rk.T = S->alloc<double2>(4LL * kyl * S->Nx * ZR);
+        const long long blk = std::max(4LL * Rk.Xl * S->Py * ZR, 4LL * kyl * S->Nx * ZR);
         Rk.sb = S->alloc<double2>(blk);
         Rk.rb = S->alloc<double2>(blk);
         Rk.hb = S->alloc<double2>(4LL * S->M * S->Ny * NzR);
         std::vector<long long> off(S->world + 1, 0);
-        for (int w = 0; w < S->world; ++w) off[w + 1] = off[w] + 4LL * (S->KY[w + 1] - S->KY[w]) * Rk.Xl * NzR;
+        for (int w = 0; w < S->world; ++w) off[w + 1] = off[w] + 4LL * (S->KY[w + 1] - S->KY[w]) * Rk.Xl * ZR;
         Rk.d_off1 = S->alloc<long long>(S->world + 1);
         h2d(Rk.d_off1, off.data(), sizeof(long long) * (S->world + 1), S->stream);
     }
@@ -487,9 +500,11 @@ static aim_slab_rank* rank_of(aim_slab* S, int w) {
     return nullptr;
 }
 
-// one y pass per component: [Xl][Ny -> Py][NzR] forward or [Xl][Py -> Ny][NzR] inverse
+// one y pass per component: [Xl][Ny -> Py][NzR] forward (Qh -> Y) or
+// [Xl][Py -> Ny][NzR] inverse (Y -> Qh); Y = Wy (planar) or Wy1 (3-D)
 static void slab_ypass(aim_slab* S, aim_slab_rank& Rk, int R, bool inverse, cudaStream_t s) {
     const long long NzR = (long long)S->Nz * R;
+    double2* Y = S->planar ? Rk.Wy : Rk.Wy1;
     for (int c = 0; c < 4; ++c) {
         FftPass f{};
         f.prec = AIM_C128;
@@ -499,15 +514,31 @@ static void slab_ypass(aim_slab* S, aim_slab_rank& Rk, int R, bool inverse, cuda
         f.TO = f.TI = 0;
         if (!inverse) {
             f.in = Rk.Qh + c * (long long)Rk.Xh * S->Ny * NzR;
-            f.out = Rk.Wy + c * (long long)Rk.Xl * S->Py * NzR;
+            f.out = Y + c * (long long)Rk.Xl * S->Py * NzR;
             f.Lin = S->Ny; f.Lout = S->Py; f.mode = 0;
         } else {
-            f.in = Rk.Wy + c * (long long)Rk.Xl * S->Py * NzR;
+            f.in = Y + c * (long long)Rk.Xl * S->Py * NzR;
             f.out = Rk.Qh + c * (long long)Rk.Xh * S->Ny * NzR;
             f.Lin = S->Py; f.Lout = S->Ny; f.mode = 1;
         }
         launch_fft_pass(f, s);
     }
+}
+
+// 3-D only: z pass over [4 Xl Py][Nz -> Pz][R] (Wy1 -> Wy) or back (Wy -> Wy1)
+static void slab_zpass(aim_slab* S, aim_slab_rank& Rk, int R, bool inverse, cudaStream_t s) {
+    FftPass f{};
+    f.prec = AIM_C128;
+    f.outer = 4LL * Rk.Xl * S->Py;
+    f.inner = R;
+    f.ax = S->base->ax[2];
+    f.TO = f.TI = 0;
+    f.in = inverse ? Rk.Wy : Rk.Wy1;
+    f.out = inverse ? Rk.Wy1 : Rk.Wy;
+    f.Lin = inverse ? S->Pz : S->Nz;
+    f.Lout = inverse ? S->Nz : S->Pz;
+    f.mode = inverse ? 1 : 0;
+    launch_fft_pass(f, s);
 }
 
 // halo planes [Xl, Xh) of every component, packed [4][Xh - Xl][Ny][NzR]
@@ -525,7 +556,7 @@ static void halo_copy(aim_slab* S, const aim_slab_rank& Rk, double2* grid, doubl
 static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaStream_t s) {
     slab_workspace(S, R);
     const int G = S->world, M = S->M;
-    const long long N = S->N, NzR = (long long)S->Nz * R;
+    const long long N = S->N, NzR = (long long)S->Nz * R, ZR = (long long)S->Zc * R;
     const size_t esz = sizeof(double2);
     NcclApi* nc = S->virt ? nullptr : &nccl();
     // x in permuted order (replicated)
@@ -571,26 +602,27 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
             halo_copy(S, Rk, Rk.Qh, Rk.sb, false, 0, M, R, s);
         }
     }
-    // y forward on the owned planes, pack for all-to-all #1
+    // y (3-D: and z) forward on the owned planes, pack for all-to-all #1
     for (auto& Rk : S->ranks) {
         slab_ypass(S, Rk, R, false, s);
-        const long long tot = 4LL * Rk.Xl * S->Py * NzR;
-        slab_pack_kernel<false><<<nblk(tot, 256), 256, 0, s>>>(Rk.Wy, Rk.sb, Rk.Xl, S->Py, NzR, S->kyown, S->d_KY,
+        if (!S->planar) slab_zpass(S, Rk, R, false, s);
+        const long long tot = 4LL * Rk.Xl * S->Py * ZR;
+        slab_pack_kernel<false><<<nblk(tot, 256), 256, 0, s>>>(Rk.Wy, Rk.sb, Rk.Xl, S->Py, ZR, S->kyown, S->d_KY,
                                                                 Rk.d_off1);
         note_launch("slab_pack");
     }
-    // all-to-all #1: block (w -> v) = [4 kys_v][Xl_w][NzR] at sb(w) offset off1_w[v]; lands in T_v at x = X_w
-    auto blk1 = [&](int w, int v) { return 4LL * (S->KY[v + 1] - S->KY[v]) * (S->X[w + 1] - S->X[w]) * NzR; };
+    // all-to-all #1: block (w -> v) = [4 kys_v][Xl_w][ZR] at sb(w) offset off1_w[v]; lands in T_v at x = X_w
+    auto blk1 = [&](int w, int v) { return 4LL * (S->KY[v + 1] - S->KY[v]) * (S->X[w + 1] - S->X[w]) * ZR; };
     auto off1 = [&](int w, int v) {
         long long o = 0;
         for (int u = 0; u < v; ++u) o += blk1(w, u);
         return o;
     };
     auto place = [&](aim_slab_rank& Dv, const double2* src, int w, bool into_T) {
-        // rows (c, kyl) of width Xl_w NzR: T_v[c][kyl][X_w + x][zr] <-> src[c][kyl][x][zr]
+        // rows (c, kyl) of width Xl_w ZR: T_v[c][kyl][X_w + x][zr] <-> src[c][kyl][x][zr]
         const long long Xl = S->X[w + 1] - S->X[w], kys = Dv.KY1 - Dv.KY0;
-        const size_t wb = esz * Xl * NzR, tp = esz * (size_t)S->Nx * NzR;
-        char* t = (char*)(Dv.T + (long long)S->X[w] * NzR);
+        const size_t wb = esz * Xl * ZR, tp = esz * (size_t)S->Nx * ZR;
+        char* t = (char*)(Dv.T + (long long)S->X[w] * ZR);
         if (into_T) AIM_CUDA(cudaMemcpy2DAsync(t, tp, src, wb, wb, 4 * kys, cudaMemcpyDeviceToDevice, s));
         else AIM_CUDA(cudaMemcpy2DAsync((void*)src, wb, t, tp, wb, 4 * kys, cudaMemcpyDeviceToDevice, s));
     };
@@ -614,8 +646,27 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
             ro += blk1(v, w);
         }
     }
-    // x forward, z Toeplitz x G2, x inverse on the ky pencils
+    // x forward, z Toeplitz x G2 (3-D: x G^), x inverse on the ky pencils
     for (auto& Rk : S->ranks) {
+        if (!S->planar) {
+            FftPass f{};
+            f.prec = AIM_C128;
+            f.in = Rk.T;
+            f.out = Rk.T;
+            f.outer = 4LL * (Rk.KY1 - Rk.KY0);
+            f.Lin = f.Lout = S->Nx;
+            f.inner = ZR;
+            f.mode = 2;
+            f.ax = S->base->ax[0];
+            f.TO = f.TI = 0;
+            f.spec = S->g2t;
+            f.spec_mode = 1;
+            f.Px = S->Px; f.Py = S->Py; f.Pz = S->Pz;
+            f.PxH = S->Px / 2 + 1; f.PyH = S->Py / 2 + 1; f.PzH = S->Pz / 2 + 1;
+            f.off = Rk.KY0; f.nky = std::max(1, Rk.KY1 - Rk.KY0); f.Rin = R;
+            if (f.outer > 0) launch_fft_pass(f, s);
+            continue;
+        }
         PlanarPass q{};
         q.prec = AIM_C128;
         q.W = Rk.T;
@@ -652,10 +703,11 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
         AIM_NCCL(nc->GroupEnd());
     }
     for (auto& Rk : S->ranks) {
-        const long long tot = 4LL * Rk.Xl * S->Py * NzR;
-        slab_pack_kernel<true><<<nblk(tot, 256), 256, 0, s>>>(Rk.Wy, Rk.rb, Rk.Xl, S->Py, NzR, S->kyown, S->d_KY,
+        const long long tot = 4LL * Rk.Xl * S->Py * ZR;
+        slab_pack_kernel<true><<<nblk(tot, 256), 256, 0, s>>>(Rk.Wy, Rk.rb, Rk.Xl, S->Py, ZR, S->kyown, S->d_KY,
                                                                Rk.d_off1);
         note_launch("slab_unpack");
+        if (!S->planar) slab_zpass(S, Rk, R, true, s);
         slab_ypass(S, Rk, R, true, s);   // Phi on the owned planes, into Qh
     }
     // Phi halo: planes [Xl, Xh) of rank w <- planes [0, Xh - Xl) of rank w+1

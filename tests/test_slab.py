@@ -105,17 +105,22 @@ def test_gloo_world2_partition_and_plumbing():
 
 # ------------------------------------------------------------------ GPU
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["planar", "3d"])
 @pytest.mark.parametrize("name,world,nrhs", [("c1", 2, 1), ("c1", 3, 5), ("c1", 6, 16), ("t_m3", 2, 2),
-                                             ("t_dissim", 3, 9)])
-def test_slab_matvec_vs_single_and_oracle(name, world, nrhs):
+                                             ("t_dissim", 3, 9), ("t_vol", 2, 3)])
+def test_slab_matvec_vs_single_and_oracle(name, world, nrhs, mode, monkeypatch):
+    """planar: x pencils through the planar kernel (transposed 2-D spectrum);
+    3d (AIM_CONV_MODE=0): y and z passes local, x turnaround on the pencils
+    with the transposed octant."""
     import torch
     from conftest import oracle_plan
     from paper_1712_02443_b200 import AimPlan, AimSlabPlan
     cfg = get_config(name)
     mesh = make_mesh(cfg)
+    if mode == "3d":
+        monkeypatch.setenv("AIM_CONV_MODE", "0")
     single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    if single.info["conv_mode"] != 1:
-        pytest.skip("slab mode needs a planar grid")
+    assert single.info["conv_mode"] == (1 if mode == "planar" else 0) or name == "t_vol"
     slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
     q = [slab.query(r) for r in range(world)]
     assert q[0]["n0"] == 0 and q[-1]["n1"] == mesh.n_rwg
@@ -149,3 +154,22 @@ def test_slab_matvec_c2_full_size():
         yg = slab.matvec(x)
         assert float((yg - y1).norm() / y1.norm()) <= 1e-13
         slab.close()
+
+
+@pytest.mark.gpu
+def test_slab_nccl_one_rank():
+    """The NCCL exchange path (libnccl.so.2 loaded at run time, grouped
+    send/recv to self, broadcast) on a one-rank communicator equals the
+    single-GPU plan."""
+    import torch
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan, nccl_unique_id
+    cfg = get_config("c1")
+    mesh = make_mesh(cfg)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, 1, 0, nccl_unique_id())
+    x = torch.from_numpy(make_vectors(mesh.n_rwg, 3, 5)).cuda()
+    y1 = single.matvec(x)
+    yg = slab.matvec(x)
+    assert float((yg - y1).norm() / y1.norm()) <= 1e-13
+    slab.close()
+    single.close()
