@@ -76,6 +76,7 @@ static float* rounded_copy(aim_plan* p, const double* a, long long n, cudaStream
 
 void make_c64_tables(aim_plan* p, cudaStream_t s) {
     p->W32 = rounded_copy(p, p->W, p->N * p->S * 4, s);
+    p->Wc32 = rounded_copy(p, p->Wc, p->nnzP * 4, s);
     p->nval32 = (float2*)rounded_copy(p, (const double*)p->nval, 2 * p->nnzN, s);
     p->spec32 = (float2*)rounded_copy(p, (const double*)p->spec, 2 * p->spec_len, s);
 }

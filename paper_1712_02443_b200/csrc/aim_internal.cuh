@@ -155,6 +155,9 @@ struct aim_plan {
     double* W = nullptr;          // [N][S][4] weights (x, y, z, phi)
     int32_t* prow = nullptr;      // [Ng+1]
     int32_t* pent = nullptr;      // [nnzP]  n*S + u
+    int32_t* pn = nullptr;        // [nnzP]  n        (CSR order)
+    double* Wc = nullptr;         // [nnzP][4] weights in CSR order (streamed by the projection)
+    float* Wc32 = nullptr;        // [nnzP][4] complex64 plans
     int64_t* nrow = nullptr;      // [N+1]
     int32_t* ncol = nullptr;      // [nnzN]
     double2* nval = nullptr;      // [nnzN]

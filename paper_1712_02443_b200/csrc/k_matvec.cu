@@ -49,18 +49,18 @@ struct Lanes {
 
 // ------------------------------------------------------------ H1 projection
 // Q^psi[u,r] = sum_{n in col(u)} w^psi_{n,u} x[n,r]; warp per grid node.
+// The weights are read in CSR order (Wc, pn: coalesced streams), not gathered.
 template <int M, int LPE, int RPL, class C>
 __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict__ prow,
-                                                      const int32_t* __restrict__ pent,
-                                                      const Real<C>* __restrict__ W, const C* __restrict__ x,
+                                                      const int32_t* __restrict__ pn,
+                                                      const Real<C>* __restrict__ Wc, const C* __restrict__ x,
                                                       long long Ng, int R, C* __restrict__ Q) {
-    constexpr int S = (M + 1) * (M + 1) * (M + 1);
     using L = Lanes<LPE, RPL>;
     const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (g >= Ng) return;
     const L ln;
     const int e0 = prow[g], e1 = prow[g + 1];
-    const C* W2 = reinterpret_cast<const C*>(W);
+    const C* W2 = reinterpret_cast<const C*>(Wc);
     for (int r0 = 0; r0 < R; r0 += L::RC) {
         C a[4][RPL];
 #pragma unroll
@@ -71,10 +71,9 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
             int n_l = 0;
             C w01 = mkc<C>(0, 0), w23 = w01;
             if (ln.lane < cnt) {
-                const int ent = __ldg(&pent[b + ln.lane]);
-                n_l = ent / S;
-                w01 = __ldcs(W2 + 2 * (long long)ent);
-                w23 = __ldcs(W2 + 2 * (long long)ent + 1);
+                n_l = __ldcs(&pn[b + ln.lane]);
+                w01 = __ldcs(W2 + 2 * (long long)(b + ln.lane));
+                w23 = __ldcs(W2 + 2 * (long long)(b + ln.lane) + 1);
             }
 #pragma unroll kGatherUnroll
             for (int t = ln.grp; t < 32; t += L::G) {
@@ -144,8 +143,8 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
 template <class C>
 static void launch_project_t(const aim_plan* p, const C* x, C* Q, int R, cudaStream_t s) {
     const unsigned grid = nblk(p->Ng * 32, 256);
-    const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->W : (const void*)p->W32);
-#define PJ_CALL(LPE, RPL) project_kernel<MM, LPE, RPL, C><<<grid, 256, 0, s>>>(p->prow, p->pent, W, x, p->Ng, R, Q)
+    const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->Wc : (const void*)p->Wc32);
+#define PJ_CALL(LPE, RPL) project_kernel<MM, LPE, RPL, C><<<grid, 256, 0, s>>>(p->prow, p->pn, W, x, p->Ng, R, Q)
 #define PJ_M(MMV)                                   \
     if (p->M == MMV) {                              \
         constexpr int MM = MMV;                     \

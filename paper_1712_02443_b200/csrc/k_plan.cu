@@ -120,6 +120,19 @@ __global__ void proj_fill_kernel(const int32_t* __restrict__ bptr, const int32_t
             }
 }
 
+// pn[e] = n, Wc[e][0..3] = W[n][u][0..3] for entry e = n S + u
+__global__ void proj_gather_kernel(const int32_t* __restrict__ pent, long long nnz, int S,
+                                   const double* __restrict__ W, int32_t* __restrict__ pn, double* __restrict__ Wc) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int ent = pent[e];
+    pn[e] = ent / S;
+    const double2* src = reinterpret_cast<const double2*>(W) + 2 * (long long)ent;
+    double2* dst = reinterpret_cast<double2*>(Wc) + 2 * e;
+    dst[0] = src[0];
+    dst[1] = src[1];
+}
+
 void build_projection_csr(aim_plan* p, const std::vector<int32_t>& node0, cudaStream_t s) {
     const long long Ng = p->Ng;
     // counting sort of RWGs by base node (stable: ascending n inside a bucket)
@@ -158,6 +171,13 @@ void build_projection_csr(aim_plan* p, const std::vector<int32_t>& node0, cudaSt
     proj_fill_kernel<<<nblk(Ng, 256), 256, 0, s>>>(d_bptr, d_bids, p->dims[0], p->dims[1], p->dims[2], p->M,
                                                    p->prow, p->pent);
     note_launch("proj_fill");
+    // the weights in CSR order (projection streams them instead of gathering)
+    p->pn = p->alloc<int32_t>(acc);
+    p->Wc = p->alloc<double>(4 * (size_t)std::max<long long>(acc, 1));
+    if (acc) {
+        proj_gather_kernel<<<nblk(acc, 256), 256, 0, s>>>(p->pent, acc, p->S, p->W, p->pn, p->Wc);
+        note_launch("proj_gather");
+    }
     AIM_CUDA(cudaStreamSynchronize(s));
     cudaFree(d_bptr);
     cudaFree(d_bids);

@@ -446,9 +446,11 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     S->release(d_iperm);
     S->release(d_owner);
     // the full plan's per-RWG tables are no longer needed
-    for (void* ptr : {(void*)B->W, (void*)B->nval, (void*)B->ncol, (void*)B->pent, (void*)B->prow})
+    for (void* ptr : {(void*)B->W, (void*)B->nval, (void*)B->ncol, (void*)B->pent, (void*)B->prow, (void*)B->pn,
+                      (void*)B->Wc})
         B->release(ptr);
-    B->W = nullptr; B->nval = nullptr; B->ncol = nullptr; B->pent = nullptr; B->prow = nullptr;
+    B->W = nullptr; B->nval = nullptr; B->ncol = nullptr; B->pent = nullptr; B->prow = nullptr; B->pn = nullptr;
+    B->Wc = nullptr;
     if (!S->virt) {
         if (!nccl_id) throw Error(AIM_E_ARG, "rank >= 0 needs an NCCL unique id");
         ncclUniqueId id;
