@@ -188,6 +188,17 @@ struct aim_plan {
     uint32_t* nm_mask = nullptr;  // [nm_chunks][nm_mt]
     int32_t* nm_col = nullptr;    // [nm_chunks][4]
     double2* nm_val = nullptr;    // [nnzN]
+    // interpolation in 8*im_mt-row blocks for the FP64 tensor cores (complex128,
+    // R >= 8; built on first use): one chunk per union stencil node, k = component
+    int64_t im_count = 0;         // number of blocks (0 = not built)
+    int64_t im_chunks = 0;
+    int im_mt = 2;
+    int32_t* im_rows = nullptr;   // [im_count][8 im_mt]
+    int64_t* im_cptr = nullptr;   // [im_count+1]
+    int64_t* im_vptr = nullptr;   // [im_count+1] packed weight ranges (doubles)
+    int32_t* im_node = nullptr;   // [im_chunks] grid node index
+    uint32_t* im_mask = nullptr;  // [im_chunks][im_mt]
+    double* im_val = nullptr;     // packed weights, phi scaled by -1/k^2
     int planar = 0;               // 1: z handled by direct convolution (spec = G2)
     double2* spec = nullptr;      // 3-D: [(Px/2+1)(Py/2+1)(Pz/2+1)]; planar: [(Px/2+1)(Py/2+1)][Nz]
     int64_t spec_len = 0;
@@ -262,12 +273,13 @@ void build_near_values(aim_plan* p, cudaStream_t s);
 void build_green_spectrum(aim_plan* p, cudaStream_t s);
 void build_near_blocks(aim_plan* p, cudaStream_t s);
 void build_near_mma(aim_plan* p, cudaStream_t s);
+void build_interp_mma(aim_plan* p, cudaStream_t s);
 void make_c64_blocks(aim_plan* p, cudaStream_t s);   // rounded nb_val for AIM_C64 plans
 
 // ---- matvec launches (k_matvec.cu)
 // x, y, Q, Phi are complex128 (double2) or complex64 (float2) by plan->prec
 void launch_project(const aim_plan* p, const void* x, void* Q, int R, cudaStream_t s);
-void launch_interp(const aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s);
+void launch_interp(aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s);
 void launch_near(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
 void launch_planewave(const aim_plan* p, const double* khat, const double* pol, double2 E0, double2* V,
                       cudaStream_t s);

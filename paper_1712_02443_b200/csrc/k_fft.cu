@@ -14,6 +14,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -357,6 +358,168 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
         ckx = lkx; cc = lc; cch = lch;
         advance();
         C* tmp = X;
+        X = Z;
+        Z = tmp;
+        __syncthreads();
+    }
+}
+
+// Four-step planar y/z pass (complex128, Py = N1 N2): every half-warp owns one
+// z line of the (kx, component, rhs) tile and transforms it in registers,
+//   forward  step 1: lane n2 < N2: DFT_N1 over x[N2 n1 + n2], x w^(n2 k1) -> row N2 k1 + n2
+//            step 2: lane k1 < N1: DFT_N2 over rows N2 k1 + n2       -> X[k1 + N1 k2]
+// (each step reads and writes only the half-warp's own column of the [y][z]
+// tile; __syncwarp separates the steps), then the CTA-wide z Toeplitz x G2
+// (spectrum slice of this kx staged in shared memory), then the same two steps
+// with conjugate twiddles and the pruned output (y < Ny) stored straight from
+// registers.  Versus the Stockham stage kernel: 2 register passes instead of 3
+// shared-memory stages per direction and no CTA barrier inside the FFTs.
+// Persistent CTAs; the next tile is fetched by cp.async into a second buffer.
+template <int NZ, int N1, int N2>
+__global__ void __launch_bounds__(32 * ((NZ + 1) / 2), 2) planar4_kernel(PlanarPass p, int tiles) {
+    constexpr int Py = N1 * N2, NW = (NZ + 1) / 2, T = 32 * NW;
+    constexpr int PyH = Py / 2 + 1;
+    static_assert(N1 <= 16 && N2 <= 16, "register radices");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* bufA = reinterpret_cast<double2*>(smraw);
+    double2* bufB = bufA + Py * NZ;
+    double2* g2s = bufB + Py * NZ;        // [PyH][NZ] spectrum slice of the current kx
+    double2* tws = g2s + PyH * NZ;        // [Py] exp(-2 pi i e / Py)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int z = 2 * w + (lane >> 4), h = lane & 15;
+    const bool zl = z < NZ;
+    const int nchunk = p.R;
+    const int ystride = NZ * p.R;
+    for (int e = threadIdx.x; e < Py; e += T) tws[e] = p.ay.tw[e];
+    int t0, t1;
+    tile_range(tiles, t0, t1);
+    if (t0 >= t1) return;
+    int lkx = t0 / (4 * nchunk), lc = (t0 / nchunk) % 4, lch = t0 % nchunk;
+    auto base_of = [&](int kx, int c, int r) -> double2* {
+        const long long plane = (long long)c * p.Px + kx;
+        return ((double2*)p.W) + plane * p.Ny * ystride + r;   // + y * ystride + z * R
+    };
+    // tile load: [y][z] rows, zero rows y >= Ny (the padding), coalesced over z
+    auto issue = [&](double2* buf) {
+        const double2* src = base_of(lkx, lc, lch);
+        for (int e = threadIdx.x; e < Py * NZ; e += T) {
+            const int yy = e / NZ, zz = e - (e / NZ) * NZ;
+            const bool v = yy < p.Ny;
+            cp_async_c(&buf[e], v ? src + (long long)yy * ystride + zz * p.R : (const double2*)p.W, v);
+        }
+    };
+    auto advance = [&]() {
+        if (++lch == nchunk) {
+            lch = 0;
+            if (++lc == 4) { lc = 0; ++lkx; }
+        }
+    };
+    double2* X = bufA;
+    double2* Z = bufB;
+    issue(X);
+    cp_commit();
+    int ckx = lkx, cc = lc, cch = lch;
+    int g2kx = -1;
+    advance();
+    for (int t = t0; t < t1; ++t) {
+        if (t + 1 < t1) issue(Z);
+        cp_commit();
+        const int kg = ckx + p.off;
+        const int ax_ = min(kg, p.Pfold - kg);
+        if (ax_ != g2kx) {   // stage the spectrum slice of this kx (uniform across the CTA)
+            const double2* g2 = ((const double2*)p.spec) + (long long)ax_ * PyH * NZ;
+            for (int e = threadIdx.x; e < PyH * NZ; e += T) g2s[e] = __ldg(&g2[e]);
+            g2kx = ax_;
+        }
+        cp_wait_prev();
+        __syncthreads();
+        double2* col = X + z;   // this half-warp's column: element y at col[y * NZ]
+        // ---- forward, step 1
+        if (zl && h < N2) {
+            double2 a[N1];
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) a[n1] = col[(N2 * n1 + h) * NZ];
+            dft<N1>(a, -1.0);
+#pragma unroll
+            for (int k1 = 1; k1 < N1; ++k1) a[k1] = cmul(a[k1], tws[h * k1]);
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) col[(N2 * k1 + h) * NZ] = a[k1];
+        }
+        __syncwarp();
+        // ---- forward, step 2
+        {
+            double2 b[N2];
+            const bool act = zl && h < N1;
+            if (act) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) b[n2] = col[(N2 * h + n2) * NZ];
+                dft<N2>(b, -1.0);
+            }
+            __syncwarp();
+            if (act) {
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) col[(h + N1 * k2) * NZ] = b[k2];
+            }
+        }
+        __syncthreads();
+        // ---- z Toeplitz against G2(kx, ky, |dz|)
+        for (int ky = threadIdx.x; ky < Py; ky += T) {
+            const int ay = min(ky, Py - ky);
+            const double2* g = g2s + ay * NZ;
+            double2* row = X + ky * NZ;
+            double2 gk[NZ], in[NZ];
+#pragma unroll
+            for (int d = 0; d < NZ; ++d) gk[d] = g[d];
+#pragma unroll
+            for (int zz = 0; zz < NZ; ++zz) in[zz] = row[zz];
+#pragma unroll
+            for (int zz = 0; zz < NZ; ++zz) {
+                double2 acc = cmul(gk[0], in[zz]);
+#pragma unroll
+                for (int d = 1; d < NZ; ++d) {
+                    if (zz - d < 0 && zz + d >= NZ) continue;
+                    double2 sum = zz - d >= 0 ? in[zz - d] : make_double2(0.0, 0.0);
+                    if (zz + d < NZ) sum = zz - d >= 0 ? cadd(sum, in[zz + d]) : in[zz + d];
+                    const double2 gd = gk[d];
+                    acc.x = fma(gd.x, sum.x, fma(-gd.y, sum.y, acc.x));
+                    acc.y = fma(gd.x, sum.y, fma(gd.y, sum.x, acc.y));
+                }
+                row[zz] = acc;
+            }
+        }
+        __syncthreads();
+        // ---- inverse, step 1
+        if (zl && h < N2) {
+            double2 a[N1];
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) a[n1] = col[(N2 * n1 + h) * NZ];
+            dft<N1>(a, +1.0);
+#pragma unroll
+            for (int k1 = 1; k1 < N1; ++k1) {
+                double2 tw = tws[h * k1];
+                tw.y = -tw.y;
+                a[k1] = cmul(a[k1], tw);
+            }
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) col[(N2 * k1 + h) * NZ] = a[k1];
+        }
+        __syncwarp();
+        // ---- inverse, step 2 and the pruned store (y = k1 + N1 k2 < Ny)
+        if (zl && h < N1) {
+            double2 b[N2];
+#pragma unroll
+            for (int n2 = 0; n2 < N2; ++n2) b[n2] = col[(N2 * h + n2) * NZ];
+            dft<N2>(b, +1.0);
+            double2* dst = base_of(ckx, cc, cch) + z * p.R;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                const int yy = h + N1 * k2;
+                if (yy < p.Ny) __stcs(dst + (long long)yy * ystride, b[k2]);
+            }
+        }
+        ckx = lkx; cc = lc; cch = lch;
+        advance();
+        double2* tmp = X;
         X = Z;
         Z = tmp;
         __syncthreads();
@@ -734,8 +897,30 @@ static bool try_ct_planar(PlanarPass p, cudaStream_t s) {
     return true;
 }
 
+template <int NZ, int N1, int N2>
+static bool try_planar4(const PlanarPass& p, cudaStream_t s) {
+    constexpr int Py = N1 * N2;
+    if (p.ay.P != Py || p.Nz != NZ || p.PyH != Py / 2 + 1) return false;
+    const long long tiles = 4LL * p.Px * p.R;
+    const size_t smem = sizeof(double2) * ((size_t)2 * Py * NZ + (Py / 2 + 1) * NZ + Py);
+    auto kern = planar4_kernel<NZ, N1, N2>;
+    constexpr int T = 32 * ((NZ + 1) / 2);
+    ensure_smem_attr(kern);
+    const long long grid = persistent_grid(kern, T, smem, tiles);
+    kern<<<(unsigned)grid, T, smem, s>>>(p, (int)tiles);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(AIM_E_CUDA, std::string("planar4_kernel: ") + cudaGetErrorString(e));
+    return true;
+}
+
 template <class C>
 static void launch_planar_yz_t(PlanarPass p, cudaStream_t s) {
+    if constexpr (sizeof(C) == 16) {
+        // four-step register kernel (AIM_PLANAR_KERNEL=stockham forces the stage kernel, A/B timing only)
+        const char* e = getenv("AIM_PLANAR_KERNEL");
+        if (!(e && !strcmp(e, "stockham")) && (try_planar4<11, 14, 15>(p, s) || try_planar4<7, 4, 6>(p, s)))
+            return;
+    }
     if (try_ct_planar<C, 11, Ct210z11, 2>(p, s) || try_ct_planar<C, 7, Ct24z7, 2>(p, s)) return;
     const int Py = p.ay.P;
     const int rc_fft = (int)(kPlanarThreads * (long long)p.ay.min_radix / ((long long)Py * p.Nz));

@@ -562,8 +562,167 @@ __global__ void __launch_bounds__(32 * kNmWarps) near_mma_kernel(const int32_t* 
     }
 }
 
+// ------------------------------ H5 interpolation on the FP64 tensor cores
+// y[m, r] += j k eta0 sum_{u, comp} w'[m, u, comp] Phi[comp][g(m, u)][r] (w'_phi =
+// -w_phi / k^2) as a block-sparse product (build_interp_mma): warp per block of
+// 8*MT RWGs, one chunk per union stencil node, the 4 components are the k
+// extent of mma.m8n8k4.f64.  A = real weights (lane l: row l/4, comp l%4, bit l
+// of the chunk mask, packed value popc(mask below l)); B = Phi[comp][node][8 RHS]
+// (lane l: comp l%4, RHS l/4): real and imaginary parts are two MMAs.  The same
+// per-lane cp.async ring as near_mma_kernel; a node index per chunk and MT
+// masks, windows of 8 chunks handed out by shuffles.
+__device__ __forceinline__ void cpa8_ca(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+template <int MT, int NT>
+constexpr size_t interp_mma_smem() { return sizeof(double2) * kNmWarps * kNmDepth * (MT + NT) * 32; }
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(32 * kNmWarps) interp_mma_kernel(const int32_t* __restrict__ rows,
+                                                                const int64_t* __restrict__ cptr,
+                                                                const int64_t* __restrict__ vptr,
+                                                                const uint32_t* __restrict__ cmask,
+                                                                const int32_t* __restrict__ cnode,
+                                                                const double* __restrict__ val,
+                                                                const double2* __restrict__ Phi, long long Ng,
+                                                                long long nblk, int R, double keta,
+                                                                double2* __restrict__ y) {
+    constexpr int D = kNmDepth, W = 8, SL = (MT + NT) * 32;
+    static_assert(D >= 1 && D <= W, "ring depth");
+    extern __shared__ __align__(16) double2 nm_sm[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const long long b = (long long)blockIdx.x * kNmWarps + wid;
+    if (b >= nblk) return;
+    double2* ring = nm_sm + (size_t)wid * D * SL + lane;
+    const uint32_t below = (1u << lane) - 1u;
+    const int c0 = (int)cptr[b], c1 = (int)cptr[b + 1];
+    auto meta = [&](int w, int& nodew, uint32_t& mw) {
+        nodew = (lane < W && w + lane < c1) ? __ldcs(&cnode[w + lane]) : -1;
+        mw = (lane < W * MT && MT * w + lane < MT * c1) ? __ldcs(&cmask[MT * w + lane]) : 0u;
+    };
+    for (int r0 = 0; r0 < R; r0 += 8 * NT) {
+        // lane's B column: component t, rhs r0 + 8 n + g
+        const double2* ph = Phi + (long long)t * Ng * R + r0 + g;
+        int vo = (int)vptr[b];
+        auto issue = [&](int nodew, uint32_t mw, int j, int slot) {
+            const int node = __shfl_sync(0xffffffffu, nodew, j);
+            double2* sl = ring + slot * SL;
+#pragma unroll
+            for (int q = 0; q < MT; ++q) {
+                const uint32_t m = __shfl_sync(0xffffffffu, mw, MT * j + q);
+                if (m >> lane & 1u) cpa8_ca(sl + q * 32, val + vo + __popc(m & below));
+                else sl[q * 32].x = 0.0;
+                vo += __popc(m);
+            }
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                if (node >= 0 && r0 + 8 * n + g < R) cpa16_ca(sl + (MT + n) * 32, ph + ((long long)node * R + 8 * n));
+                else sl[(MT + n) * 32] = make_double2(0.0, 0.0);
+            }
+            cpa_commit();
+        };
+        double Yr[MT][NT][2], Yi[MT][NT][2];
+#pragma unroll
+        for (int q = 0; q < MT; ++q)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) Yr[q][n][i] = Yi[q][n][i] = 0.0;
+        int nw, nw_n;
+        uint32_t mw, mw_n;
+        meta(c0, nw, mw);
+        meta(c0 + W, nw_n, mw_n);
+#pragma unroll
+        for (int u = 0; u < D; ++u) issue(nw, mw, u, u);
+        for (int w = c0; w < c1; w += W) {
+            int nw_nn;
+            uint32_t mw_nn;
+            meta(w + 2 * W, nw_nn, mw_nn);
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                cpa_wait<D - 1>();
+                const double2* sl = ring + (u % D) * SL;
+                double a[MT];
+                double2 xv[NT];
+#pragma unroll
+                for (int q = 0; q < MT; ++q) a[q] = sl[q * 32].x;
+#pragma unroll
+                for (int n = 0; n < NT; ++n) xv[n] = sl[(MT + n) * 32];
+                if (u + D < W) issue(nw, mw, u + D, u % D);
+                else issue(nw_n, mw_n, u + D - W, u % D);
+#pragma unroll
+                for (int n = 0; n < NT; ++n)
+#pragma unroll
+                    for (int q = 0; q < MT; ++q) {
+                        dmma(Yr[q][n][0], Yr[q][n][1], a[q], xv[n].x);
+                        dmma(Yi[q][n][0], Yi[q][n][1], a[q], xv[n].y);
+                    }
+            }
+            nw = nw_n;
+            mw = mw_n;
+            nw_n = nw_nn;
+            mw_n = mw_nn;
+        }
+        cpa_wait<0>();
+#pragma unroll
+        for (int q = 0; q < MT; ++q) {
+            const int row = rows[8 * MT * b + 8 * q + g];
+            if (row < 0) continue;
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int rr = r0 + 8 * n + 2 * t + i;
+                    if (rr < R) {
+                        double2* yp = y + (long long)row * R + rr;
+                        const double2 o = *yp;   // near rows written before (accumulate)
+                        *yp = make_double2(o.x - keta * Yi[q][n][i], o.y + keta * Yr[q][n][i]);
+                    }
+                }
+        }
+    }
+}
+
+// The tensor-core interpolation is opt-in (AIM_INTERP_KERNEL=mma, complex128,
+// R >= 8, accumulating onto the near rows): measured on C2 it is slower than
+// the gather kernel (0.253 vs 0.233 ms; chunk fill 0.26 at 16 rows), so the
+// gather kernel is the default.
+constexpr int kInterpMmaRhs = 8;
+
 template <class C>
-static void launch_interp_t(const aim_plan* p, const C* Phi, C* y, int R, bool accumulate, cudaStream_t s) {
+static void launch_interp_t(aim_plan* p, const C* Phi, C* y, int R, bool accumulate, cudaStream_t s) {
+    if constexpr (sizeof(C) == 16) {
+        const char* e = getenv("AIM_INTERP_KERNEL");
+        if (R >= kInterpMmaRhs && accumulate && e && !strcmp(e, "mma")) {
+            if (p->N * (long long)R >= (1LL << 31) || p->Ng * 4LL * R >= (1LL << 40))
+                throw Error(AIM_E_ARG, "interp_mma: index range");
+            build_interp_mma(p, s);
+            const double keta = p->k * eta0();
+#define IM_CALL(MT, NT)                                                                                            \
+    {                                                                                                              \
+        static bool attr = false;                                                                                  \
+        if (!attr) {                                                                                               \
+            AIM_CUDA(cudaFuncSetAttribute(interp_mma_kernel<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                          (int)interp_mma_smem<MT, NT>()));                                        \
+            attr = true;                                                                                           \
+        }                                                                                                          \
+        interp_mma_kernel<MT, NT><<<nblk(p->im_count, kNmWarps), 32 * kNmWarps, interp_mma_smem<MT, NT>(), s>>>(   \
+            p->im_rows, p->im_cptr, p->im_vptr, p->im_mask, p->im_node, p->im_val, (const double2*)Phi, p->Ng,     \
+            p->im_count, R, keta, (double2*)y);                                                                    \
+    }
+            if (p->im_mt == 1) {
+                if (R <= 8) IM_CALL(1, 1)
+                else IM_CALL(1, 2)
+            } else {
+                if (R <= 8) IM_CALL(2, 1)
+                else IM_CALL(2, 2)
+            }
+#undef IM_CALL
+            return;
+        }
+    }
     const unsigned grid = nblk(p->N * 32, 256);
     const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
     const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->W : (const void*)p->W32);
@@ -582,7 +741,7 @@ static void launch_interp_t(const aim_plan* p, const C* Phi, C* y, int R, bool a
     throw Error(AIM_E_ARG, "unsupported M");
 }
 
-void launch_interp(const aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s) {
+void launch_interp(aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s) {
     if (p->prec == AIM_C64) launch_interp_t(p, (const float2*)Phi, (float2*)y, R, accumulate, s);
     else launch_interp_t(p, (const double2*)Phi, (double2*)y, R, accumulate, s);
     note_launch("interp");

@@ -508,6 +508,100 @@ void build_near_mma(aim_plan* p, cudaStream_t s) {
     p->nm_count = nblk;
 }
 
+// --------------------------------- interpolation, 8*MT-row blocks for FP64 MMA
+// H5 as a block-sparse product y = jk eta0 W Phi: rows = 8*MT Morton-consecutive
+// RWGs, columns = the sorted union of their stencil nodes; one chunk per node
+// whose 4 k-columns are the components (x, y, z, phi).  Chunk c stores the
+// node index and MT masks (bit 4i + comp: row 8q + i touches the node); the
+// present weights are packed in mask order, the phi weight pre-scaled by
+// -1/k^2, so y = jk eta0 sum_k A B.  Built on the host once (first
+// multi-RHS interpolation).
+void build_interp_mma(aim_plan* p, cudaStream_t s) {
+    if (p->im_count) return;
+    const long long N = p->N;
+    const int M1 = p->M + 1, S = p->S, Ny = p->dims[1], Nz = p->dims[2];
+    const char* e = getenv("AIM_INTERP_RB");
+    const int MT = (e && atoi(e) == 8) ? 1 : 2;
+    const int RB = 8 * MT;
+    const std::vector<int32_t> rows = morton_rows(p, RB);
+    const long long nblk = (long long)rows.size() / RB;
+    std::vector<int32_t> node0(N);
+    std::vector<double> W((size_t)N * S * 4);
+    AIM_CUDA(cudaStreamSynchronize(s));
+    AIM_CUDA(cudaMemcpy(node0.data(), p->node0, sizeof(int32_t) * N, cudaMemcpyDeviceToHost));
+    AIM_CUDA(cudaMemcpy(W.data(), p->W, sizeof(double) * W.size(), cudaMemcpyDeviceToHost));
+    const double ik2 = 1.0 / (p->k * p->k);
+    std::vector<int64_t> cptr(nblk + 1, 0), vptr(nblk + 1, 0);
+    std::vector<int32_t> cnode;
+    std::vector<uint32_t> cmask;
+    std::vector<double> cval;
+    cnode.reserve(N * 8);
+    cval.reserve((size_t)N * S * 4);
+    std::vector<int32_t> nodes;
+    auto coords = [&](long long g, int& x, int& y, int& z) {
+        z = (int)(g % Nz);
+        y = (int)((g / Nz) % Ny);
+        x = (int)(g / ((long long)Ny * Nz));
+    };
+    for (long long b = 0; b < nblk; ++b) {
+        nodes.clear();
+        for (int i = 0; i < RB; ++i) {
+            const int r = rows[RB * b + i];
+            if (r < 0) continue;
+            int bx, by, bz;
+            coords(node0[r], bx, by, bz);
+            for (int u = 0; u < S; ++u) {
+                const int ux = u / (M1 * M1), uy = (u / M1) % M1, uz = u % M1;
+                nodes.push_back((int32_t)(((long long)(bx + ux) * Ny + (by + uy)) * Nz + (bz + uz)));
+            }
+        }
+        std::sort(nodes.begin(), nodes.end());
+        nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+        for (int32_t g : nodes) {
+            int gx, gy, gz;
+            coords(g, gx, gy, gz);
+            cnode.push_back(g);
+            for (int q = 0; q < MT; ++q) {
+                uint32_t m = 0;
+                for (int i = 0; i < 8; ++i) {
+                    const int r = rows[RB * b + 8 * q + i];
+                    if (r < 0) continue;
+                    int bx, by, bz;
+                    coords(node0[r], bx, by, bz);
+                    const int dx = gx - bx, dy = gy - by, dz = gz - bz;
+                    if (dx < 0 || dx > p->M || dy < 0 || dy > p->M || dz < 0 || dz > p->M) continue;
+                    const int u = (dx * M1 + dy) * M1 + dz;
+                    m |= 0xFu << (4 * i);
+                    const double* w = &W[((size_t)r * S + u) * 4];
+                    cval.push_back(w[0]);
+                    cval.push_back(w[1]);
+                    cval.push_back(w[2]);
+                    cval.push_back(-w[3] * ik2);
+                }
+                cmask.push_back(m);
+            }
+        }
+        cptr[b + 1] = (int64_t)cnode.size();
+        vptr[b + 1] = (int64_t)cval.size();
+    }
+    if ((long long)cval.size() >= (1LL << 31)) throw Error(AIM_E_GRID, "interp_mma: packed weights exceed 2^31");
+    p->im_mt = MT;
+    p->im_chunks = (int64_t)cnode.size();
+    p->im_rows = p->alloc<int32_t>(rows.size());
+    p->im_cptr = p->alloc<int64_t>(nblk + 1);
+    p->im_vptr = p->alloc<int64_t>(nblk + 1);
+    p->im_node = p->alloc<int32_t>(cnode.size());
+    p->im_mask = p->alloc<uint32_t>(cmask.size());
+    p->im_val = p->alloc<double>(cval.size());
+    h2d(p->im_rows, rows.data(), sizeof(int32_t) * rows.size(), s);
+    h2d(p->im_cptr, cptr.data(), sizeof(int64_t) * (nblk + 1), s);
+    h2d(p->im_vptr, vptr.data(), sizeof(int64_t) * (nblk + 1), s);
+    h2d(p->im_node, cnode.data(), sizeof(int32_t) * cnode.size(), s);
+    h2d(p->im_mask, cmask.data(), sizeof(uint32_t) * cmask.size(), s);
+    h2d(p->im_val, cval.data(), sizeof(double) * cval.size(), s);
+    p->im_count = nblk;
+}
+
 void build_near_blocks(aim_plan* p, cudaStream_t s) {
     if (p->nb_count) return;
     const std::vector<int32_t> rows = morton_rows(p, 4);

@@ -287,3 +287,31 @@ def test_near_kernels_all_rhs_counts(name, rb, monkeypatch):
         monkeypatch.delenv("AIM_NEAR_KERNEL")
         assert rel(outs["mma"], outs["csr"]) <= 1e-14
     G.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "t_m3", "t_dissim"])
+@pytest.mark.parametrize("rb", [8, 16])
+def test_interp_mma_kernel(name, rb, monkeypatch):
+    """H5 interpolation on the FP64 tensor cores (opt-in AIM_INTERP_KERNEL=mma;
+    complex128, R >= 8, blocks of 8 or 16 RWGs, one chunk per union stencil
+    node) accumulated onto the near rows: equal to the default gather kernel
+    and to the oracle's P^T Phi + Z_corr x."""
+    from paper_1712_02443_b200 import AimPlan
+    cfg = get_config(name)
+    O = oracle_plan(name)
+    monkeypatch.setenv("AIM_INTERP_RB", str(rb))
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    Z = O.near_full()
+    for nrhs in (8, 9, 16, 33):
+        x = make_vectors(O.N, nrhs, 5)
+        xt = torch.from_numpy(x).cuda()
+        Q = G.project(xt).contiguous()
+        Phi = G.convolve(Q).contiguous()
+        monkeypatch.setenv("AIM_INTERP_KERNEL", "mma")
+        y_mma = G.interpolate(Phi, xt, add_near=True).cpu().numpy()
+        monkeypatch.delenv("AIM_INTERP_KERNEL")
+        y_g = G.interpolate(Phi, xt, add_near=True).cpu().numpy()
+        assert rel(y_mma, y_g) <= 1e-13, nrhs
+        ref = O.interpolate(Phi.cpu().numpy()) + Z @ x
+        assert rel(y_mma, ref) <= 1e-12, nrhs
+    G.close()
