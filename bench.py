@@ -55,7 +55,7 @@ def alg_bytes(info, R):
     nnzP, nnzN = info["nnz_proj"], info["nnz_near"]
     Px, Py, Pz = info["fft_dims"]
     Nx, Ny, Nz = info["grid_dims"]
-    spec = 16 * (Px // 2 + 1) * (Py // 2 + 1) * (Nz if info["conv_mode"] == 1 else Pz // 2 + 1)
+    spec = 16 * (Px // 2 + 1) * (Py // 2 + 1) * (Nz if info["conv_mode"] != 0 else Pz // 2 + 1)
     matvec = (16 * N * R + 36 * nnzP + 4 * (Ng + 1) + 4 * 64 * Ng * R + spec
               + 32 * nnzP + 4 * N + 20 * nnzN + 4 * (N + 1) + 16 * N * R)
     grid = 64 * Ng * R                                   # one 4-component grid, R RHS

@@ -74,7 +74,11 @@ typedef struct aim_info {
     int32_t conv_mode;      /* 0: 3-D FFT convolution, spectrum octant
                                [(Px/2+1)][(Py/2+1)][(Pz/2+1)];
                                1: planar -- 2-D FFT in x,y and direct Toeplitz
-                               product in z, spectrum [(Px/2+1)][(Py/2+1)][Nz]  */
+                               product in z, spectrum [(Px/2+1)][(Py/2+1)][Nz],
+                               y passes and z product fused in one kernel;
+                               2: planar with separate y passes and a z
+                               Toeplitz kernel (same spectrum; grids whose
+                               Py x Nz plane does not fit shared memory)      */
     int32_t precision;      /* AIM_C128 or AIM_C64                               */
 } aim_info;
 
@@ -217,7 +221,7 @@ int aim_profile_read(aim_plan* plan, double* ms, int64_t* count);
  * [X[r], X[r+1]), balanced by the number of RWGs whose stencil base x index
  * (D3) lies in them, each at least M planes wide; rank r owns those RWGs
  * (near rows, weights) and the grid planes [X[r], X[r+1] + M).  Planar grids
- * (aim_info.conv_mode == 1) only. */
+ * (aim_info.conv_mode 1 or 2) and 3-D grids (conv_mode 0). */
 typedef struct aim_slab aim_slab; /* opaque */
 
 /* Host only (no device work): the partition of `world` slabs.
@@ -245,8 +249,8 @@ int aim_nccl_unique_id(void* id, int64_t bytes);
  * rank < 0 (nccl_id ignored): all `world` slabs on the current GPU in this
  *   process, exchanges as device copies with the same packing (checks the
  *   decomposition on one device).
- * Errors: as aim_plan_create; AIM_E_ARG also for a non-planar grid or
- * world * M > Nx; AIM_E_NCCL.  Synchronous.
+ * Errors: as aim_plan_create; AIM_E_ARG also for world * M > Nx;
+ * AIM_E_NCCL.  Synchronous.
  */
 int aim_slab_create(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt,
                     const int32_t* rwg_edges, int64_t n_rwg, double k, double h, int32_t M,

@@ -199,7 +199,7 @@ class AimPlan:
             "near_rowptr": (np.int64, (N + 1,)), "near_col": (np.int32, (inf["nnz_near"],)),
             "near_val": (np.complex128, (inf["nnz_near"],)),
             "green": (np.complex128, (Px // 2 + 1, Py // 2 + 1,
-                                      inf["grid_dims"][2] if inf["conv_mode"] == 1 else Pz // 2 + 1)),
+                                      inf["grid_dims"][2] if inf["conv_mode"] != 0 else Pz // 2 + 1)),
             "proj_rowptr": (np.int32, (inf["n_nodes"] + 1,)), "proj_ent": (np.int32, (inf["nnz_proj"],)),
         }
         dt, sh = shapes[what]

@@ -197,9 +197,15 @@ void create_plan(const double* V, int64_t nv, const int32_t* T, int64_t nt, cons
     p->base = upload(p, base);
     p->node0 = upload(p, node0);
     for (int d = 0; d < 3; ++d) make_fft_axis(p->pads[d], p->ax[d]);
-    p->planar = planar_supported(p->pads[1], p->dims[2], p->ax[1].min_radix) ? 1 : 0;
-    // AIM_CONV_MODE=0 in the environment forces the 3-D FFT convolution (tests of that path on small grids)
-    if (getenv("AIM_CONV_MODE") && getenv("AIM_CONV_MODE")[0] == '0') p->planar = 0;
+    // conv mode: 1 = fused planar y/z kernel (the Py x Nz plane fits shared memory),
+    // 2 = thin grid with long lines: separate y passes around a z Toeplitz kernel,
+    // 0 = 3-D FFT convolution.  AIM_CONV_MODE=0|1|2 forces one (tests on small grids).
+    p->planar = planar_supported(p->pads[1], p->dims[2], p->ax[1].min_radix) ? 1
+              : (p->dims[2] <= kPlanarMaxNz ? 2 : 0);
+    if (const char* cm = getenv("AIM_CONV_MODE")) {
+        if (cm[0] == '0') p->planar = 0;
+        else if (cm[0] == '2' && p->dims[2] <= kPlanarMaxNz) p->planar = 2;
+    }
 
     // ---- device setup S2-S4
     cudaStream_t s = p->stream;

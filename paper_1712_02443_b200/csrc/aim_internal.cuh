@@ -120,6 +120,10 @@ struct PlanarPass {
 
 void launch_fft_pass(const FftPass& p, cudaStream_t s);
 void launch_planar_yz(const PlanarPass& p, cudaStream_t s);
+// z Toeplitz x G2 in place on lines [4][A][B][Nz][R]: (kx, ky) = (a, b) if kx_is_a
+// else (b + 0, a + off) -- the second form serves the slab path's ky pencils
+void launch_ztoeplitz(void* W, int prec, int A, int B, int Nz, int R, int kx_is_a, int off, int Px, int Py,
+                      const void* spec, cudaStream_t s);
 bool planar_supported(int Py, int Nz, int min_radix);
 void make_fft_axis(int P, FftAxis& ax);    // factorisation + device twiddles
 int smooth_size_at_least(int n);           // smallest 2^a 3^b 5^c 7^d >= n
@@ -199,7 +203,8 @@ struct aim_plan {
     int32_t* im_node = nullptr;   // [im_chunks] grid node index
     uint32_t* im_mask = nullptr;  // [im_chunks][im_mt]
     double* im_val = nullptr;     // packed weights, phi scaled by -1/k^2
-    int planar = 0;               // 1: z handled by direct convolution (spec = G2)
+    int planar = 0;               // conv mode: 1 fused planar, 2 planar with separate passes (both
+                                  // spec = G2, z by direct Toeplitz), 0 3-D FFT (spec = octant)
     double2* spec = nullptr;      // 3-D: [(Px/2+1)(Py/2+1)(Pz/2+1)]; planar: [(Px/2+1)(Py/2+1)][Nz]
     int64_t spec_len = 0;
     aim::FftAxis ax[3];

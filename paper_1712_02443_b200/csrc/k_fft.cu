@@ -375,9 +375,10 @@ __global__ void __launch_bounds__(F::T, MINB) planar_ct_kernel(PlanarPass p, int
 // registers.  Versus the Stockham stage kernel: 2 register passes instead of 3
 // shared-memory stages per direction and no CTA barrier inside the FFTs.
 // Persistent CTAs; the next tile is fetched by cp.async into a second buffer.
-template <int NZ, int N1, int N2>
-__global__ void __launch_bounds__(32 * ((NZ + 1) / 2), 2) planar4_kernel(PlanarPass p, int tiles) {
-    constexpr int Py = N1 * N2, NW = (NZ + 1) / 2, T = 32 * NW;
+template <int NZ, int N1, int N2, int NW>
+__global__ void __launch_bounds__(32 * NW, 2) planar4_kernel(PlanarPass p, int tiles) {
+    constexpr int Py = N1 * N2, T = 32 * NW;
+    static_assert(2 * NW >= NZ, "one z line per half-warp");
     constexpr int PyH = Py / 2 + 1;
     static_assert(N1 <= 16 && N2 <= 16, "register radices");
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -659,6 +660,67 @@ __global__ void __launch_bounds__(MAXT, MINB) planar_yz_kernel(PlanarPass p, int
     }
 }
 
+// ------------------------------------------------------- z Toeplitz (mode 2)
+// Thread per z line (component, a, b, rhs) of W[4][A][B][NZ][R]:
+//   out[z] = sum_z' G2(kx, ky, |z - z'|) in[z'],  symmetric form
+//   out[z] = g0 in[z] + sum_{d>0} g_d (in[z-d] + in[z+d]).
+// The line's NZ values are one contiguous run for R = 1 (the GMRES case).
+template <int NZ, class C>
+__global__ void __launch_bounds__(128) ztoeplitz_kernel(C* __restrict__ W, long long lines, int A, int B, int R,
+                                                        int kx_is_a, int off, int Px, int Py,
+                                                        const C* __restrict__ spec) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= lines) return;
+    const int r = (int)(t % R);
+    long long q = t / R;
+    const int b = (int)(q % B);
+    q /= B;
+    const int a = (int)(q % A);
+    const int c = (int)(q / A);
+    const int kx = kx_is_a ? a : b, ky = kx_is_a ? b + off : a + off;
+    const int ax_ = min(kx, Px - kx), ay = min(ky, Py - ky);
+    const C* g = spec + ((long long)ax_ * (Py / 2 + 1) + ay) * NZ;
+    C* row = W + (((long long)c * A + a) * B + b) * NZ * R + r;
+    C in[NZ];
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) in[z] = row[(long long)z * R];
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) {
+        C acc = cmul(__ldg(&g[0]), in[z]);
+#pragma unroll
+        for (int d = 1; d < NZ; ++d) {
+            if (z - d < 0 && z + d >= NZ) continue;
+            C sum = z - d >= 0 ? in[z - d] : mkc<C>(0, 0);
+            if (z + d < NZ) sum = z - d >= 0 ? cadd(sum, in[z + d]) : in[z + d];
+            const C gd = __ldg(&g[d]);
+            acc.x = fma(gd.x, sum.x, fma(-gd.y, sum.y, acc.x));
+            acc.y = fma(gd.x, sum.y, fma(gd.y, sum.x, acc.y));
+        }
+        __stcs(&row[(long long)z * R], acc);
+    }
+}
+
+template <class C>
+static void launch_ztoeplitz_t(C* W, int A, int B, int Nz, int R, int kx_is_a, int off, int Px, int Py,
+                               const C* spec, cudaStream_t s) {
+    const long long lines = 4LL * A * B * R;
+    if (lines <= 0) return;
+    const unsigned grid = (unsigned)((lines + 127) / 128);
+    switch (Nz) {
+#define ZT(NZ) case NZ: ztoeplitz_kernel<NZ, C><<<grid, 128, 0, s>>>(W, lines, A, B, R, kx_is_a, off, Px, Py, spec); break;
+        ZT(1) ZT(2) ZT(3) ZT(4) ZT(5) ZT(6) ZT(7) ZT(8) ZT(9) ZT(10) ZT(11) ZT(12) ZT(13) ZT(14) ZT(15) ZT(16)
+#undef ZT
+        default: throw Error(AIM_E_GRID, "z Toeplitz: Nz out of range");
+    }
+}
+
+void launch_ztoeplitz(void* W, int prec, int A, int B, int Nz, int R, int kx_is_a, int off, int Px, int Py,
+                      const void* spec, cudaStream_t s) {
+    if (prec == 1) launch_ztoeplitz_t((float2*)W, A, B, Nz, R, kx_is_a, off, Px, Py, (const float2*)spec, s);
+    else launch_ztoeplitz_t((double2*)W, A, B, Nz, R, kx_is_a, off, Px, Py, (const double2*)spec, s);
+    note_launch("ztoeplitz");
+}
+
 // ------------------------------------------------------------------- host
 int smooth_size_at_least(int n) {
     if (n <= 1) return 1;
@@ -897,14 +959,19 @@ static bool try_ct_planar(PlanarPass p, cudaStream_t s) {
     return true;
 }
 
-template <int NZ, int N1, int N2>
+// NW warps per CTA: at least one half-warp per z line; more warps so that the
+// Toeplitz step (one thread per ky) runs in one round.
+#ifndef AIM_PLANAR4_NW11
+#define AIM_PLANAR4_NW11 6
+#endif
+template <int NZ, int N1, int N2, int NW>
 static bool try_planar4(const PlanarPass& p, cudaStream_t s) {
     constexpr int Py = N1 * N2;
     if (p.ay.P != Py || p.Nz != NZ || p.PyH != Py / 2 + 1) return false;
     const long long tiles = 4LL * p.Px * p.R;
     const size_t smem = sizeof(double2) * ((size_t)2 * Py * NZ + (Py / 2 + 1) * NZ + Py);
-    auto kern = planar4_kernel<NZ, N1, N2>;
-    constexpr int T = 32 * ((NZ + 1) / 2);
+    auto kern = planar4_kernel<NZ, N1, N2, NW>;
+    constexpr int T = 32 * NW;
     ensure_smem_attr(kern);
     const long long grid = persistent_grid(kern, T, smem, tiles);
     kern<<<(unsigned)grid, T, smem, s>>>(p, (int)tiles);
@@ -918,7 +985,7 @@ static void launch_planar_yz_t(PlanarPass p, cudaStream_t s) {
     if constexpr (sizeof(C) == 16) {
         // four-step register kernel (AIM_PLANAR_KERNEL=stockham forces the stage kernel, A/B timing only)
         const char* e = getenv("AIM_PLANAR_KERNEL");
-        if (!(e && !strcmp(e, "stockham")) && (try_planar4<11, 14, 15>(p, s) || try_planar4<7, 4, 6>(p, s)))
+        if (!(e && !strcmp(e, "stockham")) && (try_planar4<11, 14, 15, AIM_PLANAR4_NW11>(p, s) || try_planar4<7, 4, 6, 4>(p, s)))
             return;
     }
     if (try_ct_planar<C, 11, Ct210z11, 2>(p, s) || try_ct_planar<C, 7, Ct24z7, 2>(p, s)) return;

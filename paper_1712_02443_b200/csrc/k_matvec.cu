@@ -863,7 +863,7 @@ void ensure_workspace(aim_plan* p, int R) {
     const long long es = p->prec == AIM_C64 ? 1 : 2;   // element size in 8-byte units
     p->Q = (double2*)p->alloc<float2>(es * 4 * Nx * Ny * Nz * R);
     p->W1 = (double2*)p->alloc<float2>(es * 4 * Px * Ny * Nz * R);
-    if (!p->planar) p->W2 = (double2*)p->alloc<float2>(es * 4 * Px * Py * Nz * R);
+    if (p->planar != 1) p->W2 = (double2*)p->alloc<float2>(es * 4 * Px * Py * Nz * R);
     p->ws_nrhs = R;
 }
 
@@ -897,7 +897,7 @@ static void convolve_impl(aim_plan* p, const void* Q, void* Phi, int R, cudaStre
     f.mode = 0; f.ax = p->ax[0]; f.TO = f.TI = 0;
     launch_fft_pass(f, s);
     if (pr) pr->mark(2, s);
-    if (p->planar) {
+    if (p->planar == 1) {
         PlanarPass q{};
         q.prec = p->prec;
         q.W = p->W1; q.Px = Px; q.Ny = (int)Ny; q.Nz = (int)Nz; q.R = R; q.PyH = Py / 2 + 1; q.ay = p->ax[1];
@@ -909,11 +909,16 @@ static void convolve_impl(aim_plan* p, const void* Q, void* Phi, int R, cudaStre
         f.in = p->W1; f.out = p->W2; f.outer = 4LL * Px; f.Lin = (int)Ny; f.Lout = Py; f.inner = Nz * R;
         f.mode = 0; f.ax = p->ax[1]; f.TO = f.TI = 0;
         launch_fft_pass(f, s);
-        // z turnaround in place, [4 Px Py][Nz -> Pz -> Nz][R]
-        f.in = p->W2; f.out = p->W2; f.outer = 4LL * Px * Py; f.Lin = (int)Nz; f.Lout = (int)Nz; f.inner = R;
-        f.mode = 2; f.ax = p->ax[2]; f.TO = f.TI = 0;
-        f.spec = spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
-        launch_fft_pass(f, s);
+        if (p->planar == 2) {
+            // z convolution as a direct Toeplitz product with G2(kx, ky, |dz|), in place
+            launch_ztoeplitz(p->W2, p->prec, Px, Py, (int)Nz, R, 1, 0, Px, Py, spec, s);
+        } else {
+            // z turnaround in place, [4 Px Py][Nz -> Pz -> Nz][R]
+            f.in = p->W2; f.out = p->W2; f.outer = 4LL * Px * Py; f.Lin = (int)Nz; f.Lout = (int)Nz; f.inner = R;
+            f.mode = 2; f.ax = p->ax[2]; f.TO = f.TI = 0;
+            f.spec = spec; f.Px = Px; f.Py = Py; f.PyH = Py / 2 + 1; f.PzH = Pz / 2 + 1;
+            launch_fft_pass(f, s);
+        }
         // y inverse, [4 Px][Py -> Ny][Nz R]
         f.in = p->W2; f.out = p->W1; f.outer = 4LL * Px; f.Lin = Py; f.Lout = (int)Ny; f.inner = Nz * R;
         f.mode = 1; f.ax = p->ax[1]; f.TO = f.TI = 0;

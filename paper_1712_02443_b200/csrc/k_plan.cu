@@ -924,7 +924,7 @@ __global__ void spectrum_octant(const double2* F, double2* spec, int Px, int Py,
 
 void build_green_spectrum(aim_plan* p, cudaStream_t s) {
     const int Px = p->pads[0], Py = p->pads[1], Pz = p->pads[2], Nz = p->dims[2];
-    const int Lz = p->planar ? Nz : Pz;
+    const int Lz = p->planar ? Nz : Pz;   // modes 1 and 2 share the 2-D spectrum G2(kx, ky, dz)
     const long long tot = (long long)Px * Py * Lz;
     double2 *A = nullptr, *B = nullptr;
     AIM_CUDA(cudaMalloc(&A, sizeof(double2) * tot));

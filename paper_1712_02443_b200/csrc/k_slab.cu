@@ -11,13 +11,14 @@
 // renumbered so each rank's rows are contiguous (permuted order = by owner,
 // then by id); x is replicated, y is gathered back to every rank.
 //
-// One product (planar grids, conv_mode 1; 3-D grids add the z passes):
+// One product (planar grids, conv_modes 1 and 2; 3-D grids add the z passes):
 //   near rows + projection of the owned RWGs  -> Q on [X_r, X_{r+1} + M)
 //   halo reduce: planes [X_{r+1}, X_{r+1} + M) are added into rank r+1
 //   y forward FFT (pad Ny -> Py) on the owned planes [3-D: then z forward, pad Nz -> Pz]
 //   all-to-all #1: x-slabs -> ky-slabs [KY_s, KY_{s+1}) with every x
 //   planar: x forward FFT (pad Nx -> Px), z Toeplitz x G2, x inverse (prune) --
-//     the planar kernel with the roles of x and y swapped (transposed spectrum);
+//     mode 1: the fused planar kernel with the roles of x and y swapped
+//     (transposed spectrum); mode 2: x pass, z Toeplitz kernel, x pass;
 //   3-D: x turnaround (pad, forward, x G^ octant transposed to [ky][kz][kx], inverse, prune)
 //   all-to-all #2 back to x-slabs [3-D: z inverse], y inverse FFT (prune Py -> Ny)
 //   halo copy: planes [X_{r+1}, X_{r+1} + M) of Phi from rank r+1
@@ -238,6 +239,7 @@ struct aim_slab_rank {
     double2* Wy = nullptr;    // [4][Xl][Py][Zc][R]   after the y (3-D: and z) forward pass
     double2* Wy1 = nullptr;   // [4][Xl][Py][Nz][R]   3-D only: between the y and z passes
     double2* T = nullptr;     // [4][KYl][Nx][Zc][R]  x pencils
+    double2* Tp = nullptr;    // [4][KYl][Px][Nz][R]  conv mode 2: x-padded pencils
     double2* sb = nullptr;    // send blocks  (max of the two all-to-alls)
     double2* rb = nullptr;    // receive blocks
     double2* hb = nullptr;    // halo staging [4][M][Ny][Nz][R]
@@ -319,7 +321,7 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     create_plan(V, nv, T, nt, E, N, k, h, M, r, AIM_C128, S->base);
     aim_plan* B = S->base;
     S->planar = B->planar;
-    if (S->planar && !planar_supported(B->pads[0], B->dims[2], B->ax[0].min_radix))
+    if (S->planar == 1 && !planar_supported(B->pads[0], B->dims[2], B->ax[0].min_radix))
         throw Error(AIM_E_ARG, "planar slab pass: the x lines do not fit the planar kernel");
     S->Nx = B->dims[0]; S->Ny = B->dims[1]; S->Nz = B->dims[2];
     S->Px = B->pads[0]; S->Py = B->pads[1]; S->Pz = B->pads[2];
@@ -475,15 +477,17 @@ static void slab_workspace(aim_slab* S, int R) {
     S->yp = S->alloc<double2>((size_t)S->N * R);
     const long long NzR = (long long)S->Nz * R, ZR = (long long)S->Zc * R;
     for (auto& Rk : S->ranks) {
-        for (void* ptr : {(void*)Rk.Qh, (void*)Rk.Wy, (void*)Rk.Wy1, (void*)Rk.T, (void*)Rk.sb, (void*)Rk.rb,
-                          (void*)Rk.hb, (void*)Rk.d_off1})
+        for (void* ptr : {(void*)Rk.Qh, (void*)Rk.Wy, (void*)Rk.Wy1, (void*)Rk.T, (void*)Rk.Tp, (void*)Rk.sb,
+                          (void*)Rk.rb, (void*)Rk.hb, (void*)Rk.d_off1})
             S->release(ptr);
         Rk.Wy1 = nullptr;
+        Rk.Tp = nullptr;
         const long long kyl = Rk.KY1 - Rk.KY0;
         Rk.Qh = S->alloc<double2>(4LL * Rk.Xh * S->Ny * NzR);
         Rk.Wy = S->alloc<double2>(4LL * Rk.Xl * S->Py * ZR);
         if (!S->planar) Rk.Wy1 = S->alloc<double2>(4LL * Rk.Xl * S->Py * NzR);
         Rk.T = S->alloc<double2>(4LL * kyl * S->Nx * ZR);
+        if (S->planar == 2) Rk.Tp = S->alloc<double2>(4LL * kyl * S->Px * ZR);
         const long long blk = std::max(4LL * Rk.Xl * S->Py * ZR, 4LL * kyl * S->Nx * ZR);
         Rk.sb = S->alloc<double2>(blk);
         Rk.rb = S->alloc<double2>(blk);
@@ -650,6 +654,24 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
     }
     // x forward, z Toeplitz x G2 (3-D: x G^), x inverse on the ky pencils
     for (auto& Rk : S->ranks) {
+        if (S->planar == 2) {
+            // separate passes: x forward (pad) into Tp, z Toeplitz (ky = KY0 + a, kx = b), x inverse (prune)
+            const int kyl = Rk.KY1 - Rk.KY0;
+            if (kyl <= 0) continue;
+            FftPass f{};
+            f.prec = AIM_C128;
+            f.outer = 4LL * kyl;
+            f.inner = ZR;
+            f.ax = S->base->ax[0];
+            f.TO = f.TI = 0;
+            f.in = Rk.T; f.out = Rk.Tp; f.Lin = S->Nx; f.Lout = S->Px; f.mode = 0;
+            launch_fft_pass(f, s);
+            launch_ztoeplitz(Rk.Tp, AIM_C128, kyl, S->Px, S->Nz, R, 0, Rk.KY0, S->Px, S->Py, S->base->spec, s);
+            f.TO = f.TI = 0;
+            f.in = Rk.Tp; f.out = Rk.T; f.Lin = S->Px; f.Lout = S->Nx; f.mode = 1;
+            launch_fft_pass(f, s);
+            continue;
+        }
         if (!S->planar) {
             FftPass f{};
             f.prec = AIM_C128;

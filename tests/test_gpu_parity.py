@@ -67,7 +67,7 @@ def test_green_spectrum(name):
     K(x, y, dz), dz < Nz, divided by PxPy (numpy FFT of the oracle's samples)."""
     G, O = gpu_plan(name), oracle_plan(name)
     pads = G.info["fft_dims"]
-    if G.info["conv_mode"] == 1:
+    if G.info["conv_mode"] != 0:
         Nz = G.info["grid_dims"][2]
         K = O.kernel_samples((pads[0], pads[1], 2 * Nz))[:, :, :Nz]
         F = np.fft.fft2(K, axes=(0, 1)) / (pads[0] * pads[1])
@@ -314,4 +314,27 @@ def test_interp_mma_kernel(name, rb, monkeypatch):
         assert rel(y_mma, y_g) <= 1e-13, nrhs
         ref = O.interpolate(Phi.cpu().numpy()) + Z @ x
         assert rel(y_mma, ref) <= 1e-12, nrhs
+    G.close()
+
+
+@pytest.mark.parametrize("name,nrhs", [("c1", 1), ("c1", 16), ("t_m3", 3), ("t_dissim", 1), ("t_vol", 2)])
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_conv_modes_forced(name, nrhs, mode, monkeypatch):
+    """The 3-D FFT convolution (conv_mode 0) and the planar mode with separate
+    y passes around the z Toeplitz kernel (conv_mode 2; C3/C4 use it) forced on
+    small grids: matvec vs the oracle <= 1e-10, convolution stage vs the oracle
+    <= 1e-12."""
+    from paper_1712_02443_b200 import AimPlan
+    monkeypatch.setenv("AIM_CONV_MODE", mode)
+    cfg = get_config(name)
+    O = oracle_plan(name)
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    assert G.info["conv_mode"] == int(mode)
+    x = make_vectors(O.N, nrhs, 2)
+    xt = torch.from_numpy(x).cuda()
+    assert rel(G.matvec(xt).cpu().numpy(), O.matvec(x)) <= 1e-10
+    Qo = O.project(x)
+    Phi = G.convolve(torch.from_numpy(np.ascontiguousarray(Qo)).cuda())
+    Phio = O.convolve_direct(Qo) if O.Ng <= 4000 else O.convolve_fft(Qo)
+    assert rel(Phi.cpu().numpy(), Phio) <= 1e-12
     G.close()

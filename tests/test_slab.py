@@ -105,22 +105,23 @@ def test_gloo_world2_partition_and_plumbing():
 
 # ------------------------------------------------------------------ GPU
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["planar", "3d"])
+@pytest.mark.parametrize("mode", ["planar", "planar2", "3d"])
 @pytest.mark.parametrize("name,world,nrhs", [("c1", 2, 1), ("c1", 3, 5), ("c1", 6, 16), ("t_m3", 2, 2),
                                              ("t_dissim", 3, 9), ("t_vol", 2, 3)])
 def test_slab_matvec_vs_single_and_oracle(name, world, nrhs, mode, monkeypatch):
-    """planar: x pencils through the planar kernel (transposed 2-D spectrum);
-    3d (AIM_CONV_MODE=0): y and z passes local, x turnaround on the pencils
-    with the transposed octant."""
+    """planar: x pencils through the fused planar kernel (transposed 2-D
+    spectrum); planar2 (AIM_CONV_MODE=2): x passes around the z Toeplitz
+    kernel; 3d (AIM_CONV_MODE=0): y and z passes local, x turnaround on the
+    pencils with the transposed octant."""
     import torch
     from conftest import oracle_plan
     from paper_1712_02443_b200 import AimPlan, AimSlabPlan
     cfg = get_config(name)
     mesh = make_mesh(cfg)
-    if mode == "3d":
-        monkeypatch.setenv("AIM_CONV_MODE", "0")
+    if mode != "planar":
+        monkeypatch.setenv("AIM_CONV_MODE", "0" if mode == "3d" else "2")
     single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    assert single.info["conv_mode"] == (1 if mode == "planar" else 0) or name == "t_vol"
+    assert single.info["conv_mode"] == {"planar": 1, "planar2": 2, "3d": 0}[mode] or name == "t_vol"
     slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
     q = [slab.query(r) for r in range(world)]
     assert q[0]["n0"] == 0 and q[-1]["n1"] == mesh.n_rwg
