@@ -93,7 +93,7 @@ KERNEL_NAMES = {
     "project": "project_kernel (H1 projection gather)",
     "interp": "interp_kernel (H5 interpolation)",
     "fft_x": "fft_ct_kernel (x forward, zero-pad fused)",
-    "fft_yz": "planar_ct_kernel (y fwd FFT, z Toeplitz x G2, y inv FFT, fused)",
+    "fft_yz": "planar4_kernel (y fwd FFT, z Toeplitz x G2, y inv FFT, fused)",
     "ifft_x": "fft_ct_kernel (x inverse, pruned)",
 }
 

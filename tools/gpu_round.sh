@@ -11,5 +11,5 @@ timeout 300 python tools/prof_matvec.py $CFG 3 > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python tools/prof_matvec.py $CFG 3 > gpurun_out/ncu_launch.log 2>&1
 python tools/launches.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt; cat gpurun_out/launches_summary.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'near_b4|planar_ct|fft_ct|project_kernel|interp_kernel' \
-  -s 11 -c 6 -o gpurun_out/prof_full python tools/prof_matvec.py $CFG 3 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'near_mma|planar4|fft_ct|project_kernel|interp_kernel' \
+  -s 8 -c 6 -o gpurun_out/prof_full python tools/prof_matvec.py $CFG 3 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
