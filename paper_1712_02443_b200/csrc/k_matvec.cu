@@ -123,6 +123,44 @@ __global__ void __launch_bounds__(256) project_kernel(const int32_t* __restrict_
     }
 }
 
+// Single right-hand side (GMRES products): G lanes per grid node, 32/G nodes
+// per warp, each lane strides over the node's entries (fixed order), group
+// reduction by shuffles; a node's 4 components are written by its first lane.
+template <int G, class C>
+__global__ void __launch_bounds__(256) project1_kernel(const int32_t* __restrict__ prow,
+                                                       const int32_t* __restrict__ pn,
+                                                       const Real<C>* __restrict__ Wc, const C* __restrict__ x,
+                                                       long long Ng, C* __restrict__ Q) {
+    const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int sub = threadIdx.x % G;
+    const bool live = gid < Ng;
+    const int e0 = live ? prow[gid] : 0, e1 = live ? prow[gid + 1] : 0;
+    const C* W2 = reinterpret_cast<const C*>(Wc);
+    C a[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[c] = mkc<C>(0, 0);
+#pragma unroll 2
+    for (int e = e0 + sub; e < e1; e += G) {
+        const int n = __ldcs(&pn[e]);
+        const C w01 = __ldcs(W2 + 2 * (long long)e), w23 = __ldcs(W2 + 2 * (long long)e + 1);
+        const C xv = __ldg(&x[n]);
+        a[0].x = fma(w01.x, xv.x, a[0].x); a[0].y = fma(w01.x, xv.y, a[0].y);
+        a[1].x = fma(w01.y, xv.x, a[1].x); a[1].y = fma(w01.y, xv.y, a[1].y);
+        a[2].x = fma(w23.x, xv.x, a[2].x); a[2].y = fma(w23.x, xv.y, a[2].y);
+        a[3].x = fma(w23.y, xv.x, a[3].x); a[3].y = fma(w23.y, xv.y, a[3].y);
+    }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const C t = shfl_xor2(a[c], off);
+            a[c].x += t.x; a[c].y += t.y;
+        }
+    if (live && sub == 0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) __stcs(&Q[(long long)c * Ng + gid], a[c]);
+}
+
 // (LPE, RPL) per RHS count.  NEAR: 4 RHS per lane (instruction-bound SpMV);
 // GATHER (projection / interpolation): one RHS per lane (latency-bound).
 #define AIM_LANE_DISPATCH_NEAR(R, CALL)                \
@@ -144,6 +182,18 @@ template <class C>
 static void launch_project_t(const aim_plan* p, const C* x, C* Q, int R, cudaStream_t s) {
     const unsigned grid = nblk(p->Ng * 32, 256);
     const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->Wc : (const void*)p->Wc32);
+    if (R == 1) {
+        // lanes per node ~ entries per node / 4 (power of two in [4, 32])
+        const double per = p->Ng ? (double)p->nnzP / (double)p->Ng : 1.0;
+        const int G = per > 96 ? 32 : per > 48 ? 16 : per > 24 ? 8 : 4;
+#define P1(GG) project1_kernel<GG, C><<<nblk(p->Ng * GG, 256), 256, 0, s>>>(p->prow, p->pn, W, x, p->Ng, Q)
+        if (G == 32) P1(32);
+        else if (G == 16) P1(16);
+        else if (G == 8) P1(8);
+        else P1(4);
+#undef P1
+        return;
+    }
 #define PJ_CALL(LPE, RPL) project_kernel<MM, LPE, RPL, C><<<grid, 256, 0, s>>>(p->prow, p->pn, W, x, p->Ng, R, Q)
 #define PJ_M(MMV)                                   \
     if (p->M == MMV) {                              \
