@@ -356,6 +356,44 @@ __global__ void __launch_bounds__(256) near_kernel(const int64_t* __restrict__ r
     }
 }
 
+// Single right-hand side (GMRES products): warp per row, each lane takes
+// entries lane, lane + 32, ... in unrolled groups of 4 (values, columns, then
+// the 4 x gathers in flight together); fixed order => deterministic.
+template <class C>
+__global__ void __launch_bounds__(256) near1_kernel(const int64_t* __restrict__ rowp, const int32_t* __restrict__ col,
+                                                    const C* __restrict__ val, const C* __restrict__ x, long long N,
+                                                    C* __restrict__ y) {
+    const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (m >= N) return;
+    const int lane = threadIdx.x & 31;
+    const long long e0 = rowp[m], e1 = rowp[m + 1];
+    C acc = mkc<C>(0, 0);
+    for (long long b = e0 + lane; b < e1; b += 128) {
+        C z[4], xv[4];
+        int n[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long e = b + 32 * u;
+            const bool v = e < e1;
+            z[u] = v ? __ldcs(&val[e]) : mkc<C>(0, 0);
+            n[u] = v ? __ldcs(&col[e]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = n[u] >= 0 ? __ldg(&x[n[u]]) : mkc<C>(0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            acc.x = fma(z[u].x, xv[u].x, acc.x); acc.x = fma(-z[u].y, xv[u].y, acc.x);
+            acc.y = fma(z[u].x, xv[u].y, acc.y); acc.y = fma(z[u].y, xv[u].x, acc.y);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const C t = shfl_xor2(acc, off);
+        acc.x += t.x; acc.y += t.y;
+    }
+    if (lane == 0) y[m] = acc;
+}
+
 // ------------------------------------------ H6 near SpMV, 4-row blocks
 // Warp per block of 4 rows (Morton-ordered RWGs); column groups of LPE
 // lanes walk the block's union columns, each lane holding RPL right-hand
@@ -855,6 +893,10 @@ static void launch_near_t(aim_plan* p, const C* x, C* y, int R, cudaStream_t s) 
     }
     const unsigned grid = nblk(p->N * 32, 256);
     const C* val = (const C*)(c64 ? (const void*)p->nval32 : (const void*)p->nval);
+    if (R == 1) {
+        near1_kernel<C><<<grid, 256, 0, s>>>(p->nrow, p->ncol, val, x, p->N, y);
+        return;
+    }
 #define NK_CALL(LPE, RPL) near_kernel<LPE, RPL, C><<<grid, 256, 0, s>>>(p->nrow, p->ncol, val, x, p->N, R, y)
     AIM_LANE_DISPATCH_NEAR(R, NK_CALL)
 #undef NK_CALL
