@@ -895,7 +895,14 @@ static void launch_fft_pass_t(FftPass p, cudaStream_t s) {
     if (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s)) return;
     // runtime radices: in place when one butterfly per thread per stage suffices for >= 2 lines
     const int nl_inplace = kFftThreads * p.ax.min_radix / P;
-    const bool inplace = nl_inplace >= 2;
+    // The ping-pong kernel (several butterflies per thread, up to
+    // fft_tile_capacity() elements per tile, one tile per CTA) beats the
+    // persistent in-place kernel on every measured size (C3 FFT 0.98 -> 0.60 ms,
+    // C4 1.93 -> 1.67, C5 5.70 -> 2.05 ms: the in-place kernel's one butterfly
+    // per thread limits a tile to 256 * min_radix / P lines, 3 for P = 243).
+    // AIM_FFT_INPLACE=1 restores the in-place kernel (A/B timing).
+    const char* fe = getenv("AIM_FFT_INPLACE");
+    const bool inplace = nl_inplace >= 2 && fe && fe[0] == '1';
     const int cap = std::max(fft_tile_capacity(), P);
     if (p.TI <= 0) tile_shape(p, inplace ? nl_inplace : std::max(1, cap / P));
     if (inplace) {
