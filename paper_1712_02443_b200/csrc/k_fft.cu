@@ -892,7 +892,8 @@ static bool try_ct_pass(FftPass p, cudaStream_t s) {
 template <class C>
 static void launch_fft_pass_t(FftPass p, cudaStream_t s) {
     const int P = p.ax.P;
-    if (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s)) return;
+    const char* ce = getenv("AIM_FFT_NOCT");   // A/B timing: skip the compile-time plans
+    if (!(ce && ce[0] == '1') && (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s))) return;
     // runtime radices: in place when one butterfly per thread per stage suffices for >= 2 lines
     const int nl_inplace = kFftThreads * p.ax.min_radix / P;
     // The ping-pong kernel (several butterflies per thread, up to
