@@ -338,3 +338,20 @@ def test_conv_modes_forced(name, nrhs, mode, monkeypatch):
     Phio = O.convolve_direct(Qo) if O.Ng <= 4000 else O.convolve_fft(Qo)
     assert rel(Phi.cpu().numpy(), Phio) <= 1e-12
     G.close()
+
+
+@pytest.mark.parametrize("name", ["t_m3", "t_dissim"])
+def test_gmres_fixed_iterations(name):
+    """D15 parity protocol for the larger cases ("at equal iteration counts"):
+    GMRES(50) run for exactly 60 inner iterations (one restart crossed) on an
+    M = 3 grid and a dissimilar-element grid; J_60 vs the oracle's <= 1e-5 and
+    the recomputed true residuals agree."""
+    from oracle.gmres import gmres
+    from oracle.excitation import plane_wave_rhs
+    G, O = gpu_plan(name), oracle_plan(name)
+    V = plane_wave_rhs(O.ctx)
+    ref = gmres(O.matvec, V, restart=50, tol=1e-4, fixed_iters=60)
+    J, it, rr, _ = G.gmres(torch.from_numpy(V).cuda(), restart=50, tol=1e-4, fixed_iters=60)
+    assert it == 60 == ref["iters"]
+    assert rel(J.cpu().numpy(), ref["x"]) <= 1e-5
+    assert abs(rr - ref["rel_res"]) <= 1e-6 * ref["rel_res"]
