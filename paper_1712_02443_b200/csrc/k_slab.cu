@@ -12,7 +12,8 @@
 // then by id); x is replicated, y is gathered back to every rank.
 //
 // One product (planar grids, conv_modes 1 and 2; 3-D grids add the z passes):
-//   near rows + projection of the owned RWGs  -> Q on [X_r, X_{r+1} + M)
+//   near rows of the owned RWGs (side stream, overlapping everything up to
+//     the interpolation) + their projection -> Q on [X_r, X_{r+1} + M)
 //   halo reduce: planes [X_{r+1}, X_{r+1} + M) are added into rank r+1
 //   y forward FFT (pad Ny -> Py) on the owned planes [3-D: then z forward, pad Nz -> Pz]
 //   all-to-all #1: x-slabs -> ky-slabs [KY_s, KY_{s+1}) with every x
@@ -266,6 +267,8 @@ struct aim_slab {
     int ws_nrhs = 0;
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;          // near-field rows, overlapping the FFT and its all-to-alls
+    cudaEvent_t ev_x = nullptr, ev_n = nullptr;
     std::vector<std::pair<void*, size_t>> allocs;
     int64_t bytes_a2a = 0, bytes_halo = 0;   // per matvec and RHS, per rank (max)
 
@@ -304,6 +307,9 @@ static void slab_destroy(aim_slab* S) {
     for (auto& a : S->allocs) cudaFree(a.first);
     if (S->comm) nccl().CommDestroy(S->comm);
     if (S->stream) cudaStreamDestroy(S->stream);
+    if (S->side) cudaStreamDestroy(S->side);
+    if (S->ev_x) cudaEventDestroy(S->ev_x);
+    if (S->ev_n) cudaEventDestroy(S->ev_n);
     delete S;
 }
 
@@ -315,6 +321,9 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     S->N = N;
     S->M = M;
     AIM_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+    AIM_CUDA(cudaStreamCreateWithFlags(&S->side, cudaStreamNonBlocking));
+    AIM_CUDA(cudaEventCreateWithFlags(&S->ev_x, cudaEventDisableTiming));
+    AIM_CUDA(cudaEventCreateWithFlags(&S->ev_n, cudaEventDisableTiming));
     cudaStream_t s = S->stream;
     // full plan: every rank builds the whole operator once and keeps its rows
     S->base = new aim_plan();
@@ -569,11 +578,15 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
     permute_rows_kernel<false><<<nblk(N * 2 * R, 256), 256, 0, s>>>((const double*)x, S->perm, N, 2 * R,
                                                                      (double*)S->xp);
     note_launch("slab_permute");
-    // near rows + projection of the owned RWGs
+    // near rows on the side stream (they overlap the projection, the FFT passes
+    // and the all-to-alls; interpolation waits for them), projection on `s`
+    AIM_CUDA(cudaEventRecord(S->ev_x, s));
+    AIM_CUDA(cudaStreamWaitEvent(S->side, S->ev_x, 0));
+    for (auto& Rk : S->ranks)
+        if (Rk.n1 > Rk.n0) launch_near(Rk.sub, S->xp, S->yp + Rk.n0 * R, R, S->side);
+    AIM_CUDA(cudaEventRecord(S->ev_n, S->side));
     for (auto& Rk : S->ranks) {
-        double2* yr = S->yp + Rk.n0 * R;
         if (Rk.n1 > Rk.n0) {
-            launch_near(Rk.sub, S->xp, yr, R, s);
             launch_project(Rk.sub, S->xp + Rk.n0 * R, Rk.Qh, R, s);
         } else {
             AIM_CUDA(cudaMemsetAsync(Rk.Qh, 0, esz * 4 * Rk.Xh * S->Ny * NzR, s));
@@ -754,6 +767,7 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
         if (w + 1 < G) halo_copy(S, Rk, Rk.Qh, Rk.hb, false, Rk.Xl, M, R, s);
     }
     // interpolation of the owned RWGs onto their near rows
+    AIM_CUDA(cudaStreamWaitEvent(s, S->ev_n, 0));
     for (auto& Rk : S->ranks)
         if (Rk.n1 > Rk.n0) launch_interp(Rk.sub, Rk.Qh, S->yp + Rk.n0 * R, R, true, s);
     // every rank gets all rows
