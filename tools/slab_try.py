@@ -20,6 +20,13 @@ print("slab plan", time.time() - t, [slab.query(r) for r in range(world)])
 x = torch.from_numpy(make_vectors(mesh.n_rwg, cfg.nrhs, 0)).cuda()
 yg = slab.matvec(x)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    slab.matvec(x, yg)
+e1.record()
+torch.cuda.synchronize()
+print("slab product ms (all slabs on this GPU, sequential):", e0.elapsed_time(e1) / 5)
 single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
 y1 = single.matvec(x)
 print("rel", float((yg - y1).norm() / y1.norm()))
