@@ -294,3 +294,49 @@ def slab_nccl_id(group=None) -> bytes:
     obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+class HostPipeline:
+    """Products from pinned host buffers with the copies overlapped: step i's
+    host->device copy, step i-1's product and step i-2's device->host copy run
+    on three streams (double-buffered device vectors, event-ordered).  Every
+    step still copies its x in and its y out; submit() returns at once, drain()
+    waits for everything submitted.  Argument marshalling only: the product is
+    aim_matvec on the plan's kernels."""
+
+    def __init__(self, plan: "AimPlan", nrhs: int, depth: int = 2):
+        torch = _torch()
+        self.plan, self.nrhs, self.depth = plan, nrhs, depth
+        shape = (plan.N, nrhs) if nrhs > 1 else (plan.N,)
+        self.xd = [torch.empty(shape, dtype=plan.dtype, device="cuda") for _ in range(depth)]
+        self.yd = [torch.empty(shape, dtype=plan.dtype, device="cuda") for _ in range(depth)]
+        self.s_in, self.s_mv, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self.ev_in = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_mv = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_out = [torch.cuda.Event() for _ in range(depth)]
+        self.i = 0
+
+    def submit(self, x_host, y_host):
+        """x_host, y_host: pinned torch tensors of the plan's dtype and shape."""
+        torch = _torch()
+        k = self.i % self.depth
+        with torch.cuda.stream(self.s_in):
+            if self.i >= self.depth:
+                self.s_in.wait_event(self.ev_mv[k])          # slot's x no longer read
+            self.xd[k].copy_(x_host, non_blocking=True)
+            self.ev_in[k].record(self.s_in)
+        with torch.cuda.stream(self.s_mv):
+            self.s_mv.wait_event(self.ev_in[k])
+            if self.i >= self.depth:
+                self.s_mv.wait_event(self.ev_out[k])         # slot's y already copied out
+            self.plan.matvec(self.xd[k], self.yd[k])
+            self.ev_mv[k].record(self.s_mv)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_mv[k])
+            y_host.copy_(self.yd[k], non_blocking=True)
+            self.ev_out[k].record(self.s_out)
+        self.i += 1
+
+    def drain(self):
+        for s in (self.s_in, self.s_mv, self.s_out):
+            s.synchronize()

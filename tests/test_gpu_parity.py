@@ -355,3 +355,19 @@ def test_gmres_fixed_iterations(name):
     assert it == 60 == ref["iters"]
     assert rel(J.cpu().numpy(), ref["x"]) <= 1e-5
     assert abs(rr - ref["rel_res"]) <= 1e-6 * ref["rel_res"]
+
+
+def test_host_pipeline_matches_device_product():
+    """HostPipeline (pinned host x in, y out, copies overlapped with the
+    products of neighbouring steps) returns exactly aim_matvec's result for
+    every step."""
+    from paper_1712_02443_b200.api import HostPipeline
+    G, O = gpu_plan("c1"), oracle_plan("c1")
+    xs = [torch.from_numpy(make_vectors(O.N, 4, s)).pin_memory() for s in range(5)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    hp = HostPipeline(G, 4)
+    for x, y in zip(xs, ys):
+        hp.submit(x, y)
+    hp.drain()
+    for x, y in zip(xs, ys):
+        assert torch.equal(y, G.matvec(x.cuda()).cpu())
