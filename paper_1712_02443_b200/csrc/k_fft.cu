@@ -98,6 +98,9 @@ __device__ __forceinline__ void tile_range(int tiles, int& t0, int& t1) {
 // kernels.  Radices <= 7: one butterfly's registers stay small.
 using Ct210 = CtpPlan<8, 336, 210, 7, 6, 5>;      // x passes of C2: 8 lines (128 B rows)
 using Ct24 = CtpPlan<32, 192, 24, 6, 4>;          // x passes of C1 (1 RHS): 32 lines
+using Ct243 = CtpPlan<8, 216, 243, 9, 9, 3>;      // every axis of C5
+using Ct486 = CtpPlan<4, 216, 486, 9, 9, 6>;      // x and y passes of C3
+using Ct784 = CtpPlan<2, 224, 784, 16, 7, 7>;     // x and y passes of C4
 using Ct210z11 = CtpPlan<11, 240, 210, 7, 6, 5>;  // planar y/z of C2, one RHS per tile
 using Ct24z7 = CtpPlan<7, 64, 24, 6, 4>;          // planar y/z of C1, one RHS per tile
 
@@ -893,7 +896,10 @@ template <class C>
 static void launch_fft_pass_t(FftPass p, cudaStream_t s) {
     const int P = p.ax.P;
     const char* ce = getenv("AIM_FFT_NOCT");   // A/B timing: skip the compile-time plans
-    if (!(ce && ce[0] == '1') && (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s))) return;
+    if (!(ce && ce[0] == '1') &&
+        (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s) || try_ct_pass<C, Ct243, 2>(p, s) ||
+         try_ct_pass<C, Ct486, 2>(p, s) || try_ct_pass<C, Ct784, 2>(p, s)))
+        return;
     // runtime radices: in place when one butterfly per thread per stage suffices for >= 2 lines
     const int nl_inplace = kFftThreads * p.ax.min_radix / P;
     // The ping-pong kernel (several butterflies per thread, up to
