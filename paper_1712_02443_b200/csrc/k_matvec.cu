@@ -298,55 +298,69 @@ __global__ void __launch_bounds__(256) interp_kernel(const C* __restrict__ Phi, 
 // Single right-hand side: warp per RWG row, lane u holds stencil entries
 // u, u + 32, ... (K = ceil(S/32) of them): all weights, then all 4K potential
 // gathers are issued before the FMAs; fixed order => deterministic.
-template <int M, class C>
+template <int M, int RW, class C>
 __global__ void __launch_bounds__(256) interp1_kernel(const C* __restrict__ Phi, const Real<C>* __restrict__ W,
                                                       const int32_t* __restrict__ node0, long long Ng, int Ny, int Nz,
                                                       long long N, double keta, double ik2, int accumulate,
                                                       C* __restrict__ y) {
+    // RW rows per warp: every row's weights and node index are requested
+    // before any row's potential gathers, which are all in flight together
     constexpr int M1 = M + 1, S = M1 * M1 * M1, K = (S + 31) / 32;
-    const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    if (m >= N) return;
+    const long long m0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32 * RW;
+    if (m0 >= N) return;
     const int lane = threadIdx.x & 31;
-    const long long g0 = node0[m];
-    const C* W2 = reinterpret_cast<const C*>(W) + 2 * m * S;
-    C w01[K], w23[K];
-    long long g[K];
+    long long g0[RW];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int u = lane + 32 * k;
-        const bool v = u < S;
-        w01[k] = v ? __ldcs(W2 + 2 * u) : mkc<C>(0, 0);
-        w23[k] = v ? __ldcs(W2 + 2 * u + 1) : mkc<C>(0, 0);
-        const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
-        g[k] = v ? g0 + ((long long)ui * Ny + uj) * Nz + uk : -1;
-    }
-    C f[K][4];
+    for (int q = 0; q < RW; ++q) g0[q] = m0 + q < N ? (long long)node0[m0 + q] : -1;
+    C w01[RW][K], w23[RW][K];
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int q = 0; q < RW; ++q) {
+        const C* W2 = reinterpret_cast<const C*>(W) + 2 * (m0 + q) * S;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) f[k][c] = g[k] >= 0 ? __ldg(&Phi[c * Ng + g[k]]) : mkc<C>(0, 0);
-    C aA = mkc<C>(0, 0), aP = mkc<C>(0, 0);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        aA.x = fma(w01[k].x, f[k][0].x, aA.x); aA.y = fma(w01[k].x, f[k][0].y, aA.y);
-        aA.x = fma(w01[k].y, f[k][1].x, aA.x); aA.y = fma(w01[k].y, f[k][1].y, aA.y);
-        aA.x = fma(w23[k].x, f[k][2].x, aA.x); aA.y = fma(w23[k].x, f[k][2].y, aA.y);
-        aP.x = fma(w23[k].y, f[k][3].x, aP.x); aP.y = fma(w23[k].y, f[k][3].y, aP.y);
-    }
-    // far = j k eta0 (aA - aP / k^2)
-    const C fr = mkc<C>(aA.x - aP.x * (Real<C>)ik2, aA.y - aP.y * (Real<C>)ik2);
-    C tot = mkc<C>(-(Real<C>)keta * fr.y, (Real<C>)keta * fr.x);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-        const C t = shfl_xor2(tot, off);
-        tot.x += t.x; tot.y += t.y;
-    }
-    if (lane == 0) {
-        if (accumulate) {
-            const C o = y[m];
-            tot.x += o.x; tot.y += o.y;
+        for (int k = 0; k < K; ++k) {
+            const int u = lane + 32 * k;
+            const bool v = u < S && g0[q] >= 0;
+            w01[q][k] = v ? __ldcs(W2 + 2 * u) : mkc<C>(0, 0);
+            w23[q][k] = v ? __ldcs(W2 + 2 * u + 1) : mkc<C>(0, 0);
         }
-        y[m] = tot;
+    }
+    C f[RW][K][4];
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int u = lane + 32 * k;
+            const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
+            const bool v = u < S && g0[q] >= 0;
+            const long long g = g0[q] + ((long long)ui * Ny + uj) * Nz + uk;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) f[q][k][c] = v ? __ldg(&Phi[c * Ng + g]) : mkc<C>(0, 0);
+        }
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+        C aA = mkc<C>(0, 0), aP = mkc<C>(0, 0);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            aA.x = fma(w01[q][k].x, f[q][k][0].x, aA.x); aA.y = fma(w01[q][k].x, f[q][k][0].y, aA.y);
+            aA.x = fma(w01[q][k].y, f[q][k][1].x, aA.x); aA.y = fma(w01[q][k].y, f[q][k][1].y, aA.y);
+            aA.x = fma(w23[q][k].x, f[q][k][2].x, aA.x); aA.y = fma(w23[q][k].x, f[q][k][2].y, aA.y);
+            aP.x = fma(w23[q][k].y, f[q][k][3].x, aP.x); aP.y = fma(w23[q][k].y, f[q][k][3].y, aP.y);
+        }
+        // far = j k eta0 (aA - aP / k^2)
+        const C fr = mkc<C>(aA.x - aP.x * (Real<C>)ik2, aA.y - aP.y * (Real<C>)ik2);
+        C tot = mkc<C>(-(Real<C>)keta * fr.y, (Real<C>)keta * fr.x);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const C t = shfl_xor2(tot, off);
+            tot.x += t.x; tot.y += t.y;
+        }
+        if (lane == 0 && g0[q] >= 0) {
+            if (accumulate) {
+                const C o = y[m0 + q];
+                tot.x += o.x; tot.y += o.y;
+            }
+            y[m0 + q] = tot;
+        }
     }
 }
 
@@ -870,8 +884,13 @@ static void launch_interp_t(aim_plan* p, const C* Phi, C* y, int R, bool accumul
     const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
     const Real<C>* W = (const Real<C>*)(sizeof(C) == 16 ? (const void*)p->W : (const void*)p->W32);
     if (R == 1 && p->M <= 4) {
+#ifndef AIM_INTERP1_RW
+#define AIM_INTERP1_RW 2
+#endif
+        constexpr int RW = AIM_INTERP1_RW;   // rows per warp
+        const unsigned grid1 = nblk((p->N + RW - 1) / RW * 32, 256);
         switch (p->M) {
-#define I1(MM) case MM: interp1_kernel<MM, C><<<grid, 256, 0, s>>>(Phi, W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, keta, ik2, accumulate ? 1 : 0, y); break;
+#define I1(MM) case MM: interp1_kernel<MM, RW, C><<<grid1, 256, 0, s>>>(Phi, W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, keta, ik2, accumulate ? 1 : 0, y); break;
             I1(1) I1(2) I1(3) I1(4)
 #undef I1
         }
