@@ -28,6 +28,10 @@ static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) 
 #define AIM_GATHER_RPL16 1
 #endif
 constexpr int kGatherUnroll = AIM_GATHER_UNROLL;   // gather steps in flight per lane
+#ifndef AIM_P1_UNROLL
+#define AIM_P1_UNROLL 4
+#endif
+constexpr int kP1Unroll = AIM_P1_UNROLL;           // single-RHS projection: entries in flight per lane
 
 
 // Lane layout of the gather kernels: LPE lanes share one CSR entry and each
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(256) project1_kernel(const int32_t* __restrict
     C a[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) a[c] = mkc<C>(0, 0);
-#pragma unroll 2
+#pragma unroll kP1Unroll
     for (int e = e0 + sub; e < e1; e += G) {
         const int n = __ldcs(&pn[e]);
         const C w01 = __ldcs(W2 + 2 * (long long)e), w23 = __ldcs(W2 + 2 * (long long)e + 1);
@@ -185,7 +189,11 @@ static void launch_project_t(const aim_plan* p, const C* x, C* Q, int R, cudaStr
     if (R == 1) {
         // lanes per node ~ entries per node / 4 (power of two in [4, 32])
         const double per = p->Ng ? (double)p->nnzP / (double)p->Ng : 1.0;
-        const int G = per > 96 ? 32 : per > 48 ? 16 : per > 24 ? 8 : 4;
+#ifndef AIM_P1_DIV
+#define AIM_P1_DIV 8
+#endif
+        const double pl = per / AIM_P1_DIV;   // entries per lane ~ AIM_P1_DIV
+        const int G = pl > 24 ? 32 : pl > 12 ? 16 : pl > 6 ? 8 : 4;
 #define P1(GG) project1_kernel<GG, C><<<nblk(p->Ng * GG, 256), 256, 0, s>>>(p->prow, p->pn, W, x, p->Ng, Q)
         if (G == 32) P1(32);
         else if (G == 16) P1(16);
