@@ -96,7 +96,10 @@ __device__ __forceinline__ void tile_range(int tiles, int& t0, int& t1) {
 // Compile-time ping-pong plans (CtpPlan<lines, threads, P, radices...>) of the
 // lengths the BASELINE configs use; other lengths run the runtime-radix
 // kernels.  Radices <= 7: one butterfly's registers stay small.
-using Ct210 = CtpPlan<8, 336, 210, 7, 6, 5>;      // x passes of C2: 8 lines (128 B rows)
+#ifndef AIM_CT210_NL
+#define AIM_CT210_NL 8
+#endif
+using Ct210 = CtpPlan<AIM_CT210_NL, 42 * AIM_CT210_NL, 210, 7, 6, 5>;   // x passes of C2: 8 lines (128 B rows)
 using Ct24 = CtpPlan<32, 192, 24, 6, 4>;          // x passes of C1 (1 RHS): 32 lines
 using Ct243 = CtpPlan<8, 216, 243, 9, 9, 3>;      // every axis of C5
 using Ct486 = CtpPlan<4, 216, 486, 9, 9, 6>;      // x and y passes of C3
