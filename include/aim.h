@@ -263,6 +263,13 @@ int aim_slab_create(const double* vertices, int64_t nv, const int32_t* triangles
  * call it (collective). */
 int aim_slab_matvec(aim_slab* slab, const void* x, void* y, int32_t nrhs, void* stream);
 
+/* aim_gmres on the slab-decomposed operator (D15).  V, J:
+ * device complex128 [N], replicated: every rank runs the identical iteration
+ * (the Krylov vectors are replicated; only the products are distributed).
+ * Collective with NCCL.  Synchronous.  Returns as aim_gmres. */
+int aim_slab_gmres(aim_slab* slab, const void* V, void* J, int32_t restart, double tol,
+                   int32_t max_iters, int32_t fixed_iters, int32_t* iters, double* rel_res);
+
 /* Host: out[10] = {X[r], X[r+1], KY[r], KY[r+1] (owned ky range of the
  * x-pencil phase), n0, n1 (rank r's rows in the permuted order), local near
  * nnz (-1 if rank r is not held here), all-to-all bytes per RHS and matvec

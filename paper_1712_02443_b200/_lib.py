@@ -47,6 +47,7 @@ SIGNATURES = [
     ("aim_nccl_unique_id", I32, [P, I64]),
     ("aim_slab_create", I32, [P, I64, P, I64, P, I64, D, D, I32, D, I32, I32, P, ctypes.POINTER(P)]),
     ("aim_slab_matvec", I32, [P, P, P, I32, P]),
+    ("aim_slab_gmres", I32, [P, P, P, I32, D, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]),
     ("aim_slab_query", I32, [P, I32, P]),
     ("aim_slab_destroy", I32, [P]),
     ("aim_last_error", ctypes.c_char_p, []),

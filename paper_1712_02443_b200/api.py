@@ -275,6 +275,17 @@ class AimSlabPlan:
                                            _stream()))
         return y
 
+    def gmres(self, V, restart=50, tol=1e-4, max_iters=0, fixed_iters=0):
+        torch = _torch()
+        J = torch.empty_like(V)
+        it = ctypes.c_int32()
+        rr = ctypes.c_double()
+        torch.cuda.current_stream().synchronize()
+        st = _check(_lib.load().aim_slab_gmres(self._p, _dev_ptr(V, self.N, 1), _dev_ptr(J, self.N, 1), int(restart),
+                                               float(tol), int(max_iters), int(fixed_iters), ctypes.byref(it),
+                                               ctypes.byref(rr)))
+        return J, int(it.value), float(rr.value), STATUS[st]
+
     def close(self):
         if getattr(self, "_p", None):
             _lib.load().aim_slab_destroy(self._p)

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -293,6 +294,9 @@ void ensure_workspace(aim_plan* p, int R);
 void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
 
 // ---- GMRES (k_gmres.cu)
+int gmres_with(aim_plan* p, const std::function<void(const double2*, double2*, cudaStream_t)>& mv,
+               const double2* b, double2* x, int restart, double tol, int max_iters, int fixed_iters,
+               int* iters_out, double* rel_out);
 int gmres(aim_plan* p, const double2* V, double2* J, int restart, double tol, int max_iters, int fixed_iters,
           int* iters, double* rel_res);
 

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <complex>
+#include <functional>
 #include <vector>
 
 #include "aim_internal.cuh"
@@ -128,6 +129,16 @@ struct Gm {
 
 int gmres(aim_plan* p, const double2* b, double2* x, int restart, double tol, int max_iters, int fixed_iters,
           int* iters_out, double* rel_out) {
+    return gmres_with(p, [p](const double2* in, double2* out, cudaStream_t st) { matvec(p, in, out, 1, st); }, b, x,
+                      restart, tol, max_iters, fixed_iters, iters_out, rel_out);
+}
+
+// The solver with any operator: `p` holds the workspace (and N, the stream),
+// `mv` applies the operator (single plan, or the slab-decomposed product with
+// replicated vectors -- every rank then runs the identical iteration).
+int gmres_with(aim_plan* p, const std::function<void(const double2*, double2*, cudaStream_t)>& mv,
+               const double2* b, double2* x, int restart, double tol, int max_iters, int fixed_iters,
+               int* iters_out, double* rel_out) {
     if (restart < 1 || restart + 1 > kMaxBasis) throw Error(AIM_E_ARG, "restart must be in [1, 1023]");
     if (max_iters <= 0) max_iters = 20000;
     const long long N = p->N;
@@ -170,7 +181,7 @@ int gmres(aim_plan* p, const double2* b, double2* x, int restart, double tol, in
         int jd = 0;
         bool stop = false;
         for (int j = 0; j < restart; ++j) {
-            matvec(p, V + (size_t)j * N, w, 1, s);
+            mv(V + (size_t)j * N, w, s);
             // CGS2: two classical Gram-Schmidt passes
             g.dots(V, j + 1, w, h1.data());
             g.axpy(V, j + 1, h1.data(), -1.0, w);
@@ -218,7 +229,7 @@ int gmres(aim_plan* p, const double2* b, double2* x, int restart, double tol, in
         }
         if (jd) g.axpy(V, jd, yv.data(), +1.0, x);
         // true residual r = b - A x into V[0]
-        matvec(p, x, w, 1, s);
+        mv(x, w, s);
         residual_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(b, w, N, V);
         note_launch("gmres_residual");
         beta = g.norm(V);

@@ -850,6 +850,21 @@ int aim_slab_matvec(aim_slab* S, const void* x, void* y, int32_t nrhs, void* str
     });
 }
 
+int aim_slab_gmres(aim_slab* S, const void* V, void* J, int32_t restart, double tol, int32_t max_iters,
+                   int32_t fixed_iters, int32_t* iters, double* rel_res) {
+    if (!S || !V || !J || restart < 1 || !(tol >= 0)) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        int it = 0;
+        double rr = 0;
+        const int st = gmres_with(
+            S->base, [S](const double2* in, double2* out, cudaStream_t s) { slab_matvec(S, in, out, 1, s); },
+            (const double2*)V, (double2*)J, restart, tol, max_iters, fixed_iters, &it, &rr);
+        if (iters) *iters = it;
+        if (rel_res) *rel_res = rr;
+        return st;
+    });
+}
+
 int aim_slab_query(const aim_slab* S, int32_t rank, int64_t* out) {
     if (!S || !out || rank < 0 || rank >= S->world) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {
