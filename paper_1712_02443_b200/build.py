@@ -39,6 +39,9 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None, de
         elif verbose and out:
             sys.stderr.write(out)
     if err:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
         raise RuntimeError("CUDA build failed")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs, "-lcudart"]
     subprocess.run(cmd, check=True)
