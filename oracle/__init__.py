@@ -9,8 +9,7 @@ arithmetic).
 
 Plain, slow, obviously-correct numpy in float64/complex128.  Every function
 cites the passage of PAPER.md (or the SURVEY.md §8(c) reading, "D#") it
-follows.  Library primitives used as single steps: numpy.fft (convolution),
-scipy.sparse (sparse products), numpy.linalg (dense solves, tiny cases).
+follows.  Library primitives used as single steps: scipy.sparse (sparse products), numpy.linalg (dense solves, tiny cases).
 
 Modules
   constants   eta0, default k                              (D1)
@@ -18,6 +17,7 @@ Modules
   green       G(R), smooth part G_s                        (D6, D8)
   potentials  analytic 1/R and (rho'-rho)/R triangle integrals   (D8)
   efie        exact Galerkin EFIE entries, dense Z         (D1, D8, D9)
+  fft         the oracle's own radix-2 FFT (and the direct DFT) (north_star)
   aim         stencils, weights, projection, convolution, interpolation,
               near list, precorrection, matvec             (D2-D6, D11, D12)
   excitation  plane-wave RHS                               (D14)

@@ -31,6 +31,7 @@ import scipy.sparse as sp
 
 from .constants import ETA0
 from .efie import EfieContext, efie_entries_sym
+from .fft import fftn_radix2
 from .green import green_grid
 
 
@@ -151,18 +152,20 @@ class OraclePlan:
         return np.stack([H @ Qf[c] for c in range(4)]).reshape(sh)
 
     def convolve_fft(self, Q, pads=None):
-        """Phi = H Q by zero-padded FFT with the min-image kernel (D11, D12)."""
+        """Phi = H Q by zero-padded FFT with the min-image kernel (D11, D12),
+        on power-of-two padded sizes with the oracle's own radix-2 FFT
+        (oracle/fft.py; north_star "its own radix-2 FFT")."""
         dims = tuple(int(d) for d in self.dims)
         if pads is None:
             pads = tuple(int(2 ** np.ceil(np.log2(2 * d - 1))) if d > 1 else 1 for d in dims)
         K = self.kernel_samples(pads)
-        Kh = np.fft.fftn(K)
+        Kh = fftn_radix2(K)
         out = np.empty_like(Q)
         for c in range(Q.shape[0]):
             for r in range(Q.shape[-1]):
                 q = np.zeros(pads, dtype=np.complex128)
                 q[: dims[0], : dims[1], : dims[2]] = Q[c, ..., r]
-                phi = np.fft.ifftn(np.fft.fftn(q) * Kh)
+                phi = fftn_radix2(fftn_radix2(q) * Kh, inverse=True)
                 out[c, ..., r] = phi[: dims[0], : dims[1], : dims[2]]
         return out
 

@@ -246,3 +246,88 @@ def test_dense_agreement():
     # the near part of Z_eq reproduces dense entries exactly on near pairs
     asym = np.linalg.norm(Z - Z.T)
     assert asym == 0
+
+
+# ------------------------------------------------ the oracle's own FFT (north_star)
+@pytest.mark.parametrize("P", [1, 2, 4, 8, 16, 32, 64])
+def test_radix2_fft_vs_direct_dft(P):
+    """oracle/fft.py radix-2 Cooley-Tukey == the O(P^2) definition, both
+    directions, along every axis of a 3-D array; inverse(forward) = identity."""
+    from oracle.fft import dft_direct, fft_radix2
+    rng = np.random.default_rng(P)
+    a = rng.standard_normal((3, P, 5)) + 1j * rng.standard_normal((3, P, 5))
+    for inv in (False, True):
+        f = fft_radix2(a, axis=1, inverse=inv)
+        d = dft_direct(a, axis=1, inverse=inv)
+        assert np.abs(f - d).max() <= 1e-13 * max(1.0, np.abs(d).max())
+    assert np.abs(fft_radix2(fft_radix2(a, axis=1), axis=1, inverse=True) - a).max() <= 1e-14 * P
+    # cross-check against a library FFT (test only; the oracle never calls it)
+    assert np.abs(fft_radix2(a, axis=1) - np.fft.fft(a, axis=1)).max() <= 1e-13 * max(1.0, np.abs(a).sum())
+
+
+def test_radix2_fft_closed_forms():
+    """Delta -> all ones; a single exponential exp(2 pi i k0 n / P) -> P at k0;
+    a 3-D separable product transforms to the product of the 1-D transforms."""
+    from oracle.fft import fft_radix2, fftn_radix2
+    P = 256
+    d = np.zeros(P, complex)
+    d[0] = 1
+    assert np.abs(fft_radix2(d) - 1).max() <= 1e-15
+    k0 = 37
+    e = np.exp(2j * np.pi * k0 * np.arange(P) / P)
+    F = fft_radix2(e)
+    ref = np.zeros(P, complex)
+    ref[k0] = P
+    assert np.abs(F - ref).max() <= 1e-11
+    rng = np.random.default_rng(9)
+    u, v, w = (rng.standard_normal(n) + 1j * rng.standard_normal(n) for n in (8, 16, 4))
+    A = np.einsum("i,j,k->ijk", u, v, w)
+    B = np.einsum("i,j,k->ijk", fft_radix2(u), fft_radix2(v), fft_radix2(w))
+    assert np.abs(fftn_radix2(A) - B).max() <= 1e-12 * np.abs(B).max()
+    with pytest.raises(ValueError):
+        fft_radix2(np.ones(12))
+
+
+def test_oracle_convolution_uses_own_fft():
+    """oracle/aim.py performs no library FFT in its arithmetic."""
+    import inspect
+    import oracle.aim as A
+    src = inspect.getsource(A)
+    assert "np.fft" not in src and "numpy.fft" not in src and "scipy.fft" not in src
+
+
+# ------------------------------ the row-sampled checker used by the full-size tests
+@pytest.mark.parametrize("name", ["c1", "t_m3", "t_vol", "t_dissim"])
+@pytest.mark.parametrize("R", [1, 3])
+def test_matvec_rows_equals_full_matvec(name, R):
+    """OraclePlan.matvec_rows (far field by the FFT path, interpolation and
+    near rows restricted to `rows`) is the reference of every full-size GPU
+    parity test: it must equal the rows of the full product, computed through
+    the sparse P^T interpolation and the full near matrix.  (t_dissim: its
+    full near matrix takes minutes to build, so there the near rows are
+    checked against the rows of a larger row set that contains them, and the
+    far rows against the full far field.)"""
+    P = oracle_plan(name)
+    x = make_vectors(P.N, R, 4)
+    rng = np.random.default_rng(R)
+    rows = np.unique(np.concatenate([[0, P.N - 1], rng.integers(0, P.N, 40)]))
+    part = P.matvec_rows(x, rows, method="fft")
+    Phi = P.convolve_fft(P.project(x))
+    far_full = P.interpolate(Phi)
+    scale = np.abs(part).max()
+    assert np.abs(P.interpolate(Phi, rows) - far_full[rows]).max() <= 1e-13 * scale
+    assert np.abs(P.far(x, "fft", rows=rows) - far_full[rows]).max() <= 1e-13 * scale
+    if name != "t_dissim":
+        full = P.matvec(x, method="fft")
+        assert np.abs(part - full[rows]).max() <= 1e-13 * np.abs(full).max()
+        Zr = P.near_matrix(rows).toarray()
+        assert np.abs(Zr - P.near_full()[rows].toarray()).max() <= 1e-15 * np.abs(Zr).max()
+    else:
+        sup = np.unique(np.concatenate([rows, rng.integers(0, P.N, 60)]))
+        pos = np.searchsorted(sup, rows)
+        Zr = P.near_matrix(rows).toarray()
+        assert np.abs(Zr - P.near_matrix(sup).toarray()[pos]).max() <= 1e-15 * np.abs(Zr).max()
+        assert np.abs(part - (far_full[rows] + P.near_matrix(sup)[pos] @ x)).max() <= 1e-13 * scale
+    # the direct-sum far field agrees with the FFT far field on the sampled rows
+    if P.Ng <= 4000:
+        assert np.abs(P.matvec_rows(x, rows, method="direct") - part).max() <= 1e-12 * np.abs(part).max()
