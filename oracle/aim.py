@@ -197,14 +197,26 @@ class OraclePlan:
         return np.nonzero(d <= self.r * (1.0 + 1e-9))[0]
 
     def near_pairs(self, rows=None, chunk=512):
+        """D5 near list of `rows` as CSR (row_ptr, sorted columns).
+
+        Candidates come from a k-d tree ball query (scipy.spatial, a library
+        neighbour search used as one step) with a radius 1e-6 larger than
+        D5's; each candidate is then kept iff the D5 test on the same
+        distance formula as near_columns holds, so the list equals the
+        brute-force one (pinned in tests/test_oracle_aim.py)."""
+        from scipy.spatial import cKDTree
         rows = np.arange(self.N) if rows is None else np.asarray(rows)
+        if getattr(self, "_tree", None) is None:
+            self._tree = cKDTree(self.centres)
         rp, cols = [0], []
         lim = self.r * (1.0 + 1e-9)
         for s in range(0, rows.size, chunk):
             rr = rows[s:s + chunk]
-            d = np.sqrt(((self.centres[rr][:, None, :] - self.centres[None, :, :]) ** 2).sum(axis=2))
+            cand = self._tree.query_ball_point(self.centres[rr], self.r * (1.0 + 1e-6) + 1e-12)
             for i in range(rr.size):
-                c = np.nonzero(d[i] <= lim)[0]
+                c = np.sort(np.asarray(cand[i], dtype=np.int64))
+                d = np.sqrt(((self.centres[c] - self.centres[rr[i]]) ** 2).sum(axis=1))
+                c = c[d <= lim]
                 cols.append(c)
                 rp.append(rp[-1] + c.size)
         return np.asarray(rp), (np.concatenate(cols) if cols else np.zeros(0, np.int64))

@@ -331,3 +331,18 @@ def test_matvec_rows_equals_full_matvec(name, R):
     # the direct-sum far field agrees with the FFT far field on the sampled rows
     if P.Ng <= 4000:
         assert np.abs(P.matvec_rows(x, rows, method="direct") - part).max() <= 1e-12 * np.abs(part).max()
+
+
+@pytest.mark.parametrize("name", ["c1", "t_m3", "t_dissim", "t_vol"])
+def test_near_pairs_equal_brute_force(name):
+    """D5: the k-d tree candidate search returns exactly the brute-force list
+    ||c_m - c_n|| <= r (1 + 1e-9) over all n (near_columns), ties included."""
+    P = oracle_plan(name)
+    rows = np.unique(np.concatenate([[0, P.N - 1], np.random.default_rng(5).integers(0, P.N, 300)]))
+    rp, cols = P.near_pairs(rows)
+    for i, m in enumerate(rows):
+        assert np.array_equal(cols[rp[i]:rp[i + 1]], P.near_columns(m)), m
+    for r in (0.0, 10.0):   # degenerate radii: self pairs only / everything
+        Q = OraclePlan(make_mesh("t_one"), 2 * np.pi, 0.1, 2, r)
+        rp, cols = Q.near_pairs()
+        assert rp[-1] == (Q.N if r == 0 else Q.N ** 2)
