@@ -52,7 +52,10 @@ typedef enum aim_status {
     AIM_E_GRID = -3,       /* grid or index space exceeds 32-bit addressing    */
     AIM_E_NOMEM = -4,      /* device allocation failed                         */
     AIM_E_CUDA = -5,       /* CUDA runtime / launch error                      */
-    AIM_E_NCCL = -6        /* NCCL failure (slab-decomposed multi-GPU path)     */
+    AIM_E_NCCL = -6,       /* NCCL failure (slab-decomposed multi-GPU path)     */
+    AIM_E_BREAKDOWN = -7   /* aim_gmres: a non-finite value (NaN/Inf) in the
+                              right-hand side, an Arnoldi coefficient, the
+                              Hessenberg solve or the residual; J unspecified  */
 } aim_status;
 
 enum { AIM_C128 = 0, AIM_C64 = 1 };
@@ -142,6 +145,20 @@ int aim_matvec(aim_plan* plan, const void* x, void* y, int32_t nrhs, void* strea
 int aim_matvec_host(aim_plan* plan, const void* x_host, void* y_host, int32_t nrhs);
 
 /*
+ * aim_matvec_host_steps -- `nsteps` products y_i := Z_eq x_i from HOST buffers
+ * with the copies overlapped (end-to-end path for a stream of inputs): step
+ * i's host->device copy, step i-1's product and step i-2's device->host copy
+ * run concurrently on three streams (two device slots per direction, ordered
+ * by events).  xs[i], ys[i]: host pointers to [N][nrhs] complex128
+ * (complex64 for AIM_C64 plans); page-locked memory is needed for the copies
+ * to overlap (pageable memory works, serialised).  xs[i] may repeat a
+ * pointer; ys[i] must not alias another ys[j] written concurrently (j = i+-1).
+ * Synchronous: returns when every y_i is in host memory.
+ */
+int aim_matvec_host_steps(aim_plan* plan, const void* const* xs, void* const* ys, int32_t nsteps,
+                          int32_t nrhs);
+
+/*
  * aim_gmres -- solve Z_eq J = V by restarted GMRES(restart) from J0 = 0
  * (reading D15: CGS2 Arnoldi, complex Givens rotations,
  * stop when ||V - Z J|| / ||V|| <= tol, the true residual being recomputed
@@ -156,7 +173,40 @@ int aim_gmres(aim_plan* plan, const void* V, void* J, int32_t restart, double to
               int32_t max_iters, int32_t fixed_iters, int32_t* iters, double* rel_res);
 
 /*
- * aim_planewave_rhs -- V_m = <Lambda_m, E_inc>, E_inc(r) = E0 pol exp(-j k khat.r)
+ * aim_gmres_history -- the residual estimates |g_{j+1}| / ||V|| of every
+ * inner iteration of the last aim_gmres / aim_slab_gmres on this plan (D15),
+ * in order.  out: host float64 [cap] (may be NULL when cap == 0); *count
+ * receives the number of iterations (copies min(count, cap) values).  Host.
+ */
+int aim_gmres_history(const aim_plan* plan, double* out, int32_t cap, int32_t* count);
+
+/* ---- block-Jacobi preconditioner -------------- */
+/* The paper preconditions GMRES ("GMRES with an ILU-2 preconditioner",
+ * PAPER.md:682, §VI-A); SPEC.md:493-501 substitutes per-element dense block
+ * solves, which this library builds (reading D18):
+ *   M = blockdiag_e Z_ex_sym[e, e],
+ * e the connected surfaces of the mesh (the array elements' equivalent
+ * surfaces), Z_ex_sym the exact symmetrised Galerkin entries (D8, D9) over
+ * ALL RWG pairs of the element.  Elements that are translates of each other
+ * (same local topology, corners equal to 1e-9 of the element size) share one
+ * block ("only need to be calculated once for each distinct element",
+ * PAPER.md:422-425).  Blocks are inverted on the device (Gauss-Jordan with
+ * partial pivoting).  Once built, aim_gmres solves Z M^-1 u = V, J = M^-1 u
+ * (right preconditioning; residuals and tolerance refer to Z J = V). */
+enum { AIM_PRECOND_NONE = 0, AIM_PRECOND_BLOCK_JACOBI = 1 };
+/* Build (kind 1) or remove (kind 0) the preconditioner.  Synchronous.
+ * Errors: AIM_E_ARG (AIM_C64 plan, unknown kind), AIM_E_NOMEM,
+ * AIM_E_BREAKDOWN (a singular or non-finite block; nothing is kept). */
+int aim_precond_build(aim_plan* plan, int32_t kind);
+/* y := M^-1 x, device complex128 [N], no overlap.  Stream-ordered.
+ * AIM_E_ARG if no preconditioner is built. */
+int aim_precond_apply(aim_plan* plan, const void* x, void* y, void* stream);
+/* Host: out[5] = {built (0/1), elements, distinct blocks, largest block,
+ * bytes of the inverses}. */
+int aim_precond_info(const aim_plan* plan, int64_t* out);
+
+/*
+ * aim_planewave_rhs --V_m = <Lambda_m, E_inc>, E_inc(r) = E0 pol exp(-j k khat.r)
  * (PAPER.md:455-459 with the sign convention of D1; D14), 7-point rule.
  * khat, pol: host float64[3]; V: device complex128 [N].  Stream-ordered.
  */

@@ -35,7 +35,12 @@ SIGNATURES = [
     ("aim_plan_info", I32, [P, ctypes.POINTER(AimInfo)]),
     ("aim_matvec", I32, [P, P, P, I32, P]),
     ("aim_matvec_host", I32, [P, P, P, I32]),
+    ("aim_matvec_host_steps", I32, [P, P, P, I32, I32]),
     ("aim_gmres", I32, [P, P, P, I32, D, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]),
+    ("aim_gmres_history", I32, [P, P, I32, ctypes.POINTER(I32)]),
+    ("aim_precond_build", I32, [P, I32]),
+    ("aim_precond_apply", I32, [P, P, P, P]),
+    ("aim_precond_info", I32, [P, P]),
     ("aim_planewave_rhs", I32, [P, P, P, D, D, P, P]),
     ("aim_project", I32, [P, P, P, I32, P]),
     ("aim_convolve", I32, [P, P, P, I32, P]),

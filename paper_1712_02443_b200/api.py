@@ -13,7 +13,7 @@ import numpy as np
 from . import _lib
 
 STATUS = {0: "AIM_OK", 1: "AIM_NOT_CONVERGED", -1: "AIM_E_ARG", -2: "AIM_E_MESH", -3: "AIM_E_GRID",
-          -4: "AIM_E_NOMEM", -5: "AIM_E_CUDA", -6: "AIM_E_NCCL"}
+          -4: "AIM_E_NOMEM", -5: "AIM_E_CUDA", -6: "AIM_E_NCCL", -7: "AIM_E_BREAKDOWN"}
 C128, C64 = 0, 1   # aim_plan_create precision (AIM_C128, AIM_C64)
 EXPORT = {"bases": 0, "weights": 1, "near_rowptr": 2, "near_col": 3, "near_val": 4, "green": 5,
           "proj_rowptr": 6, "proj_ent": 7}
@@ -127,6 +127,21 @@ class AimPlan:
         _check(_lib.load().aim_matvec_host(self._p, x.ctypes.data, y.ctypes.data, nrhs))
         return y
 
+    def matvec_host_steps(self, xs, ys):
+        """aim_matvec_host_steps: y_i := Z x_i for host arrays (numpy, ideally
+        page-locked), copies overlapped with the products inside the library."""
+        n = len(xs)
+        if len(ys) != n:
+            raise ValueError("xs and ys differ in length")
+        nrhs = 1 if xs[0].ndim == 1 else xs[0].shape[1]
+        for a in list(xs) + list(ys):
+            if a.dtype != self.np_dtype or not a.flags.c_contiguous or a.size != self.N * nrhs:
+                raise TypeError("host arrays must be contiguous, of the plan's dtype and [N][nrhs]")
+        xp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in xs])
+        yp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in ys])
+        _check(_lib.load().aim_matvec_host_steps(self._p, xp, yp, n, nrhs))
+        return ys
+
     def gmres(self, V, restart=50, tol=1e-4, max_iters=0, fixed_iters=0):
         torch = _torch()
         J = torch.empty_like(V)
@@ -137,6 +152,31 @@ class AimPlan:
                                           float(tol), int(max_iters), int(fixed_iters), ctypes.byref(it),
                                           ctypes.byref(rr)))
         return J, int(it.value), float(rr.value), STATUS[st]
+
+    def gmres_history(self) -> np.ndarray:
+        """aim_gmres_history: |g_{j+1}|/||V|| of every inner iteration of the last solve."""
+        n = ctypes.c_int32()
+        _check(_lib.load().aim_gmres_history(self._p, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.float64)
+        _check(_lib.load().aim_gmres_history(self._p, out.ctypes.data if out.size else None, out.size,
+                                             ctypes.byref(n)))
+        return out
+
+    def precond_build(self, kind: int = 1):
+        """aim_precond_build: 1 = block-Jacobi over the mesh's connected surfaces, 0 = remove."""
+        _check(_lib.load().aim_precond_build(self._p, int(kind)))
+        return self.precond_info()
+
+    def precond_info(self) -> dict:
+        out = np.zeros(5, dtype=np.int64)
+        _check(_lib.load().aim_precond_info(self._p, out.ctypes.data))
+        return dict(zip(("built", "elements", "distinct", "max_block", "bytes"), (int(v) for v in out)))
+
+    def precond_apply(self, x):
+        torch = _torch()
+        y = torch.empty_like(x)
+        _check(_lib.load().aim_precond_apply(self._p, _dev_ptr(x, self.N, 1), _dev_ptr(y, self.N, 1), _stream()))
+        return y
 
     def planewave_rhs(self, khat=(0.0, 0.0, -1.0), pol=(1.0, 0.0, 0.0), E0=1.0 + 0j):
         torch = _torch()

@@ -185,6 +185,11 @@ void create_plan(const double* V, int64_t nv, const int32_t* T, int64_t nt, cons
         node0[n] = (int32_t)(((long long)(base[3 * n] - lo[0]) * p->dims[1] + (base[3 * n + 1] - lo[1])) * p->dims[2] +
                              (base[3 * n + 2] - lo[2]));
 
+    // host copies kept for the block-Jacobi preconditioner (element grouping)
+    p->h_tv = tv;
+    p->h_cor = cor;
+    p->h_rt = rt;
+
     // ---- uploads
     p->tri_qp = upload(p, qp);
     p->tri_qw = upload(p, qw);
@@ -235,6 +240,14 @@ void destroy_plan(aim_plan* p) {
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_x) cudaEventDestroy(p->ev_x);
     if (p->ev_n) cudaEventDestroy(p->ev_n);
+    if (p->gm_host) cudaFreeHost(p->gm_host);
+    if (p->hp_in) cudaStreamDestroy(p->hp_in);
+    if (p->hp_out) cudaStreamDestroy(p->hp_out);
+    for (int k = 0; k < 2; ++k) {
+        if (p->hp_ev_in[k]) cudaEventDestroy(p->hp_ev_in[k]);
+        if (p->hp_ev_mv[k]) cudaEventDestroy(p->hp_ev_mv[k]);
+        if (p->hp_ev_out[k]) cudaEventDestroy(p->hp_ev_out[k]);
+    }
     cudaSetDevice(cur);
     delete p;
 }
@@ -327,6 +340,55 @@ int aim_matvec_host(aim_plan* p, const void* xh, void* yh, int32_t nrhs) {
         AIM_CUDA(cudaMemcpyAsync(p->hx, xh, bytes, cudaMemcpyHostToDevice, s));
         matvec(p, p->hx, p->hy, nrhs, s);
         AIM_CUDA(cudaMemcpyAsync(yh, p->hy, bytes, cudaMemcpyDeviceToHost, s));
+        AIM_CUDA(cudaStreamSynchronize(s));
+        return AIM_OK;
+    });
+}
+
+int aim_matvec_host_steps(aim_plan* p, const void* const* xs, void* const* ys, int32_t nsteps, int32_t nrhs) {
+    if (!p || !xs || !ys || nrhs < 1 || nsteps < 0) return fail(AIM_E_ARG, "bad argument");
+    for (int i = 0; i < nsteps; ++i)
+        if (!xs[i] || !ys[i]) return fail(AIM_E_ARG, "NULL host buffer");
+    return guarded([&] {
+        const size_t elems = (size_t)p->N * nrhs;
+        const size_t bytes = (p->prec == AIM_C64 ? sizeof(float2) : sizeof(double2)) * elems;
+        // two device slots per direction; step i uses slot i % 2
+        if (p->hp_nrhs < nrhs) {
+            for (int k = 0; k < 2; ++k) {
+                p->release(p->hp_x[k]);
+                p->release(p->hp_y[k]);
+                p->hp_x[k] = p->alloc<double2>(elems);
+                p->hp_y[k] = p->alloc<double2>(elems);
+            }
+            p->hp_nrhs = nrhs;
+        }
+        if (!p->hp_in) {
+            AIM_CUDA(cudaStreamCreateWithFlags(&p->hp_in, cudaStreamNonBlocking));
+            AIM_CUDA(cudaStreamCreateWithFlags(&p->hp_out, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) {
+                AIM_CUDA(cudaEventCreateWithFlags(&p->hp_ev_in[k], cudaEventDisableTiming));
+                AIM_CUDA(cudaEventCreateWithFlags(&p->hp_ev_mv[k], cudaEventDisableTiming));
+                AIM_CUDA(cudaEventCreateWithFlags(&p->hp_ev_out[k], cudaEventDisableTiming));
+            }
+        }
+        cudaStream_t s = p->stream;
+        for (int i = 0; i < nsteps; ++i) {
+            const int k = i & 1;
+            // copy-in of step i once step i-2's product no longer reads the slot
+            if (i >= 2) AIM_CUDA(cudaStreamWaitEvent(p->hp_in, p->hp_ev_mv[k], 0));
+            AIM_CUDA(cudaMemcpyAsync(p->hp_x[k], xs[i], bytes, cudaMemcpyHostToDevice, p->hp_in));
+            AIM_CUDA(cudaEventRecord(p->hp_ev_in[k], p->hp_in));
+            // product of step i once its x landed and step i-2's y was copied out
+            AIM_CUDA(cudaStreamWaitEvent(s, p->hp_ev_in[k], 0));
+            if (i >= 2) AIM_CUDA(cudaStreamWaitEvent(s, p->hp_ev_out[k], 0));
+            matvec(p, p->hp_x[k], p->hp_y[k], nrhs, s);
+            AIM_CUDA(cudaEventRecord(p->hp_ev_mv[k], s));
+            // copy-out of step i
+            AIM_CUDA(cudaStreamWaitEvent(p->hp_out, p->hp_ev_mv[k], 0));
+            AIM_CUDA(cudaMemcpyAsync(ys[i], p->hp_y[k], bytes, cudaMemcpyDeviceToHost, p->hp_out));
+            AIM_CUDA(cudaEventRecord(p->hp_ev_out[k], p->hp_out));
+        }
+        AIM_CUDA(cudaStreamSynchronize(p->hp_out));
         AIM_CUDA(cudaStreamSynchronize(s));
         return AIM_OK;
     });
@@ -448,6 +510,48 @@ int64_t aim_launch_count(int32_t reset) {
     const long long v = g_launches;
     if (reset) g_launches = 0;
     return v;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int aim_precond_build(aim_plan* p, int32_t kind) {
+    if (!p) return fail(AIM_E_ARG, "NULL plan");
+    if (kind != AIM_PRECOND_NONE && kind != AIM_PRECOND_BLOCK_JACOBI) return fail(AIM_E_ARG, "unknown preconditioner");
+    if (kind == AIM_PRECOND_BLOCK_JACOBI && p->prec != AIM_C128)
+        return fail(AIM_E_ARG, "the preconditioner needs an AIM_C128 plan");
+    return guarded([&] {
+        if (kind == AIM_PRECOND_NONE) free_precond(p);
+        else build_precond(p, p->stream);
+        return AIM_OK;
+    });
+}
+
+int aim_precond_apply(aim_plan* p, const void* x, void* y, void* stream) {
+    if (!p || !x || !y || x == y) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        apply_precond(p, (const double2*)x, (double2*)y, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_precond_info(const aim_plan* p, int64_t* out) {
+    if (!p || !out) return fail(AIM_E_ARG, "bad argument");
+    out[0] = p->prec_on;
+    out[1] = p->pc_nblocks;
+    out[2] = p->pc_ndistinct;
+    out[3] = p->pc_maxn;
+    out[4] = p->pc_bytes;
+    return AIM_OK;
+}
+
+int aim_gmres_history(const aim_plan* p, double* out, int32_t cap, int32_t* count) {
+    if (!p || !count || cap < 0 || (cap > 0 && !out)) return fail(AIM_E_ARG, "bad argument");
+    const int32_t n = (int32_t)p->gm_hist.size();
+    for (int32_t i = 0; i < std::min(n, cap); ++i) out[i] = p->gm_hist[i];
+    *count = n;
+    return AIM_OK;
 }
 
 }  // extern "C"

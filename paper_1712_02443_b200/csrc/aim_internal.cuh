@@ -129,6 +129,13 @@ bool planar_supported(int Py, int Nz, int min_radix);
 void make_fft_axis(int P, FftAxis& ax);    // factorisation + device twiddles
 int smooth_size_at_least(int n);           // smallest 2^a 3^b 5^c 7^d >= n
 
+// block-Jacobi apply job: distinct inverse d (n x n at element offset ioff)
+// shared by m elements listed at pc_elist[eoff ..)
+struct PcJob {
+    int d, eoff, m, n;
+    int64_t ioff;
+};
+
 // -------------------------------------------------------------------- plan
 }  // namespace aim
 
@@ -155,6 +162,10 @@ struct aim_plan {
     double* rwg_c = nullptr;      // [N][3]   centre
     int32_t* base = nullptr;      // [N][3]   absolute stencil base
     int32_t* node0 = nullptr;     // [N]      grid index of the base node
+    // host copies (element grouping of the preconditioner)
+    std::vector<int32_t> h_tv;    // [nt][3] vertex ids
+    std::vector<double> h_cor;    // [nt][3][3] corners
+    std::vector<int32_t> h_rt;    // [N][2] t+, t-
 
     // operator tables (device)
     double* W = nullptr;          // [N][S][4] weights (x, y, z, phi)
@@ -215,15 +226,41 @@ struct aim_plan {
     double2* Q = nullptr;         // [4][Nx][Ny][Nz][R]   (also Phi)
     double2* W1 = nullptr;        // [4][Px][Ny][Nz][R]
     double2* W2 = nullptr;        // [4][Px][Py][Nz][R]
-    // GMRES workspace
+    // GMRES workspace (vectors of local length gm_n)
     int gm_restart = 0;
-    double2* gm_V = nullptr;      // [(restart+1)][N]
-    double2* gm_w = nullptr;      // [N]
-    double2* gm_part = nullptr;   // partial sums
+    long long gm_n = 0;
+    double2* gm_V = nullptr;      // [(restart+1)][n]
+    double2* gm_w = nullptr;      // [n]
+    double2* gm_z = nullptr;      // [n] preconditioned vector (right preconditioning)
+    double2* gm_part = nullptr;   // block partials + device coefficients
+    double2* gm_host = nullptr;   // pinned host mirror of the coefficients
+    std::vector<double> gm_hist;  // residual estimate |g_{j+1}|/||b|| of the last solve
+    // block-Jacobi preconditioner (aim_precond_build): one dense inverse per
+    // distinct element block; element e of the mesh uses inverse pc_map[e]
+    int prec_on = 0;
+    int pc_nblocks = 0;           // connected surfaces (elements)
+    int pc_ndistinct = 0;         // distinct inverses
+    int pc_maxn = 0;              // largest block
+    int32_t* pc_rows = nullptr;   // [N] RWG ids grouped by element (element-major)
+    int64_t* pc_rptr = nullptr;   // [nblocks+1] ranges into pc_rows
+    int32_t* pc_map = nullptr;    // [nblocks] distinct inverse of each element
+    int64_t* pc_iptr = nullptr;   // [ndistinct+1] offsets of the inverses (elements of double2)
+    double2* pc_inv = nullptr;    // inverses, row-major n_b x n_b each
+    int64_t pc_bytes = 0;
+    std::vector<aim::PcJob> pc_jobs;  // GEMM applies (inverses shared by >= 8 elements)
+    int32_t* pc_elist = nullptr;  // element lists of the jobs, then the GEMV elements
+    int pc_gemv_off = 0, pc_gemv_cnt = 0;
     // host staging for aim_matvec_host
     int hs_nrhs = 0;
     double2* hx = nullptr;
     double2* hy = nullptr;
+
+    // aim_matvec_host_steps: double-buffered device vectors, copy streams, events
+    int hp_nrhs = 0;
+    double2* hp_x[2] = {nullptr, nullptr};
+    double2* hp_y[2] = {nullptr, nullptr};
+    cudaStream_t hp_in = nullptr, hp_out = nullptr;
+    cudaEvent_t hp_ev_in[2] = {nullptr, nullptr}, hp_ev_mv[2] = {nullptr, nullptr}, hp_ev_out[2] = {nullptr, nullptr};
 
     // side stream for the near-field SpMV (overlaps the FFT passes)
     cudaStream_t side = nullptr;
@@ -294,10 +331,24 @@ void ensure_workspace(aim_plan* p, int R);
 void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
 
 // ---- GMRES (k_gmres.cu)
-int gmres_with(aim_plan* p, const std::function<void(const double2*, double2*, cudaStream_t)>& mv,
-               const double2* b, double2* x, int restart, double tol, int max_iters, int fixed_iters,
-               int* iters_out, double* rel_out);
+// Operator of a GMRES solve on vectors of local length n: matvec applies A,
+// precond (optional) M^-1 (right preconditioning), allreduce (optional) sums a
+// small device vector of complex values over the ranks (distributed Krylov
+// vectors; stream-ordered).
+struct GmresOps {
+    long long n = 0;
+    std::function<void(const double2*, double2*, cudaStream_t)> matvec;
+    std::function<void(const double2*, double2*, cudaStream_t)> precond;
+    std::function<void(double2*, int, cudaStream_t)> allreduce;
+};
+int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, int restart, double tol,
+               int max_iters, int fixed_iters, int* iters_out, double* rel_out);
 int gmres(aim_plan* p, const double2* V, double2* J, int restart, double tol, int max_iters, int fixed_iters,
           int* iters, double* rel_res);
+
+// ---- block-Jacobi preconditioner (k_precond.cu)
+void build_precond(aim_plan* p, cudaStream_t s);
+void apply_precond(aim_plan* p, const double2* in, double2* out, cudaStream_t s);
+void free_precond(aim_plan* p);
 
 }  // namespace aim

@@ -2,11 +2,20 @@
 // "we solve the linear system ... iteratively using the generalized minimal
 // residual (GMRES) algorithm"; reading D15).
 //
-// Krylov basis V [restart+1][N] and all vector work stay in HBM; the host
+// Krylov basis V [restart+1][n] and all vector work stay in HBM; the host
 // keeps only the (restart+1) x restart Hessenberg matrix and the Givens
-// rotations.  Arnoldi uses classical Gram-Schmidt applied twice (CGS2):
-// each pass is one fused multi-dot kernel (partials per block, fixed-order
-// second stage => deterministic) and one fused multi-axpy kernel.
+// rotations.  Arnoldi is classical Gram-Schmidt applied twice (CGS2) in three
+// passes over the basis per iteration (DESIGN.md §5 "GMRES"):
+//   pass 1  h1 = V^H w                                   (mdot_kernel)
+//   pass 2  w -= V h1, then h2 = V^H w, V read once      (axpy_dot_kernel)
+//   pass 3  w -= V h2 and ||w||^2                        (axpy_norm_kernel)
+// then v_{j+1} = w / ||w||.  Every coefficient is produced and consumed on
+// the device (fixed-order block partials -> deterministic); the host reads
+// h1, h2, ||w|| once per iteration (one synchronisation) for the Givens
+// rotations and the convergence test.  Distributed use: `allreduce` sums the
+// small coefficient vectors over the ranks between the partial and the use,
+// with the Krylov vectors partitioned by owning rank (k_slab.cu).
+// Right preconditioning (optional): A M^-1 u = b, x = M^-1 u.
 #include <math.h>
 
 #include <algorithm>
@@ -20,158 +29,389 @@ namespace aim {
 
 using cplx = std::complex<double>;
 
-static constexpr int kDotBlocks = 296;  // 2 x 148 SMs
-static constexpr int kDotThreads = 256;
+static constexpr int kGmBlocks = 296;   // 2 x 148 SMs
+static constexpr int kGmThreads = 512;  // 16 warps
+static constexpr int kGmWarps = kGmThreads / 32;
+static constexpr int kGmChunk = 64;     // basis vectors per pass
+static constexpr int kGmQ = kGmChunk / kGmWarps;   // basis vectors per warp (4)
 static constexpr int kMaxBasis = 1024;
 
-__constant__ double2 c_coef[kMaxBasis];
+__device__ __forceinline__ void cfma_conj(double2& acc, double2 v, double2 x) {   // acc += conj(v) x
+    acc.x = fma(v.x, x.x, fma(v.y, x.y, acc.x));
+    acc.y = fma(v.x, x.y, fma(-v.y, x.x, acc.y));
+}
+__device__ __forceinline__ void cfma(double2& acc, double2 c, double2 v) {        // acc += c v
+    acc.x = fma(c.x, v.x, fma(-c.y, v.y, acc.x));
+    acc.y = fma(c.x, v.y, fma(c.y, v.x, acc.y));
+}
+__device__ __forceinline__ double2 warp_sum(double2 s) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+    }
+    return s;
+}
 
-// partial[b][i] = sum_{e in block b's range} conj(V_i[e]) w[e], i < nv
-__global__ void __launch_bounds__(kDotThreads) multidot_kernel(const double2* __restrict__ V, long long N, int nv,
-                                                               const double2* __restrict__ w,
-                                                               double2* __restrict__ partial) {
-    __shared__ double2 red[kDotThreads / 32];
-    const long long chunk = (N + gridDim.x - 1) / gridDim.x;
-    const long long a = blockIdx.x * chunk, b = min(N, a + chunk);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x / 32;
-    for (int i = 0; i < nv; ++i) {
-        const double2* Vi = V + (long long)i * N;
-        double2 s = make_double2(0, 0);
-        for (long long e = a + threadIdx.x; e < b; e += blockDim.x) {
-            const double2 v = Vi[e], x = w[e];
-            s.x += v.x * x.x + v.y * x.y;
-            s.y += v.x * x.y - v.y * x.x;
+// partial[b][i] = sum_{e in block b's range} conj(V_i[e]) w[e], i < nv (nv <= 64).
+// 16 warps; warp g owns basis vectors i = g + 16 q (q < 4); each lane takes
+// U elements per step (e = base + lane + 32 u) so U x 4 loads are in flight;
+// w[e] is read from HBM once per block (the other warps hit L1).
+template <int U>
+__global__ void __launch_bounds__(kGmThreads) mdot_kernel(const double2* __restrict__ V, long long ld, long long n,
+                                                          int nv, const double2* __restrict__ w,
+                                                          double2* __restrict__ partial) {
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 32 * U - 1) / (32 * U) * (32 * U);
+    const long long a = blockIdx.x * chunk, b = min(n, a + chunk);
+    double2 acc[kGmQ];
+#pragma unroll
+    for (int q = 0; q < kGmQ; ++q) acc[q] = make_double2(0, 0);
+    if (g < nv) {
+        for (long long e0 = a + lane; e0 < b; e0 += 32 * U) {
+            double2 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long e = e0 + 32 * u;
+                x[u] = e < b ? __ldg(&w[e]) : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < kGmQ; ++q) {
+                const int i = g + kGmWarps * q;
+                if (i < nv) {
+                    double2 v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const long long e = e0 + 32 * u;
+                        v[u] = e < b ? __ldcs(&V[i * ld + e]) : make_double2(0, 0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) cfma_conj(acc[q], v[u], x[u]);
+                }
+            }
         }
-        for (int off = 16; off; off >>= 1) {
-            s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
-            s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
-        }
-        if (lane == 0) red[warp] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double2 t = make_double2(0, 0);
-            for (int q = 0; q < kDotThreads / 32; ++q) { t.x += red[q].x; t.y += red[q].y; }
-            partial[(long long)blockIdx.x * nv + i] = t;
-        }
-        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < kGmQ; ++q) {
+        const int i = g + kGmWarps * q;
+        const double2 s = warp_sum(acc[q]);
+        if (lane == 0 && i < nv) partial[(long long)blockIdx.x * kGmChunk + i] = s;
     }
 }
 
-// out[i] = sum_b partial[b][i] in block order
-__global__ void multidot_final(const double2* __restrict__ partial, int nb, int nv, double2* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// w -= sum_i c[i] V_i (c on the device), then partial dots of the updated w
+// with every V_i; V is read once.  Steps of 32 U elements: warp g forms
+// sum_{i in g} c_i V_i[e] from its registers, the 16 partial sums meet in
+// shared memory, every warp rebuilds w'[e] and accumulates conj(V_i[e]) w'[e].
+template <int U>
+__global__ void __launch_bounds__(kGmThreads, 2) axpy_dot_kernel(const double2* __restrict__ V, long long ld,
+                                                              long long n, int nv, const double2* __restrict__ c,
+                                                              double2* __restrict__ w,
+                                                              double2* __restrict__ partial) {
+    __shared__ double2 red[kGmWarps][32 * U];
+    __shared__ double2 xs[32 * U];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 32 * U - 1) / (32 * U) * (32 * U);
+    const long long a = blockIdx.x * chunk, b = min(n, a + chunk);
+    double2 cc[kGmQ], acc[kGmQ];
+#pragma unroll
+    for (int q = 0; q < kGmQ; ++q) {
+        const int i = g + kGmWarps * q;
+        cc[q] = i < nv ? c[i] : make_double2(0, 0);
+        acc[q] = make_double2(0, 0);
+    }
+    for (long long e0 = a + lane; e0 < b + lane; e0 += 32 * U) {
+        double2 sm[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) sm[u] = make_double2(0, 0);
+        {
+            double2 v[kGmQ][U];
+#pragma unroll
+            for (int q = 0; q < kGmQ; ++q) {
+                const int i = g + kGmWarps * q;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const long long e = e0 + 32 * u;
+                    v[q][u] = (e < b && i < nv) ? __ldg(&V[i * ld + e]) : make_double2(0, 0);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kGmQ; ++q)
+#pragma unroll
+                for (int u = 0; u < U; ++u) cfma(sm[u], cc[q], v[q][u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) red[g][lane + 32 * u] = sm[u];
+        __syncthreads();
+        // the first 32 U threads rebuild w' = w - sum_g red[g] for the step's elements
+        if (threadIdx.x < 32 * U) {
+            const int t = threadIdx.x;
+            const long long e = e0 - lane + t;
+            const bool live = e < b;
+            double2 x = live ? w[e] : make_double2(0, 0);
+#pragma unroll
+            for (int q = 0; q < kGmWarps; ++q) {
+                x.x -= red[q][t].x;
+                x.y -= red[q][t].y;
+            }
+            xs[t] = x;
+            if (live) w[e] = x;
+        }
+        __syncthreads();
+        // second read of the step's V tile: L1 hits (read a moment ago with the
+        // default caching), so V costs HBM traffic once and no registers across
+        // the barriers (2 CTAs per SM)
+#pragma unroll
+        for (int q = 0; q < kGmQ; ++q) {
+            const int i = g + kGmWarps * q;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long e = e0 + 32 * u;
+                const double2 v = (e < b && i < nv) ? __ldcs(&V[i * ld + e]) : make_double2(0, 0);
+                cfma_conj(acc[q], v, xs[lane + 32 * u]);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kGmQ; ++q) {
+        const int i = g + kGmWarps * q;
+        const double2 s = warp_sum(acc[q]);
+        if (lane == 0 && i < nv) partial[(long long)blockIdx.x * kGmChunk + i] = s;
+    }
+}
+
+// w -= sum_i c[i] V_i, and partial[b] = sum |w|^2 over block b's elements
+// (thread per element, coefficients staged in shared memory).
+__global__ void __launch_bounds__(kGmThreads) axpy_norm_kernel(const double2* __restrict__ V, long long ld,
+                                                               long long n, int nv, const double2* __restrict__ c,
+                                                               double2* __restrict__ w,
+                                                               double2* __restrict__ partial, int want_norm) {
+    __shared__ double2 cs[kGmChunk];
+    __shared__ double red[kGmWarps];
+    if (threadIdx.x < nv) cs[threadIdx.x] = c[threadIdx.x];
+    __syncthreads();
+    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const long long a = blockIdx.x * chunk, b = min(n, a + chunk);
+    double nrm = 0.0;
+    for (long long e = a + threadIdx.x; e < b; e += blockDim.x) {
+        double2 x = w[e];
+#pragma unroll 8
+        for (int i = 0; i < nv; ++i) {
+            const double2 ci = cs[i];
+            const double2 v = __ldcs(&V[i * ld + e]);
+            x.x -= ci.x * v.x - ci.y * v.y;
+            x.y -= ci.x * v.y + ci.y * v.x;
+        }
+        w[e] = x;
+        nrm = fma(x.x, x.x, fma(x.y, x.y, nrm));
+    }
+    if (!want_norm) return;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int q = 0; q < kGmWarps; ++q) t += red[q];
+        partial[(long long)blockIdx.x * kGmChunk] = make_double2(t, 0.0);
+    }
+}
+
+// out[i] (+)= sum_b partial[b][i], blocks in order (deterministic).
+// Warp per i: lane l sums blocks l, l + 32, ..., then a fixed shuffle tree.
+__global__ void gm_reduce_kernel(const double2* __restrict__ partial, int nb, int nv, double2* __restrict__ out,
+                                 int accumulate) {
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (i >= nv) return;
     double2 t = make_double2(0, 0);
-    for (int b = 0; b < nb; ++b) { t.x += partial[(long long)b * nv + i].x; t.y += partial[(long long)b * nv + i].y; }
-    out[i] = t;
-}
-
-// w[e] += sign * sum_i coef[i] V_i[e]
-__global__ void multiaxpy_kernel(const double2* __restrict__ V, long long N, int nv, double sign,
-                                 double2* __restrict__ w) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= N) return;
-    double2 acc = w[e];
-    for (int i = 0; i < nv; ++i) {
-        const double2 c = c_coef[i], v = V[(long long)i * N + e];
-        acc.x += sign * (c.x * v.x - c.y * v.y);
-        acc.y += sign * (c.x * v.y + c.y * v.x);
+    for (int b = lane; b < nb; b += 32) {
+        const double2 v = partial[(long long)b * kGmChunk + i];
+        t.x += v.x;
+        t.y += v.y;
     }
-    w[e] = acc;
+    t = warp_sum(t);
+    if (lane) return;
+    if (accumulate) {
+        out[i].x += t.x;
+        out[i].y += t.y;
+    } else {
+        out[i] = t;
+    }
 }
 
-__global__ void scale_copy_kernel(const double2* __restrict__ a, long long N, double s, double2* __restrict__ b) {
+// dst = src / sqrt(nrm2->x)   (nrm2 on the device)
+__global__ void gm_scale_kernel(const double2* __restrict__ src, long long n, const double2* __restrict__ nrm2,
+                                double2* __restrict__ dst) {
+    const double s = 1.0 / sqrt(nrm2->x);
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < N) b[e] = make_double2(a[e].x * s, a[e].y * s);
+    if (e < n) dst[e] = make_double2(src[e].x * s, src[e].y * s);
+}
+
+// out (+)= sum_i y[i] V_i
+__global__ void gm_combine_kernel(const double2* __restrict__ V, long long ld, long long n, int nv,
+                                  const double2* __restrict__ y, double2* __restrict__ out, int accumulate) {
+    __shared__ double2 ys[kGmChunk];
+    if (threadIdx.x < nv) ys[threadIdx.x] = y[threadIdx.x];
+    __syncthreads();
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double2 acc = accumulate ? out[e] : make_double2(0, 0);
+    for (int i = 0; i < nv; ++i) cfma(acc, ys[i], V[i * ld + e]);
+    out[e] = acc;
 }
 
 // r = b - Ax
-__global__ void residual_kernel(const double2* __restrict__ b, const double2* __restrict__ Ax, long long N,
+__global__ void residual_kernel(const double2* __restrict__ b, const double2* __restrict__ Ax, long long n,
                                 double2* __restrict__ r) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < N) r[e] = make_double2(b[e].x - Ax[e].x, b[e].y - Ax[e].y);
+    if (e < n) r[e] = make_double2(b[e].x - Ax[e].x, b[e].y - Ax[e].y);
 }
 
-struct Gm {
+__global__ void add_kernel(const double2* __restrict__ a, long long n, double2* __restrict__ x) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) x[e] = make_double2(x[e].x + a[e].x, x[e].y + a[e].y);
+}
+
+namespace {
+
+struct Vec {
     aim_plan* p;
     cudaStream_t s;
-    double2* part;
-    double2* dres;
-    std::vector<double2> hbuf;
+    long long n;
+    double2* part;        // [kGmBlocks][kGmChunk]
+    double2* dcoef;       // [3][kMaxBasis + 1] device coefficients: h1, h2, misc
+    const GmresOps& ops;
 
-    void dots(const double2* V, int nv, const double2* w, cplx* out) {
-        multidot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(V, p->N, nv, w, part);
-        note_launch("gmres_multidot");
-        multidot_final<<<(nv + 127) / 128, 128, 0, s>>>(part, kDotBlocks, nv, dres);
-        note_launch("gmres_multidot_final");
-        hbuf.resize(nv);
-        AIM_CUDA(cudaMemcpyAsync(hbuf.data(), dres, sizeof(double2) * nv, cudaMemcpyDeviceToHost, s));
-        AIM_CUDA(cudaStreamSynchronize(s));
-        for (int i = 0; i < nv; ++i) out[i] = cplx(hbuf[i].x, hbuf[i].y);
+    unsigned nb() const { return (unsigned)((n + 255) / 256); }
+    void reduce(int nv, double2* out, bool acc) {
+        gm_reduce_kernel<<<(nv + 7) / 8, 256, 0, s>>>(part, kGmBlocks, nv, out, acc ? 1 : 0);
+        note_launch("gmres_reduce");
     }
-    double norm(const double2* w) {
-        cplx d;
-        dots(w, 1, w, &d);
-        return sqrt(std::max(0.0, d.real()));
+    void allreduce(double2* d, int nv) {
+        if (ops.allreduce) ops.allreduce(d, nv, s);
     }
-    void axpy(const double2* V, int nv, const cplx* c, double sign, double2* w) {
-        std::vector<double2> h(nv);
-        for (int i = 0; i < nv; ++i) h[i] = make_double2(c[i].real(), c[i].imag());
-        AIM_CUDA(cudaMemcpyToSymbolAsync(c_coef, h.data(), sizeof(double2) * nv, 0, cudaMemcpyHostToDevice, s));
-        multiaxpy_kernel<<<(unsigned)((p->N + 255) / 256), 256, 0, s>>>(V, p->N, nv, sign, w);
-        note_launch("gmres_multiaxpy");
+    // out[0..nv) = V^H w (device)
+    void dots(const double2* V, int nv, const double2* w, double2* out) {
+        for (int i0 = 0; i0 < nv; i0 += kGmChunk) {
+            const int m = std::min(kGmChunk, nv - i0);
+            mdot_kernel<4><<<kGmBlocks, kGmThreads, 0, s>>>(V + (size_t)i0 * n, n, n, m, w, part);
+            note_launch("gmres_mdot");
+            reduce(m, out + i0, false);
+        }
+        allreduce(out, nv);
     }
-    void scale(const double2* a, double f, double2* b) {
-        scale_copy_kernel<<<(unsigned)((p->N + 255) / 256), 256, 0, s>>>(a, p->N, f, b);
+    // w -= V c, then out = V^H w
+    void axpy_dots(const double2* V, int nv, const double2* c, double2* w, double2* out) {
+        if (nv <= kGmChunk) {
+            axpy_dot_kernel<1><<<kGmBlocks, kGmThreads, 0, s>>>(V, n, n, nv, c, w, part);
+            note_launch("gmres_axpy_dot");
+            reduce(nv, out, false);
+            allreduce(out, nv);
+            return;
+        }
+        axpy(V, nv, c, w, nullptr);
+        dots(V, nv, w, out);
+    }
+    // w -= V c (and ||w||^2 into *nrm2 when given)
+    void axpy(const double2* V, int nv, const double2* c, double2* w, double2* nrm2) {
+        for (int i0 = 0; i0 < nv; i0 += kGmChunk) {
+            const int m = std::min(kGmChunk, nv - i0);
+            const bool last = i0 + m >= nv;
+            axpy_norm_kernel<<<kGmBlocks, kGmThreads, 0, s>>>(V + (size_t)i0 * n, n, n, m, c + i0, w, part,
+                                                             (last && nrm2) ? 1 : 0);
+            note_launch("gmres_axpy_norm");
+        }
+        if (nrm2) {
+            reduce(1, nrm2, false);
+            allreduce(nrm2, 1);
+        }
+    }
+    void norm2(const double2* w, double2* out) {
+        dots(w, 1, w, out);
+    }
+    void scale(const double2* src, const double2* nrm2, double2* dst) {
+        gm_scale_kernel<<<nb(), 256, 0, s>>>(src, n, nrm2, dst);
         note_launch("gmres_scale");
+    }
+    void combine(const double2* V, int nv, const double2* y, double2* out, bool acc) {
+        for (int i0 = 0; i0 < nv; i0 += kGmChunk) {
+            const int m = std::min(kGmChunk, nv - i0);
+            gm_combine_kernel<<<nb(), 256, 0, s>>>(V + (size_t)i0 * n, n, n, m, y + i0, out, (acc || i0) ? 1 : 0);
+            note_launch("gmres_combine");
+        }
     }
 };
 
+inline bool finite(cplx z) { return std::isfinite(z.real()) && std::isfinite(z.imag()); }
+
+}  // namespace
+
 int gmres(aim_plan* p, const double2* b, double2* x, int restart, double tol, int max_iters, int fixed_iters,
           int* iters_out, double* rel_out) {
-    return gmres_with(p, [p](const double2* in, double2* out, cudaStream_t st) { matvec(p, in, out, 1, st); }, b, x,
-                      restart, tol, max_iters, fixed_iters, iters_out, rel_out);
+    GmresOps ops;
+    ops.n = p->N;
+    ops.matvec = [p](const double2* in, double2* out, cudaStream_t st) { matvec(p, in, out, 1, st); };
+    if (p->prec_on) ops.precond = [p](const double2* in, double2* out, cudaStream_t st) { apply_precond(p, in, out, st); };
+    return gmres_core(p, ops, b, x, restart, tol, max_iters, fixed_iters, iters_out, rel_out);
 }
 
-// The solver with any operator: `p` holds the workspace (and N, the stream),
-// `mv` applies the operator (single plan, or the slab-decomposed product with
-// replicated vectors -- every rank then runs the identical iteration).
-int gmres_with(aim_plan* p, const std::function<void(const double2*, double2*, cudaStream_t)>& mv,
-               const double2* b, double2* x, int restart, double tol, int max_iters, int fixed_iters,
-               int* iters_out, double* rel_out) {
+// The solver with any operator on vectors of local length ops.n: `p` holds the
+// workspace and the stream; ops.matvec applies A, ops.precond (optional) M^-1,
+// ops.allreduce (optional) sums small device vectors over the ranks.
+int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, int restart, double tol,
+               int max_iters, int fixed_iters, int* iters_out, double* rel_out) {
     if (restart < 1 || restart + 1 > kMaxBasis) throw Error(AIM_E_ARG, "restart must be in [1, 1023]");
     if (max_iters <= 0) max_iters = 20000;
-    const long long N = p->N;
+    const long long n = ops.n;
     cudaStream_t s = p->stream;
-    if (p->gm_restart < restart) {
+    const bool pre = (bool)ops.precond;
+    if (p->gm_restart < restart || p->gm_n != n || (pre && !p->gm_z)) {
         p->release(p->gm_V);
         p->release(p->gm_w);
+        p->release(p->gm_z);
         p->release(p->gm_part);
-        p->gm_V = p->alloc<double2>((size_t)(restart + 1) * N);
-        p->gm_w = p->alloc<double2>(N);
-        p->gm_part = p->alloc<double2>((size_t)kDotBlocks * (restart + 1) + kMaxBasis);
+        p->gm_V = p->alloc<double2>((size_t)(restart + 1) * std::max(1LL, n));
+        p->gm_w = p->alloc<double2>(std::max(1LL, n));
+        p->gm_z = pre ? p->alloc<double2>(std::max(1LL, n)) : nullptr;
+        p->gm_part = p->alloc<double2>((size_t)kGmBlocks * kGmChunk + 3 * (kMaxBasis + 1));
         p->gm_restart = restart;
+        p->gm_n = n;
     }
-    Gm g{p, s, p->gm_part, p->gm_part + (size_t)kDotBlocks * (restart + 1), {}};
+    if (!p->gm_host) AIM_CUDA(cudaMallocHost(&p->gm_host, sizeof(double2) * 3 * (kMaxBasis + 1)));
+    double2* hbuf = p->gm_host;
+    Vec g{p, s, n, p->gm_part, p->gm_part + (size_t)kGmBlocks * kGmChunk, ops};
+    double2* dh1 = g.dcoef;
+    double2* dh2 = g.dcoef + (kMaxBasis + 1);
+    double2* dmisc = g.dcoef + 2 * (kMaxBasis + 1);   // [0] ||.||^2, [1..] y coefficients
     double2* V = p->gm_V;
     double2* w = p->gm_w;
+    double2* z = p->gm_z;
     const int limit = fixed_iters > 0 ? fixed_iters : max_iters;
+    p->gm_hist.clear();
 
-    AIM_CUDA(cudaMemsetAsync(x, 0, sizeof(double2) * N, s));
-    const double bnorm = g.norm(b);
+    auto fetch = [&](const double2* d, int cnt, double2* h) {
+        AIM_CUDA(cudaMemcpyAsync(h, d, sizeof(double2) * cnt, cudaMemcpyDeviceToHost, s));
+    };
+    auto sync = [&]() { AIM_CUDA(cudaStreamSynchronize(s)); };
+
+    AIM_CUDA(cudaMemsetAsync(x, 0, sizeof(double2) * n, s));
+    g.norm2(b, dmisc);
+    fetch(dmisc, 1, hbuf);
+    sync();
+    if (!std::isfinite(hbuf[0].x)) throw Error(AIM_E_BREAKDOWN, "GMRES: right-hand side is not finite");
+    const double bnorm = std::sqrt(std::max(0.0, hbuf[0].x));
+    if (!std::isfinite(bnorm)) throw Error(AIM_E_BREAKDOWN, "GMRES: right-hand side is not finite");
     if (bnorm == 0.0) {
-        AIM_CUDA(cudaStreamSynchronize(s));
         if (iters_out) *iters_out = 0;
         if (rel_out) *rel_out = 0.0;
         return AIM_OK;
     }
     // r0 = b (x0 = 0)
     double beta = bnorm;
-    g.scale(b, 1.0 / beta, V);
+    g.scale(b, dmisc, V);
     int total = 0;
     double rel = 1.0;
-    std::vector<cplx> H((size_t)(restart + 1) * restart), gv(restart + 1), sn(restart), h1(restart + 1),
-        h2(restart + 1);
+    std::vector<cplx> H((size_t)(restart + 1) * restart), gv(restart + 1), sn(restart);
     std::vector<double> cs(restart);
     auto Hij = [&](int i, int j) -> cplx& { return H[(size_t)i * restart + j]; };
     while (true) {
@@ -181,16 +421,30 @@ int gmres_with(aim_plan* p, const std::function<void(const double2*, double2*, c
         int jd = 0;
         bool stop = false;
         for (int j = 0; j < restart; ++j) {
-            mv(V + (size_t)j * N, w, s);
-            // CGS2: two classical Gram-Schmidt passes
-            g.dots(V, j + 1, w, h1.data());
-            g.axpy(V, j + 1, h1.data(), -1.0, w);
-            g.dots(V, j + 1, w, h2.data());
-            g.axpy(V, j + 1, h2.data(), -1.0, w);
-            for (int i = 0; i <= j; ++i) Hij(i, j) = h1[i] + h2[i];
-            const double hn = g.norm(w);
+            double2* vj = V + (size_t)j * n;
+            if (pre) {
+                ops.precond(vj, z, s);
+                ops.matvec(z, w, s);
+            } else {
+                ops.matvec(vj, w, s);
+            }
+            const int nv = j + 1;
+            g.dots(V, nv, w, dh1);                 // pass 1
+            g.axpy_dots(V, nv, dh1, w, dh2);       // pass 2
+            g.axpy(V, nv, dh2, w, dmisc);          // pass 3 (+ ||w||^2)
+            g.scale(w, dmisc, V + (size_t)(j + 1) * n);
+            fetch(dh1, nv, hbuf);
+            fetch(dh2, nv, hbuf + (kMaxBasis + 1));
+            fetch(dmisc, 1, hbuf + 2 * (kMaxBasis + 1));
+            sync();
+            for (int i = 0; i <= j; ++i) {
+                Hij(i, j) = cplx(hbuf[i].x, hbuf[i].y) + cplx(hbuf[kMaxBasis + 1 + i].x, hbuf[kMaxBasis + 1 + i].y);
+                if (!finite(Hij(i, j))) throw Error(AIM_E_BREAKDOWN, "GMRES: non-finite Arnoldi coefficient");
+            }
+            const double hn2 = hbuf[2 * (kMaxBasis + 1)].x;
+            const double hn = std::isfinite(hn2) ? std::sqrt(std::max(0.0, hn2)) : hn2;
+            if (!std::isfinite(hn)) throw Error(AIM_E_BREAKDOWN, "GMRES: non-finite Arnoldi norm");
             Hij(j + 1, j) = hn;
-            if (hn > 0) g.scale(w, 1.0 / hn, V + (size_t)(j + 1) * N);
             for (int i = 0; i < j; ++i) {
                 const cplx t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
                 Hij(i + 1, j) = -std::conj(sn[i]) * Hij(i, j) + cs[i] * Hij(i + 1, j);
@@ -216,28 +470,45 @@ int gmres_with(aim_plan* p, const std::function<void(const double2*, double2*, c
             ++total;
             jd = j + 1;
             const double est = std::abs(gv[j + 1]) / bnorm;
+            p->gm_hist.push_back(est);
             if (total >= limit) { stop = true; break; }
             if (fixed_iters <= 0 && est <= tol) break;
             if (hn == 0) break;
         }
-        // y = H^-1 g (upper triangular), x += V y
+        // y = H^-1 g (upper triangular), x += M^-1 (V y)
         std::vector<cplx> yv(jd);
         for (int i = jd - 1; i >= 0; --i) {
             cplx t = gv[i];
             for (int q = i + 1; q < jd; ++q) t -= Hij(i, q) * yv[q];
             yv[i] = t / Hij(i, i);
+            if (!finite(yv[i])) throw Error(AIM_E_BREAKDOWN, "GMRES: singular Hessenberg matrix");
         }
-        if (jd) g.axpy(V, jd, yv.data(), +1.0, x);
+        if (jd) {
+            for (int i = 0; i < jd; ++i) hbuf[i] = make_double2(yv[i].real(), yv[i].imag());
+            AIM_CUDA(cudaMemcpyAsync(dmisc + 1, hbuf, sizeof(double2) * jd, cudaMemcpyHostToDevice, s));
+            if (pre) {
+                g.combine(V, jd, dmisc + 1, w, false);
+                ops.precond(w, z, s);
+                add_kernel<<<g.nb(), 256, 0, s>>>(z, n, x);
+                note_launch("gmres_add");
+            } else {
+                g.combine(V, jd, dmisc + 1, x, true);
+            }
+        }
         // true residual r = b - A x into V[0]
-        mv(x, w, s);
-        residual_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(b, w, N, V);
+        ops.matvec(x, w, s);
+        residual_kernel<<<g.nb(), 256, 0, s>>>(b, w, n, V);
         note_launch("gmres_residual");
-        beta = g.norm(V);
+        g.norm2(V, dmisc);
+        fetch(dmisc, 1, hbuf);
+        sync();
+        beta = std::isfinite(hbuf[0].x) ? std::sqrt(std::max(0.0, hbuf[0].x)) : hbuf[0].x;
+        if (!std::isfinite(beta)) throw Error(AIM_E_BREAKDOWN, "GMRES: non-finite residual");
         rel = beta / bnorm;
         if (stop || (fixed_iters <= 0 && rel <= tol) || beta == 0.0) break;
-        g.scale(V, 1.0 / beta, V);
+        g.scale(V, dmisc, V);
     }
-    AIM_CUDA(cudaStreamSynchronize(s));
+    sync();
     if (iters_out) *iters_out = total;
     if (rel_out) *rel_out = rel;
     return rel <= tol ? AIM_OK : AIM_NOT_CONVERGED;

@@ -964,3 +964,28 @@ void build_green_spectrum(aim_plan* p, cudaStream_t s) {
 }
 
 }  // namespace aim
+
+namespace aim {
+
+// Dense element block for the block-Jacobi preconditioner (k_precond.cu):
+// out[i][j] = Z_ex_sym[rows[i], rows[j]] (j k eta0 included), all pairs of the
+// element, the same exact Galerkin entries as the near field (D8, D9).
+__global__ void exact_block_kernel(NearArgs a, const int32_t* __restrict__ rows, int n, double2* __restrict__ out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)n * n) return;
+    const int i = (int)(e / n), j = (int)(e - (e / n) * n);
+    const double2 z = exact_sym(a, rows[i], rows[j]);
+    out[e] = make_double2(-a.keta * z.y, a.keta * z.x);
+}
+
+void fill_exact_block(aim_plan* p, const int32_t* d_rows, int n, double2* d_out, cudaStream_t s) {
+    NearArgs a{};
+    a.qp = p->tri_qp; a.qw = p->tri_qw; a.cor = p->tri_cor; a.tv = p->tri_v;
+    a.rt = p->rwg_t; a.ra = p->rwg_a; a.rp = p->rwg_p;
+    a.N = p->N; a.k = p->k; a.h = p->h; a.keta = p->k * eta0();
+    const long long tot = (long long)n * n;
+    exact_block_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, s>>>(a, d_rows, n, d_out);
+    note_launch("exact_block");
+}
+
+}  // namespace aim

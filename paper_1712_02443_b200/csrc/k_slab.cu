@@ -856,9 +856,11 @@ int aim_slab_gmres(aim_slab* S, const void* V, void* J, int32_t restart, double 
     return guarded([&] {
         int it = 0;
         double rr = 0;
-        const int st = gmres_with(
-            S->base, [S](const double2* in, double2* out, cudaStream_t s) { slab_matvec(S, in, out, 1, s); },
-            (const double2*)V, (double2*)J, restart, tol, max_iters, fixed_iters, &it, &rr);
+        GmresOps ops;
+        ops.n = S->base->N;
+        ops.matvec = [S](const double2* in, double2* out, cudaStream_t s) { slab_matvec(S, in, out, 1, s); };
+        const int st = gmres_core(S->base, ops, (const double2*)V, (double2*)J, restart, tol, max_iters,
+                                  fixed_iters, &it, &rr);
         if (iters) *iters = it;
         if (rel_res) *rel_res = rr;
         return st;

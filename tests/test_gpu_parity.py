@@ -371,3 +371,18 @@ def test_host_pipeline_matches_device_product():
     hp.drain()
     for x, y in zip(xs, ys):
         assert torch.equal(y, G.matvec(x.cuda()).cpu())
+
+
+def test_matvec_host_steps_matches_device_product():
+    """aim_matvec_host_steps (C ABI, host buffers, copies overlapped inside
+    the library) returns exactly aim_matvec's result for every step, with a
+    repeated input pointer and ragged step counts."""
+    G, O = gpu_plan("c1"), oracle_plan("c1")
+    for nrhs, n in ((1, 1), (1, 5), (3, 4)):
+        xs = [torch.from_numpy(make_vectors(O.N, nrhs, s).reshape(O.N, nrhs) if nrhs > 1
+                               else make_vectors(O.N, 1, s)[:, 0].copy()).pin_memory().numpy() for s in range(n)]
+        xs.append(xs[0])
+        ys = [np.empty_like(x) for x in xs]
+        G.matvec_host_steps(xs, ys)
+        for x, y in zip(xs, ys):
+            assert np.array_equal(y, G.matvec(torch.from_numpy(x).cuda()).cpu().numpy())
