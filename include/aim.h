@@ -205,6 +205,49 @@ int aim_precond_apply(aim_plan* plan, const void* x, void* y, void* stream);
  * bytes of the inverses}. */
 int aim_precond_info(const aim_plan* plan, int64_t* out);
 
+/* ---- array elements and the reduced (macromodel) system (NEXT-2) -------- */
+/*
+ * aim_plan_elements -- the array elements as the library enumerates them: the
+ * connected surfaces of the mesh (triangles joined by an RWG), ordered by
+ * their smallest RWG id; within an element the RWGs are in ascending id.
+ * elem_of_rwg: host int32 [N] (or NULL) element of every RWG; group: host
+ * int32 [n_elements] (or NULL) translate group of every element (elements
+ * that are translates of one another share a group, D18); *n_elements.
+ */
+int aim_plan_elements(aim_plan* plan, int32_t* elem_of_rwg, int32_t* group, int32_t* n_elements);
+
+/*
+ * aim_reduced_set -- the macromodel blocks of the reduced system
+ *   ( D - G^(E^,J^) T A^-1 B ) E^ = V^        (eq. finalsystem)
+ * per element TYPE d (n_types types; "only need to be calculated once for each
+ * distinct element").  Host complex128 row-major arrays,
+ * the blocks of all types concatenated in type order:
+ *   D  [nhat_d][nhat_d]
+ *   T  [nhat_d][nint_d]   transfer matrix (eq. Tm1)
+ *   A  [nint_d][nint_d]   interior operator A_m (eq. JM)
+ *   B  [nint_d][nhat_d]   B_m (eq. JM)
+ * nhat_d = RWGs of an element of type d on its equivalent surface (rows in
+ * ascending RWG id, see aim_plan_elements), nint_d = interior unknowns.
+ * elem_type: host int32 [n_elements], the type of every element.  The library
+ * copies the blocks, inverts every A_d on the device and keeps D_d and
+ * K_d = T_d A_d^-1 B_d.  Synchronous.  Errors: AIM_E_ARG (sizes or element
+ * count not matching the mesh, AIM_C64 plan), AIM_E_NOMEM, AIM_E_BREAKDOWN
+ * (singular A_d).
+ */
+int aim_reduced_set(aim_plan* plan, int32_t n_types, const int32_t* nhat, const int32_t* nint, const void* D,
+                    const void* T, const void* A, const void* B, const int32_t* elem_type, int32_t n_elements);
+/*
+ * aim_reduced_matvec -- out := (D - G T A^-1 B) Y (eq. MV_product1,
+ * PAPER.md:512-523) with G the AIM exterior operator; with the sign
+ * convention of reading D1, G = -Z_eq, so out = D Y + Z_eq (K Y).  Y, out:
+ * device complex128 [N], no overlap.  Stream-ordered.
+ */
+int aim_reduced_matvec(aim_plan* plan, const void* Y, void* out, void* stream);
+/* GMRES on the reduced system (D15), as aim_gmres with the
+ * operator of aim_reduced_matvec (no preconditioner).  Synchronous. */
+int aim_reduced_gmres(aim_plan* plan, const void* V, void* E, int32_t restart, double tol, int32_t max_iters,
+                      int32_t fixed_iters, int32_t* iters, double* rel_res);
+
 /*
  * aim_planewave_rhs --V_m = <Lambda_m, E_inc>, E_inc(r) = E0 pol exp(-j k khat.r)
  * (PAPER.md:455-459 with the sign convention of D1; D14), 7-point rule.

@@ -41,6 +41,10 @@ SIGNATURES = [
     ("aim_precond_build", I32, [P, I32]),
     ("aim_precond_apply", I32, [P, P, P, P]),
     ("aim_precond_info", I32, [P, P]),
+    ("aim_plan_elements", I32, [P, P, P, ctypes.POINTER(I32)]),
+    ("aim_reduced_set", I32, [P, I32, P, P, P, P, P, P, P, I32]),
+    ("aim_reduced_matvec", I32, [P, P, P, P]),
+    ("aim_reduced_gmres", I32, [P, P, P, I32, D, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]),
     ("aim_planewave_rhs", I32, [P, P, P, D, D, P, P]),
     ("aim_project", I32, [P, P, P, I32, P]),
     ("aim_convolve", I32, [P, P, P, I32, P]),

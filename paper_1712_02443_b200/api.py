@@ -178,6 +178,44 @@ class AimPlan:
         _check(_lib.load().aim_precond_apply(self._p, _dev_ptr(x, self.N, 1), _dev_ptr(y, self.N, 1), _stream()))
         return y
 
+    # ---- array elements and the reduced (macromodel) system
+    def elements(self):
+        """aim_plan_elements: (element of every RWG [N], translate group of every element)."""
+        n = ctypes.c_int32()
+        _check(_lib.load().aim_plan_elements(self._p, None, None, ctypes.byref(n)))
+        eo = np.empty(self.N, dtype=np.int32)
+        gr = np.empty(n.value, dtype=np.int32)
+        _check(_lib.load().aim_plan_elements(self._p, eo.ctypes.data, gr.ctypes.data, ctypes.byref(n)))
+        return eo, gr
+
+    def reduced_set(self, elem_type, blocks):
+        """aim_reduced_set: blocks[d] = (D, T, A, B) complex128 arrays of type d."""
+        nhat = np.array([b[0].shape[0] for b in blocks], dtype=np.int32)
+        nint = np.array([b[2].shape[0] for b in blocks], dtype=np.int32)
+        cat = [np.ascontiguousarray(np.concatenate([np.ascontiguousarray(b[i], dtype=np.complex128).ravel()
+                                                    for b in blocks])) for i in range(4)]
+        et = np.ascontiguousarray(elem_type, dtype=np.int32)
+        _check(_lib.load().aim_reduced_set(self._p, len(blocks), nhat.ctypes.data, nint.ctypes.data,
+                                           *[c.ctypes.data for c in cat], et.ctypes.data, et.size))
+
+    def reduced_matvec(self, Y, out=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty_like(Y)
+        _check(_lib.load().aim_reduced_matvec(self._p, _dev_ptr(Y, self.N, 1), _dev_ptr(out, self.N, 1), _stream()))
+        return out
+
+    def reduced_gmres(self, V, restart=50, tol=1e-4, max_iters=0, fixed_iters=0):
+        torch = _torch()
+        E = torch.empty_like(V)
+        it = ctypes.c_int32()
+        rr = ctypes.c_double()
+        torch.cuda.current_stream().synchronize()
+        st = _check(_lib.load().aim_reduced_gmres(self._p, _dev_ptr(V, self.N, 1), _dev_ptr(E, self.N, 1),
+                                                  int(restart), float(tol), int(max_iters), int(fixed_iters),
+                                                  ctypes.byref(it), ctypes.byref(rr)))
+        return E, int(it.value), float(rr.value), STATUS[st]
+
     def planewave_rhs(self, khat=(0.0, 0.0, -1.0), pol=(1.0, 0.0, 0.0), E0=1.0 + 0j):
         torch = _torch()
         V = torch.empty(self.N, dtype=torch.complex128, device="cuda")

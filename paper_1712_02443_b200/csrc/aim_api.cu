@@ -539,11 +539,63 @@ int aim_precond_apply(aim_plan* p, const void* x, void* y, void* stream) {
 int aim_precond_info(const aim_plan* p, int64_t* out) {
     if (!p || !out) return fail(AIM_E_ARG, "bad argument");
     out[0] = p->prec_on;
-    out[1] = p->pc_nblocks;
-    out[2] = p->pc_ndistinct;
-    out[3] = p->pc_maxn;
-    out[4] = p->pc_bytes;
+    out[1] = p->prec_on ? p->el_count : 0;
+    out[2] = p->pc.ndistinct;
+    out[3] = p->pc.maxn;
+    out[4] = p->pc.bytes;
     return AIM_OK;
+}
+
+int aim_plan_elements(aim_plan* p, int32_t* elem_of_rwg, int32_t* group, int32_t* n_elements) {
+    if (!p || !n_elements) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        ensure_elements(p, p->stream);
+        *n_elements = p->el_count;
+        if (elem_of_rwg)
+            for (int e = 0; e < p->el_count; ++e)
+                for (int64_t q = p->el_rptr_h[e]; q < p->el_rptr_h[e + 1]; ++q) elem_of_rwg[p->el_rows_h[q]] = e;
+        if (group)
+            for (int e = 0; e < p->el_count; ++e) group[e] = p->el_group_h[e];
+        return AIM_OK;
+    });
+}
+
+int aim_reduced_set(aim_plan* p, int32_t n_types, const int32_t* nhat, const int32_t* nint, const void* D,
+                    const void* T, const void* A, const void* B, const int32_t* elem_type, int32_t n_elements) {
+    if (!p || n_types < 1 || !nhat || !nint || !D || !T || !A || !B || !elem_type || n_elements < 1)
+        return fail(AIM_E_ARG, "bad argument");
+    if (p->prec != AIM_C128) return fail(AIM_E_ARG, "the reduced system needs an AIM_C128 plan");
+    return guarded([&] {
+        reduced_set(p, n_types, nhat, nint, (const double2*)D, (const double2*)T, (const double2*)A,
+                    (const double2*)B, elem_type, n_elements);
+        return AIM_OK;
+    });
+}
+
+int aim_reduced_matvec(aim_plan* p, const void* Y, void* out, void* stream) {
+    if (!p || !Y || !out || Y == out) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        reduced_matvec(p, (const double2*)Y, (double2*)out, (cudaStream_t)stream);
+        return AIM_OK;
+    });
+}
+
+int aim_reduced_gmres(aim_plan* p, const void* V, void* E, int32_t restart, double tol, int32_t max_iters,
+                      int32_t fixed_iters, int32_t* iters, double* rel_res) {
+    if (!p || !V || !E || restart < 1 || !(tol >= 0)) return fail(AIM_E_ARG, "bad argument");
+    if (!p->rd_on) return fail(AIM_E_ARG, "no reduced system set (aim_reduced_set)");
+    return guarded([&] {
+        GmresOps ops;
+        ops.n = p->N;
+        ops.matvec = [p](const double2* in, double2* o, cudaStream_t st) { reduced_matvec(p, in, o, st); };
+        int it = 0;
+        double rr = 0;
+        const int st = gmres_core(p, ops, (const double2*)V, (double2*)E, restart, tol, max_iters, fixed_iters,
+                                  &it, &rr);
+        if (iters) *iters = it;
+        if (rel_res) *rel_res = rr;
+        return st;
+    });
 }
 
 int aim_gmres_history(const aim_plan* p, double* out, int32_t cap, int32_t* count) {

@@ -126,14 +126,30 @@ void launch_planar_yz(const PlanarPass& p, cudaStream_t s);
 void launch_ztoeplitz(void* W, int prec, int A, int B, int Nz, int R, int kx_is_a, int off, int Px, int Py,
                       const void* spec, cudaStream_t s);
 bool planar_supported(int Py, int Nz, int min_radix);
+// fused mode-2 y/z pass (ymode2.cuh) for the compiled (Py, Nz) plans, one RHS,
+// complex128; false if not applicable (the caller runs the separate passes)
+bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, const void* spec, const FftAxis& ay,
+                   cudaStream_t s);
 void make_fft_axis(int P, FftAxis& ax);    // factorisation + device twiddles
 int smooth_size_at_least(int n);           // smallest 2^a 3^b 5^c 7^d >= n
 
-// block-Jacobi apply job: distinct inverse d (n x n at element offset ioff)
-// shared by m elements listed at pc_elist[eoff ..)
-struct PcJob {
+// Per-element dense blocks (block-Jacobi inverses, reduced-system D and K):
+// element e uses block map[e] (n_d x n_d row-major at mats + off[d]).
+// apply_blocks: out[rows_e] (+)= B_map[e] in[rows_e] for every element, as a
+// GEMM over the elements sharing a block (jobs) or a GEMV per element.
+struct PcJob {                    // block d shared by m elements listed at elist[eoff ..)
     int d, eoff, m, n;
     int64_t ioff;
+};
+struct BlockSet {
+    int ndistinct = 0, maxn = 0;
+    int64_t bytes = 0;
+    double2* mats = nullptr;      // blocks, concatenated
+    int64_t* off = nullptr;       // [ndistinct+1] (device)
+    int32_t* map = nullptr;       // [elements] (device)
+    std::vector<PcJob> jobs;
+    int32_t* elist = nullptr;     // job element lists, then the GEMV elements
+    int gemv_off = 0, gemv_cnt = 0;
 };
 
 // -------------------------------------------------------------------- plan
@@ -235,21 +251,24 @@ struct aim_plan {
     double2* gm_part = nullptr;   // block partials + device coefficients
     double2* gm_host = nullptr;   // pinned host mirror of the coefficients
     std::vector<double> gm_hist;  // residual estimate |g_{j+1}|/||b|| of the last solve
+    // array elements = connected surfaces of the mesh (built on first use by
+    // ensure_elements): ordered by smallest RWG id, RWGs ascending within
+    int el_count = 0;
+    std::vector<int64_t> el_rptr_h;   // [el_count+1]
+    std::vector<int32_t> el_rows_h;   // [N] RWG ids element-major
+    std::vector<int32_t> el_group_h;  // [el_count] translate group (first element of the group defines it)
+    std::vector<int32_t> el_reps_h;   // [groups] representative element of each group
+    int32_t* el_rows = nullptr;   // device copies
+    int64_t* el_rptr = nullptr;
     // block-Jacobi preconditioner (aim_precond_build): one dense inverse per
-    // distinct element block; element e of the mesh uses inverse pc_map[e]
+    // translate group
     int prec_on = 0;
-    int pc_nblocks = 0;           // connected surfaces (elements)
-    int pc_ndistinct = 0;         // distinct inverses
-    int pc_maxn = 0;              // largest block
-    int32_t* pc_rows = nullptr;   // [N] RWG ids grouped by element (element-major)
-    int64_t* pc_rptr = nullptr;   // [nblocks+1] ranges into pc_rows
-    int32_t* pc_map = nullptr;    // [nblocks] distinct inverse of each element
-    int64_t* pc_iptr = nullptr;   // [ndistinct+1] offsets of the inverses (elements of double2)
-    double2* pc_inv = nullptr;    // inverses, row-major n_b x n_b each
-    int64_t pc_bytes = 0;
-    std::vector<aim::PcJob> pc_jobs;  // GEMM applies (inverses shared by >= 8 elements)
-    int32_t* pc_elist = nullptr;  // element lists of the jobs, then the GEMV elements
-    int pc_gemv_off = 0, pc_gemv_cnt = 0;
+    aim::BlockSet pc;
+    // reduced (macromodel) system of PAPER.md eq. finalsystem (aim_reduced_set):
+    // D and K = T A^-1 B per element type
+    int rd_on = 0;
+    aim::BlockSet rd_D, rd_K;
+    double2* rd_t = nullptr;      // [N] K Y
     // host staging for aim_matvec_host
     int hs_nrhs = 0;
     double2* hx = nullptr;
@@ -346,9 +365,25 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
 int gmres(aim_plan* p, const double2* V, double2* J, int restart, double tol, int max_iters, int fixed_iters,
           int* iters, double* rel_res);
 
-// ---- block-Jacobi preconditioner (k_precond.cu)
+// ---- elements, per-element blocks, block-Jacobi preconditioner (k_precond.cu)
+void ensure_elements(aim_plan* p, cudaStream_t s);
+// finish a block set whose mats/off are filled: map, jobs, element lists
+void setup_block_apply(aim_plan* p, BlockSet& b, const std::vector<int32_t>& map, const std::vector<int>& sizes,
+                       cudaStream_t s);
+void apply_blocks(aim_plan* p, const BlockSet& b, const double2* in, double2* out, bool accumulate, cudaStream_t s);
+void free_blocks(aim_plan* p, BlockSet& b);
+// batched Gauss-Jordan inversion in place of the blocks (n_d x n_d at mats + off_h[d]);
+// throws AIM_E_BREAKDOWN on a singular block
+void invert_blocks(double2* mats, const std::vector<int64_t>& off_h, const std::vector<int>& sizes, cudaStream_t s);
+// C[m x n] = A[m x k] B[k x n], row-major complex128, device
+void zgemm_rm(const double2* A, const double2* B, double2* C, int m, int n, int k, cudaStream_t s);
 void build_precond(aim_plan* p, cudaStream_t s);
 void apply_precond(aim_plan* p, const double2* in, double2* out, cudaStream_t s);
 void free_precond(aim_plan* p);
+// ---- reduced (macromodel) system (k_reduced.cu)
+void reduced_set(aim_plan* p, int ntypes, const int32_t* nhat, const int32_t* nint, const double2* D,
+                 const double2* T, const double2* A, const double2* B, const int32_t* elem_type, int nelem);
+void reduced_matvec(aim_plan* p, const double2* Y, double2* out, cudaStream_t s);
+void free_reduced(aim_plan* p);
 
 }  // namespace aim

@@ -727,6 +727,8 @@ void launch_ztoeplitz(void* W, int prec, int A, int B, int Nz, int R, int kx_is_
     note_launch("ztoeplitz");
 }
 
+#include "ymode2.cuh"
+
 // ------------------------------------------------------------------- host
 int smooth_size_at_least(int n) {
     if (n <= 1) return 1;

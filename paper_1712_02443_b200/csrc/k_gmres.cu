@@ -7,7 +7,7 @@
 // rotations.  Arnoldi is classical Gram-Schmidt applied twice (CGS2) in three
 // passes over the basis per iteration (DESIGN.md §5 "GMRES"):
 //   pass 1  h1 = V^H w                                   (mdot_kernel)
-//   pass 2  w -= V h1, then h2 = V^H w, V read once      (axpy_dot_kernel)
+//   pass 2  w -= V h1, then h2 = V^H w, V read once      (axpy_dot_smem_kernel)
 //   pass 3  w -= V h2 and ||w||^2                        (axpy_norm_kernel)
 // then v_{j+1} = w / ||w||.  Every coefficient is produced and consumed on
 // the device (fixed-order block partials -> deterministic); the host reads
@@ -100,81 +100,89 @@ __global__ void __launch_bounds__(kGmThreads) mdot_kernel(const double2* __restr
 }
 
 // w -= sum_i c[i] V_i (c on the device), then partial dots of the updated w
-// with every V_i; V is read once.  Steps of 32 U elements: warp g forms
-// sum_{i in g} c_i V_i[e] from its registers, the 16 partial sums meet in
-// shared memory, every warp rebuilds w'[e] and accumulates conj(V_i[e]) w'[e].
-template <int U>
-__global__ void __launch_bounds__(kGmThreads, 2) axpy_dot_kernel(const double2* __restrict__ V, long long ld,
-                                                              long long n, int nv, const double2* __restrict__ c,
-                                                              double2* __restrict__ w,
-                                                              double2* __restrict__ partial) {
-    __shared__ double2 red[kGmWarps][32 * U];
-    __shared__ double2 xs[32 * U];
-    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-    const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 32 * U - 1) / (32 * U) * (32 * U);
+// with every V_i, V read from HBM once: the V tile is staged in shared memory
+// by cp.async, double buffered: tile t+1 (nv x 64 elements, and w) lands while tile t is used.
+// Per tile: thread (group q = tid / 64, element t = tid % 64) forms
+// sum_{i = q mod 4} c_i V_i[e]; 64 threads rebuild w' = w - sum of the 4
+// group sums; then warp g accumulates conj(V_i[e]) w'[e] for i = g mod 8
+// (lanes over the 64 elements).
+constexpr int kAdT = 64, kAdThreads = 256;
+__device__ __forceinline__ void cp16(void* sdst, const void* gsrc, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__global__ void __launch_bounds__(kAdThreads, 2) axpy_dot_smem_kernel(const double2* __restrict__ V, long long ld,
+                                                                      long long n, int nv,
+                                                                      const double2* __restrict__ c,
+                                                                      double2* __restrict__ w,
+                                                                      double2* __restrict__ partial) {
+    extern __shared__ __align__(16) double2 sm[];
+    double2* buf[2] = {sm, sm + (nv + 1) * kAdT};    // [nv + 1][kAdT]: V rows then w
+    __shared__ double2 red[4][kAdT];
+    __shared__ double2 xs[kAdT];
+    __shared__ double2 cs[kGmChunk];
+    const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
+    if (tid < nv) cs[tid] = c[tid];
+    const long long chunk = ((n + gridDim.x - 1) / gridDim.x + kAdT - 1) / kAdT * kAdT;
     const long long a = blockIdx.x * chunk, b = min(n, a + chunk);
-    double2 cc[kGmQ], acc[kGmQ];
+    const int ntiles = b > a ? (int)((b - a + kAdT - 1) / kAdT) : 0;
+    auto issue = [&](int t, double2* dst) {
+        const long long e0 = a + (long long)t * kAdT;
+        for (int q = tid; q < (nv + 1) * kAdT; q += kAdThreads) {
+            const int i = q / kAdT, el = q - (q / kAdT) * kAdT;
+            const long long e = e0 + el;
+            const bool v = e < b;
+            const double2* src = i < nv ? V + i * ld + (v ? e : 0) : w + (v ? e : 0);
+            cp16(&dst[q], src, v);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double2 acc[8];
 #pragma unroll
-    for (int q = 0; q < kGmQ; ++q) {
-        const int i = g + kGmWarps * q;
-        cc[q] = i < nv ? c[i] : make_double2(0, 0);
-        acc[q] = make_double2(0, 0);
-    }
-    for (long long e0 = a + lane; e0 < b + lane; e0 += 32 * U) {
-        double2 sm[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) sm[u] = make_double2(0, 0);
+    for (int q = 0; q < 8; ++q) acc[q] = make_double2(0, 0);
+    if (ntiles) issue(0, buf[0]);
+    for (int t = 0; t < ntiles; ++t) {
+        double2* cur = buf[t & 1];
+        if (t + 1 < ntiles) {
+            issue(t + 1, buf[(t + 1) & 1]);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
         {
-            double2 v[kGmQ][U];
-#pragma unroll
-            for (int q = 0; q < kGmQ; ++q) {
-                const int i = g + kGmWarps * q;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const long long e = e0 + 32 * u;
-                    v[q][u] = (e < b && i < nv) ? __ldg(&V[i * ld + e]) : make_double2(0, 0);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < kGmQ; ++q)
-#pragma unroll
-                for (int u = 0; u < U; ++u) cfma(sm[u], cc[q], v[q][u]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) red[g][lane + 32 * u] = sm[u];
-        __syncthreads();
-        // the first 32 U threads rebuild w' = w - sum_g red[g] for the step's elements
-        if (threadIdx.x < 32 * U) {
-            const int t = threadIdx.x;
-            const long long e = e0 - lane + t;
-            const bool live = e < b;
-            double2 x = live ? w[e] : make_double2(0, 0);
-#pragma unroll
-            for (int q = 0; q < kGmWarps; ++q) {
-                x.x -= red[q][t].x;
-                x.y -= red[q][t].y;
-            }
-            xs[t] = x;
-            if (live) w[e] = x;
+            const int q = tid / kAdT, el = tid - (tid / kAdT) * kAdT;
+            double2 s = make_double2(0, 0);
+            for (int i = q; i < nv; i += 4) cfma(s, cs[i], cur[i * kAdT + el]);
+            red[q][el] = s;
         }
         __syncthreads();
-        // second read of the step's V tile: L1 hits (read a moment ago with the
-        // default caching), so V costs HBM traffic once and no registers across
-        // the barriers (2 CTAs per SM)
+        if (tid < kAdT) {
+            double2 x = cur[nv * kAdT + tid];
 #pragma unroll
-        for (int q = 0; q < kGmQ; ++q) {
-            const int i = g + kGmWarps * q;
+            for (int q = 0; q < 4; ++q) {
+                x.x -= red[q][tid].x;
+                x.y -= red[q][tid].y;
+            }
+            xs[tid] = x;
+            const long long e = a + (long long)t * kAdT + tid;
+            if (e < b) w[e] = x;
+        }
+        __syncthreads();
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const long long e = e0 + 32 * u;
-                const double2 v = (e < b && i < nv) ? __ldcs(&V[i * ld + e]) : make_double2(0, 0);
-                cfma_conj(acc[q], v, xs[lane + 32 * u]);
+        for (int q = 0; q < 8; ++q) {
+            const int i = g + 8 * q;
+            if (i < nv) {
+                cfma_conj(acc[q], cur[i * kAdT + lane], xs[lane]);
+                cfma_conj(acc[q], cur[i * kAdT + lane + 32], xs[lane + 32]);
             }
         }
+        __syncthreads();   // buffer `cur` is refilled by the issue of tile t + 2
     }
 #pragma unroll
-    for (int q = 0; q < kGmQ; ++q) {
-        const int i = g + kGmWarps * q;
+    for (int q = 0; q < 8; ++q) {
+        const int i = g + 8 * q;
         const double2 s = warp_sum(acc[q]);
         if (lane == 0 && i < nv) partial[(long long)blockIdx.x * kGmChunk + i] = s;
     }
@@ -303,7 +311,16 @@ struct Vec {
     // w -= V c, then out = V^H w
     void axpy_dots(const double2* V, int nv, const double2* c, double2* w, double2* out) {
         if (nv <= kGmChunk) {
-            axpy_dot_kernel<1><<<kGmBlocks, kGmThreads, 0, s>>>(V, n, n, nv, c, w, part);
+            {
+                static unsigned long long attr_mask = 0;   // the attribute is per device
+                if (!(attr_mask >> (p->device & 63) & 1ULL)) {
+                    AIM_CUDA(cudaFuncSetAttribute(axpy_dot_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)(2 * (kGmChunk + 1) * kAdT * sizeof(double2))));
+                    attr_mask |= 1ULL << (p->device & 63);
+                }
+                const size_t smem = 2 * (size_t)(nv + 1) * kAdT * sizeof(double2);
+                axpy_dot_smem_kernel<<<kGmBlocks, kAdThreads, smem, s>>>(V, n, n, nv, c, w, part);
+            }
             note_launch("gmres_axpy_dot");
             reduce(nv, out, false);
             allreduce(out, nv);

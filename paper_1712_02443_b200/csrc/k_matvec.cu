@@ -1087,6 +1087,15 @@ static void convolve_impl(aim_plan* p, const void* Q, void* Phi, int R, cudaStre
         q.spec = spec;
         launch_planar_yz(q, s);
     } else {
+        // mode 2, one RHS, a compiled plan: the fused y/z pass in place on W1
+        if (p->planar == 2 && launch_ymode2(p->W1, p->prec, Px, (int)Ny, (int)Nz, Py, R, spec, p->ax[1], s)) {
+            if (pr) pr->mark(3, s);
+            f.in = p->W1; f.out = Phi; f.outer = 4; f.Lin = Px; f.Lout = (int)Nx; f.inner = Ny * Nz * R;
+            f.mode = 1; f.ax = p->ax[0]; f.TO = f.TI = 0;
+            launch_fft_pass(f, s);
+            if (pr) pr->mark(4, s);
+            return;
+        }
         // y forward, [4 Px][Ny -> Py][Nz R]
         f.in = p->W1; f.out = p->W2; f.outer = 4LL * Px; f.Lin = (int)Ny; f.Lout = Py; f.inner = Nz * R;
         f.mode = 0; f.ax = p->ax[1]; f.TO = f.TI = 0;

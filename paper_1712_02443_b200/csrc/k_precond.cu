@@ -141,16 +141,17 @@ __global__ void __launch_bounds__(256) gj_unperm_kernel(const GjBlk* __restrict_
 }
 
 // --------------------------------------------------------------- apply
-// Shared inverse (GEMM): out[rows_e[i]] = sum_j Inv[i][j] in[rows_e[j]] for the
-// elements e of list `el` (all of size n).  CTA tile: 64 rows x 64 elements,
-// k-chunks of 8; thread (tr, tc) owns rows tr + 16 a, elements tc + 16 b
-// (a, b < 4): 16 complex accumulators.
+// Shared block (GEMM): out[rows_e[i]] (+)= sum_j Blk[i][j] in[rows_e[j]] for
+// the elements e of list `el` (all of size n).  CTA tile: 64 rows x 64
+// elements, k-chunks of 8; thread (tr, tc) owns rows tr + 16 a, elements
+// tc + 16 b (a, b < 4): 16 complex accumulators.
 constexpr int kPcTile = 64, kPcK = 8;
-__global__ void __launch_bounds__(256) pc_gemm_kernel(const double2* __restrict__ Inv, int n,
+__global__ void __launch_bounds__(256) pc_gemm_kernel(const double2* __restrict__ Blk, int n,
                                                       const int32_t* __restrict__ el, int m,
                                                       const int32_t* __restrict__ rows,
                                                       const int64_t* __restrict__ rptr,
-                                                      const double2* __restrict__ in, double2* __restrict__ out) {
+                                                      const double2* __restrict__ in, double2* __restrict__ out,
+                                                      int accumulate) {
     __shared__ double2 As[kPcK][kPcTile + 1];
     __shared__ double2 Bs[kPcK][kPcTile + 1];
     __shared__ long long rbase[kPcTile];
@@ -167,11 +168,10 @@ __global__ void __launch_bounds__(256) pc_gemm_kernel(const double2* __restrict_
         for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0, 0);
     __syncthreads();
     for (int j0 = 0; j0 < n; j0 += kPcK) {
-        // A tile: rows i0..i0+63, columns j0..j0+7 ; B tile: in[rows_e[j]] for j0..j0+7, e0..e0+63
         for (int t = threadIdx.x; t < kPcK * kPcTile; t += 256) {
             const int r = t / kPcK, c = t - (t / kPcK) * kPcK;
             const int i = i0 + r, j = j0 + c;
-            As[c][r] = (i < n && j < n) ? __ldg(&Inv[(long long)i * n + j]) : make_double2(0, 0);
+            As[c][r] = (i < n && j < n) ? __ldg(&Blk[(long long)i * n + j]) : make_double2(0, 0);
             const int cc = t / kPcTile, ee = t - (t / kPcTile) * kPcTile;
             const int jj = j0 + cc;
             const long long rb = rbase[ee];
@@ -202,31 +202,35 @@ __global__ void __launch_bounds__(256) pc_gemm_kernel(const double2* __restrict_
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             const int i = i0 + tr + 16 * a;
-            if (i < n) out[rows[rb + i]] = acc[a][b];
+            if (i >= n) continue;
+            double2* o = &out[rows[rb + i]];
+            if (accumulate) *o = make_double2(o->x + acc[a][b].x, o->y + acc[a][b].y);
+            else *o = acc[a][b];
         }
     }
 }
 
-// Few elements per inverse (GEMV): one CTA per (element, 64-row tile); the
+// Few elements per block (GEMV): one CTA per (element, 64-row tile); the
 // element's input is staged in shared memory, warp per row.
-__global__ void __launch_bounds__(256) pc_gemv_kernel(const double2* __restrict__ inv0,
-                                                      const int64_t* __restrict__ iptr,
+__global__ void __launch_bounds__(256) pc_gemv_kernel(const double2* __restrict__ mats,
+                                                      const int64_t* __restrict__ off,
                                                       const int32_t* __restrict__ map,
                                                       const int32_t* __restrict__ el, const int32_t* __restrict__ rows,
                                                       const int64_t* __restrict__ rptr,
-                                                      const double2* __restrict__ in, double2* __restrict__ out) {
+                                                      const double2* __restrict__ in, double2* __restrict__ out,
+                                                      int accumulate) {
     extern __shared__ double2 xs[];
     const int e = el[blockIdx.y];
     const long long r0 = rptr[e];
     const int n = (int)(rptr[e + 1] - r0);
     const int i0 = blockIdx.x * 64;
     if (i0 >= n) return;
-    const double2* Inv = inv0 + iptr[map[e]];
+    const double2* Blk = mats + off[map[e]];
     for (int j = threadIdx.x; j < n; j += blockDim.x) xs[j] = __ldg(&in[rows[r0 + j]]);
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = i0 + w; i < min(n, i0 + 64); i += 8) {
-        const double2* ri = Inv + (long long)i * n;
+        const double2* ri = Blk + (long long)i * n;
         double2 s = make_double2(0, 0);
         for (int j = lane; j < n; j += 32) {
             const double2 a = __ldcs(&ri[j]), x = xs[j];
@@ -234,12 +238,69 @@ __global__ void __launch_bounds__(256) pc_gemv_kernel(const double2* __restrict_
             s.y = fma(a.x, x.y, fma(a.y, x.x, s.y));
         }
 #pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
-            s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+        for (int o = 16; o; o >>= 1) {
+            s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+            s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
         }
-        if (lane == 0) out[rows[r0 + i]] = s;
+        if (lane == 0) {
+            double2* d = &out[rows[r0 + i]];
+            if (accumulate) *d = make_double2(d->x + s.x, d->y + s.y);
+            else *d = s;
+        }
     }
+}
+
+// Plain row-major complex GEMM C = A B (setup only: K = T A^-1 B of the
+// reduced system).  Tile 64 x 64, k-chunks of 8, 16 accumulators per thread.
+__global__ void __launch_bounds__(256) zgemm_rm_kernel(const double2* __restrict__ A, const double2* __restrict__ B,
+                                                       double2* __restrict__ C, int m, int n, int k) {
+    __shared__ double2 As[kPcK][kPcTile + 1];
+    __shared__ double2 Bs[kPcK][kPcTile + 1];
+    const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
+    const int i0 = blockIdx.x * kPcTile, j0c = blockIdx.y * kPcTile;
+    double2 acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0, 0);
+    for (int q0 = 0; q0 < k; q0 += kPcK) {
+        for (int t = threadIdx.x; t < kPcK * kPcTile; t += 256) {
+            const int r = t / kPcK, c = t - (t / kPcK) * kPcK;
+            As[c][r] = (i0 + r < m && q0 + c < k) ? A[(long long)(i0 + r) * k + q0 + c] : make_double2(0, 0);
+            const int cc = t / kPcTile, jj = t - (t / kPcTile) * kPcTile;
+            Bs[cc][jj] = (q0 + cc < k && j0c + jj < n) ? B[(long long)(q0 + cc) * n + j0c + jj] : make_double2(0, 0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < kPcK; ++c) {
+            double2 av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = As[c][tr + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = Bs[c][tc + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    acc[a][b].x = fma(av[a].x, bv[b].x, fma(-av[a].y, bv[b].y, acc[a][b].x));
+                    acc[a][b].y = fma(av[a].x, bv[b].y, fma(av[a].y, bv[b].x, acc[a][b].y));
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int i = i0 + tr + 16 * a, j = j0c + tc + 16 * b;
+            if (i < m && j < n) C[(long long)i * n + j] = acc[a][b];
+        }
+}
+
+void zgemm_rm(const double2* A, const double2* B, double2* C, int m, int n, int k, cudaStream_t s) {
+    const dim3 grid((unsigned)((m + kPcTile - 1) / kPcTile), (unsigned)((n + kPcTile - 1) / kPcTile));
+    zgemm_rm_kernel<<<grid, 256, 0, s>>>(A, B, C, m, n, k);
+    note_launch("zgemm_rm");
 }
 
 // ------------------------------------------------------------- host side
@@ -259,32 +320,15 @@ struct Uf {
 };
 }  // namespace
 
-void free_precond(aim_plan* p) {
-    p->release(p->pc_rows);
-    p->release(p->pc_rptr);
-    p->release(p->pc_map);
-    p->release(p->pc_iptr);
-    p->release(p->pc_inv);
-    p->release(p->pc_elist);
-    p->pc_rows = nullptr;
-    p->pc_rptr = nullptr;
-    p->pc_map = nullptr;
-    p->pc_iptr = nullptr;
-    p->pc_inv = nullptr;
-    p->pc_elist = nullptr;
-    p->pc_jobs.clear();
-    p->prec_on = 0;
-    p->pc_nblocks = p->pc_ndistinct = p->pc_maxn = 0;
-    p->pc_bytes = 0;
-}
-
-void build_precond(aim_plan* p, cudaStream_t s) {
-    free_precond(p);
+// Elements = connected surfaces (triangles joined by an RWG), ordered by
+// smallest RWG id; translate groups (D18): same local topology, corners equal
+// to 1e-9 of the element size after removing the translation.
+void ensure_elements(aim_plan* p, cudaStream_t s) {
+    if (p->el_count) return;
     const long long N = p->N, nt = p->nt;
     const int32_t* rt = p->h_rt.data();
     const int32_t* tv = p->h_tv.data();
     const double* cor = p->h_cor.data();
-    // elements = connected surfaces (triangles joined by an RWG), ordered by smallest RWG id
     Uf uf((size_t)nt);
     for (long long n = 0; n < N; ++n) uf.unite(rt[2 * n], rt[2 * n + 1]);
     std::vector<int32_t> elem_of_root((size_t)nt, -1), elem((size_t)N);
@@ -302,7 +346,6 @@ void build_precond(aim_plan* p, cudaStream_t s) {
         std::vector<int64_t> fill(rptr.begin(), rptr.end() - 1);
         for (long long n = 0; n < N; ++n) rows[fill[elem[n]]++] = (int32_t)n;
     }
-    // per element: smallest triangle / vertex id and the translation origin
     std::vector<int32_t> tmin(ne, INT32_MAX), vmin(ne, INT32_MAX);
     for (int e = 0; e < ne; ++e)
         for (int64_t q = rptr[e]; q < rptr[e + 1]; ++q)
@@ -331,7 +374,7 @@ void build_precond(aim_plan* p, cudaStream_t s) {
             }
         return true;
     };
-    std::vector<int32_t> map(ne), reps;
+    std::vector<int32_t> group(ne), reps;
     for (int e = 0; e < ne; ++e) {
         int found = -1;
         for (size_t r = 0; r < reps.size() && found < 0; ++r)
@@ -340,32 +383,29 @@ void build_precond(aim_plan* p, cudaStream_t s) {
             found = (int)reps.size();
             reps.push_back(e);
         }
-        map[e] = found;
+        group[e] = found;
     }
-    const int nd = (int)reps.size();
-    std::vector<int64_t> iptr(nd + 1, 0);
+    p->el_rows = p->alloc<int32_t>(N);
+    p->el_rptr = p->alloc<int64_t>(ne + 1);
+    h2d(p->el_rows, rows.data(), sizeof(int32_t) * N, s);
+    h2d(p->el_rptr, rptr.data(), sizeof(int64_t) * (ne + 1), s);
+    p->el_rows_h = std::move(rows);
+    p->el_rptr_h = std::move(rptr);
+    p->el_group_h = std::move(group);
+    p->el_reps_h = std::move(reps);
+    p->el_count = ne;
+}
+
+void invert_blocks(double2* mats, const std::vector<int64_t>& off_h, const std::vector<int>& sizes, cudaStream_t s) {
+    const int nd = (int)sizes.size();
+    if (!nd) return;
     std::vector<GjBlk> blk(nd);
     int maxn = 0, poff = 0;
     for (int d = 0; d < nd; ++d) {
-        const int n = (int)(rptr[reps[d] + 1] - rptr[reps[d]]);
-        blk[d] = GjBlk{iptr[d], n, poff};
-        iptr[d + 1] = iptr[d] + (int64_t)n * n;
-        poff += n;
-        maxn = std::max(maxn, n);
+        blk[d] = GjBlk{off_h[d], sizes[d], poff};
+        poff += sizes[d];
+        maxn = std::max(maxn, sizes[d]);
     }
-    p->pc_rows = p->alloc<int32_t>(N);
-    p->pc_rptr = p->alloc<int64_t>(ne + 1);
-    p->pc_map = p->alloc<int32_t>(ne);
-    p->pc_iptr = p->alloc<int64_t>(nd + 1);
-    p->pc_inv = p->alloc<double2>(iptr[nd]);
-    h2d(p->pc_rows, rows.data(), sizeof(int32_t) * N, s);
-    h2d(p->pc_rptr, rptr.data(), sizeof(int64_t) * (ne + 1), s);
-    h2d(p->pc_map, map.data(), sizeof(int32_t) * ne, s);
-    h2d(p->pc_iptr, iptr.data(), sizeof(int64_t) * (nd + 1), s);
-    // dense blocks Z_ex_sym of the representatives
-    for (int d = 0; d < nd; ++d)
-        fill_exact_block(p, p->pc_rows + rptr[reps[d]], blk[d].n, p->pc_inv + iptr[d], s);
-    // batched Gauss-Jordan inversion
     GjBlk* dblk = nullptr;
     int32_t* perm = nullptr;
     double2* colk = nullptr;
@@ -377,12 +417,12 @@ void build_precond(aim_plan* p, cudaStream_t s) {
     AIM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
     AIM_CUDA(cudaMemcpyAsync(dblk, blk.data(), sizeof(GjBlk) * nd, cudaMemcpyHostToDevice, s));
     for (int k = 0; k < maxn; ++k) {
-        gj_pivot_kernel<<<nd, 256, 0, s>>>(dblk, p->pc_inv, k, perm, colk, bad);
+        gj_pivot_kernel<<<nd, 256, 0, s>>>(dblk, mats, k, perm, colk, bad);
         note_launch("gj_pivot");
-        gj_elim_kernel<<<dim3((maxn + 7) / 8, nd), 256, 0, s>>>(dblk, p->pc_inv, k, colk);
+        gj_elim_kernel<<<dim3((maxn + 7) / 8, nd), 256, 0, s>>>(dblk, mats, k, colk);
         note_launch("gj_elim");
     }
-    gj_unperm_kernel<<<nd, 256, 0, s>>>(dblk, p->pc_inv, perm);
+    gj_unperm_kernel<<<nd, 256, 0, s>>>(dblk, mats, perm);
     note_launch("gj_unperm");
     int hbad = 0;
     AIM_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -391,56 +431,105 @@ void build_precond(aim_plan* p, cudaStream_t s) {
     cudaFree(perm);
     cudaFree(colk);
     cudaFree(bad);
-    if (hbad) {
-        free_precond(p);
-        throw Error(AIM_E_BREAKDOWN, "block-Jacobi: a singular or non-finite element block");
-    }
-    // apply jobs: per distinct inverse, the list of elements using it
-    std::vector<int32_t> elist;
-    std::vector<std::vector<int32_t>> users(nd);
-    for (int e = 0; e < ne; ++e) users[map[e]].push_back(e);
-    p->pc_jobs.clear();
-    std::vector<int32_t> gemv_list;
-    for (int d = 0; d < nd; ++d) {
-        if (users[d].size() >= 8) {
-            p->pc_jobs.push_back({d, (int)elist.size(), (int)users[d].size(), blk[d].n, iptr[d]});
-            elist.insert(elist.end(), users[d].begin(), users[d].end());
-        } else {
-            gemv_list.insert(gemv_list.end(), users[d].begin(), users[d].end());
-        }
-    }
-    p->pc_gemv_off = (int)elist.size();
-    p->pc_gemv_cnt = (int)gemv_list.size();
-    elist.insert(elist.end(), gemv_list.begin(), gemv_list.end());
-    p->pc_elist = p->alloc<int32_t>(std::max<size_t>(1, elist.size()));
-    if (!elist.empty()) h2d(p->pc_elist, elist.data(), sizeof(int32_t) * elist.size(), s);
-    p->pc_nblocks = ne;
-    p->pc_ndistinct = nd;
-    p->pc_maxn = maxn;
-    p->pc_bytes = 16 * iptr[nd];
-    p->prec_on = 1;
+    if (hbad) throw Error(AIM_E_BREAKDOWN, "Gauss-Jordan: a singular or non-finite block");
 }
 
-void apply_precond(aim_plan* p, const double2* in, double2* out, cudaStream_t s) {
-    if (!p->prec_on) throw Error(AIM_E_ARG, "no preconditioner built (aim_precond_build)");
-    for (const auto& j : p->pc_jobs) {
-        const dim3 grid((unsigned)((j.n + kPcTile - 1) / kPcTile), (unsigned)((j.m + kPcTile - 1) / kPcTile));
-        pc_gemm_kernel<<<grid, 256, 0, s>>>(p->pc_inv + j.ioff, j.n, p->pc_elist + j.eoff, j.m, p->pc_rows,
-                                            p->pc_rptr, in, out);
-        note_launch("pc_gemm");
+void free_blocks(aim_plan* p, BlockSet& b) {
+    p->release(b.mats);
+    p->release(b.off);
+    p->release(b.map);
+    p->release(b.elist);
+    b = BlockSet{};
+}
+
+void setup_block_apply(aim_plan* p, BlockSet& b, const std::vector<int32_t>& map, const std::vector<int>& sizes,
+                       cudaStream_t s) {
+    const int ne = p->el_count, nd = (int)sizes.size();
+    b.ndistinct = nd;
+    b.maxn = 0;
+    for (int d = 0; d < nd; ++d) b.maxn = std::max(b.maxn, sizes[d]);
+    b.map = p->alloc<int32_t>(ne);
+    h2d(b.map, map.data(), sizeof(int32_t) * ne, s);
+    std::vector<int64_t> off(nd + 1, 0);
+    for (int d = 0; d < nd; ++d) off[d + 1] = off[d] + (int64_t)sizes[d] * sizes[d];
+    std::vector<std::vector<int32_t>> users(nd);
+    for (int e = 0; e < ne; ++e) users[map[e]].push_back(e);
+    std::vector<int32_t> elist, gemv;
+    b.jobs.clear();
+    for (int d = 0; d < nd; ++d) {
+        if (users[d].size() >= 8) {
+            b.jobs.push_back({d, (int)elist.size(), (int)users[d].size(), sizes[d], off[d]});
+            elist.insert(elist.end(), users[d].begin(), users[d].end());
+        } else {
+            gemv.insert(gemv.end(), users[d].begin(), users[d].end());
+        }
     }
-    if (p->pc_gemv_cnt) {
-        const size_t smem = sizeof(double2) * p->pc_maxn;
+    b.gemv_off = (int)elist.size();
+    b.gemv_cnt = (int)gemv.size();
+    elist.insert(elist.end(), gemv.begin(), gemv.end());
+    b.elist = p->alloc<int32_t>(std::max<size_t>(1, elist.size()));
+    if (!elist.empty()) h2d(b.elist, elist.data(), sizeof(int32_t) * elist.size(), s);
+    b.bytes = 16 * off[nd];
+}
+
+void apply_blocks(aim_plan* p, const BlockSet& b, const double2* in, double2* out, bool accumulate, cudaStream_t s) {
+    for (const auto& j : b.jobs) {
+        const dim3 grid((unsigned)((j.n + kPcTile - 1) / kPcTile), (unsigned)((j.m + kPcTile - 1) / kPcTile));
+        pc_gemm_kernel<<<grid, 256, 0, s>>>(b.mats + j.ioff, j.n, b.elist + j.eoff, j.m, p->el_rows, p->el_rptr, in,
+                                            out, accumulate ? 1 : 0);
+        note_launch("blk_gemm");
+    }
+    if (b.gemv_cnt) {
+        const size_t smem = sizeof(double2) * b.maxn;
         static unsigned long long attr_mask = 0;   // per device: the attribute is per device
         if (smem > 48 * 1024 && !(attr_mask >> (p->device & 63) & 1ULL)) {
             AIM_CUDA(cudaFuncSetAttribute(pc_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
             attr_mask |= 1ULL << (p->device & 63);
         }
-        const dim3 grid((unsigned)((p->pc_maxn + 63) / 64), (unsigned)p->pc_gemv_cnt);
-        pc_gemv_kernel<<<grid, 256, smem, s>>>(p->pc_inv, p->pc_iptr, p->pc_map, p->pc_elist + p->pc_gemv_off,
-                                               p->pc_rows, p->pc_rptr, in, out);
-        note_launch("pc_gemv");
+        const dim3 grid((unsigned)((b.maxn + 63) / 64), (unsigned)b.gemv_cnt);
+        pc_gemv_kernel<<<grid, 256, smem, s>>>(b.mats, b.off, b.map, b.elist + b.gemv_off, p->el_rows, p->el_rptr,
+                                               in, out, accumulate ? 1 : 0);
+        note_launch("blk_gemv");
     }
+}
+
+// ------------------------------------------------------ block-Jacobi (D18)
+void free_precond(aim_plan* p) {
+    free_blocks(p, p->pc);
+    p->prec_on = 0;
+}
+
+void build_precond(aim_plan* p, cudaStream_t s) {
+    free_precond(p);
+    ensure_elements(p, s);
+    const int nd = (int)p->el_reps_h.size();
+    std::vector<int> sizes(nd);
+    std::vector<int64_t> off(nd + 1, 0);
+    for (int d = 0; d < nd; ++d) {
+        const int r = p->el_reps_h[d];
+        sizes[d] = (int)(p->el_rptr_h[r + 1] - p->el_rptr_h[r]);
+        off[d + 1] = off[d] + (int64_t)sizes[d] * sizes[d];
+    }
+    BlockSet& b = p->pc;
+    b.mats = p->alloc<double2>(std::max<int64_t>(1, off[nd]));
+    b.off = p->alloc<int64_t>(nd + 1);
+    h2d(b.off, off.data(), sizeof(int64_t) * (nd + 1), s);
+    // dense blocks Z_ex_sym of the representatives, inverted in place
+    for (int d = 0; d < nd; ++d)
+        fill_exact_block(p, p->el_rows + p->el_rptr_h[p->el_reps_h[d]], sizes[d], b.mats + off[d], s);
+    try {
+        invert_blocks(b.mats, off, sizes, s);
+    } catch (...) {
+        free_precond(p);
+        throw;
+    }
+    setup_block_apply(p, b, p->el_group_h, sizes, s);
+    p->prec_on = 1;
+}
+
+void apply_precond(aim_plan* p, const double2* in, double2* out, cudaStream_t s) {
+    if (!p->prec_on) throw Error(AIM_E_ARG, "no preconditioner built (aim_precond_build)");
+    apply_blocks(p, p->pc, in, out, false, s);
 }
 
 }  // namespace aim

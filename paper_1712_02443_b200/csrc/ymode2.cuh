@@ -1,0 +1,207 @@
+// Fused y/z convolution pass for thin planar grids (conv mode 2: C3, C4),
+// included by k_fft.cu (shares its register radices and twiddle constants).
+//
+// Step (ii) of the AIM matvec (eq. AIM_step2) on the
+// x-transformed grid W1[4][Px][Ny][Nz] (one right-hand side): for every
+// (component, kx) plane -- one CTA, the whole [Py][Nz] plane in shared memory:
+//   1. TMA bulk copy of the plane's Ny x Nz values (contiguous), zero rows
+//      Ny .. Py-1 (the y zero padding, D11);
+//   2. forward y FFT of length Py = R1 R2 R3 in place: decimation in
+//      frequency, three radix stages in registers, output in digit-reversed
+//      order (position k1 S1 + k2 R3 + k3 holds ky = k1 + R1 k2 + R1 R2 k3);
+//   3. z convolution as the symmetric Toeplitz product with the 2-D spectrum
+//      G2(kx, ky, |dz|) (1/(Px Py) folded in), thread per ky line;
+//   4. inverse y FFT in place (decimation in time, digit-reversed -> natural);
+//   5. TMA bulk store of rows 0 .. Ny-1 (the pruning).
+// One HBM round trip of the plane instead of the three passes (y forward to
+// the y-padded W2, z Toeplitz on W2, y inverse back) of the unfused mode 2.
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n @!P bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(m)),
+        "r"(phase)
+        : "memory");
+}
+// global -> shared bulk copy (TMA, no tensor map), completion on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(m))
+                 : "memory");
+}
+// shared -> global bulk copy (TMA), bulk-group completion
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// One in-place radix-R stage over the tile [P][NZ]: butterfly j (block j / ST,
+// offset m = j % ST) on positions base + t ST, base = (j / ST) R ST + m.
+//   DIF (forward): b = DFT_R(a) (sign -), b_k *= w_{R ST}^{m k}
+//   DIT (inverse): a_t *= conj(w_{R ST}^{m t}), b = DFT_R(a) (sign +)
+template <int P, int R, int ST, int NZ, bool DIF>
+__device__ __forceinline__ void ym2_stage(double2* tile, const double2* tw) {
+    constexpr int NB = P / R;            // butterflies per column
+    constexpr int TWS = P / (R * ST);    // twiddle exponent scale
+#pragma unroll 1
+    for (int q = threadIdx.x; q < NB * NZ; q += blockDim.x) {
+        const int j = q / NZ, l = q - (q / NZ) * NZ;
+        const int m = j % ST;
+        const int base = (j / ST) * R * ST + m;
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = tile[(base + t * ST) * NZ + l];
+        if constexpr (DIF) {
+            dft<R>(a, -1.0);
+#pragma unroll
+            for (int k = 1; k < R; ++k) {
+                const int e = (m * k * TWS) % P;
+                if (e) a[k] = cmul(a[k], tw[e]);
+            }
+        } else {
+#pragma unroll
+            for (int t = 1; t < R; ++t) {
+                const int e = (m * t * TWS) % P;
+                if (e) {
+                    const double2 w = tw[e];
+                    a[t] = cmul(a[t], make_double2(w.x, -w.y));
+                }
+            }
+            dft<R>(a, 1.0);
+        }
+#pragma unroll
+        for (int t = 0; t < R; ++t) tile[(base + t * ST) * NZ + l] = a[t];
+    }
+}
+
+template <int P, int R1, int R2, int R3, int NZ, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ W, int Ny, int Px, int PyH,
+                                                           const double2* __restrict__ spec,
+                                                           const double2* __restrict__ twg, int planes) {
+    static_assert(R1 * R2 * R3 == P, "radices");
+    constexpr int S1 = R2 * R3;
+    extern __shared__ __align__(128) unsigned char ym2_raw[];
+    double2* tile = reinterpret_cast<double2*>(ym2_raw);     // [P][NZ]
+    double2* tw = tile + P * NZ;                             // [P]
+    __shared__ __align__(8) uint64_t mbar;
+    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = twg[e];
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned bytes = (unsigned)(Ny * NZ * sizeof(double2));
+    unsigned phase = 0;
+    for (int q = blockIdx.x; q < planes; q += gridDim.x) {
+        double2* plane = W + (long long)q * Ny * NZ;
+        const int kx = q % Px;
+        const int ax = min(kx, Px - kx);
+        // 1. load (the previous plane's store must have read the tile)
+        fence_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_wait_read();
+            mbar_expect_tx(&mbar, bytes);
+            bulk_g2s(tile, plane, bytes, &mbar);
+        }
+        for (int e = Ny * NZ + threadIdx.x; e < P * NZ; e += blockDim.x) tile[e] = make_double2(0, 0);
+        mbar_wait(&mbar, phase);
+        phase ^= 1;
+        __syncthreads();
+        // 2. forward y FFT (DIF), digit-reversed output
+        ym2_stage<P, R1, S1, NZ, true>(tile, tw);
+        __syncthreads();
+        ym2_stage<P, R2, R3, NZ, true>(tile, tw);
+        __syncthreads();
+        ym2_stage<P, R3, 1, NZ, true>(tile, tw);
+        __syncthreads();
+        // 3. z Toeplitz with G2(kx, ky, |dz|)
+        const double2* g2 = spec + (long long)ax * PyH * NZ;
+#pragma unroll 1
+        for (int p = threadIdx.x; p < P; p += blockDim.x) {
+            const int k1 = p / S1, k2 = (p / R3) % R2, k3 = p % R3;
+            const int ky = k1 + R1 * k2 + R1 * R2 * k3;
+            const int ay = min(ky, P - ky);
+            const double2* g = g2 + ay * NZ;
+            double2* row = tile + p * NZ;
+            double2 gk[NZ], in[NZ];
+#pragma unroll
+            for (int d = 0; d < NZ; ++d) gk[d] = __ldg(&g[d]);
+#pragma unroll
+            for (int z = 0; z < NZ; ++z) in[z] = row[z];
+#pragma unroll
+            for (int z = 0; z < NZ; ++z) {
+                double2 acc = cmul(gk[0], in[z]);
+#pragma unroll
+                for (int d = 1; d < NZ; ++d) {
+                    if (z - d < 0 && z + d >= NZ) continue;
+                    double2 sum = z - d >= 0 ? in[z - d] : make_double2(0, 0);
+                    if (z + d < NZ) sum = z - d >= 0 ? cadd(sum, in[z + d]) : in[z + d];
+                    acc.x = fma(gk[d].x, sum.x, fma(-gk[d].y, sum.y, acc.x));
+                    acc.y = fma(gk[d].x, sum.y, fma(gk[d].y, sum.x, acc.y));
+                }
+                row[z] = acc;
+            }
+        }
+        __syncthreads();
+        // 4. inverse y FFT (DIT), natural output
+        ym2_stage<P, R3, 1, NZ, false>(tile, tw);
+        __syncthreads();
+        ym2_stage<P, R2, R3, NZ, false>(tile, tw);
+        __syncthreads();
+        ym2_stage<P, R1, S1, NZ, false>(tile, tw);
+        // 5. store rows 0 .. Ny-1
+        fence_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) bulk_s2g(plane, tile, bytes);
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// Fused mode-2 pass for the compiled plans (Py, Nz) = (784, 14) (C4) and
+// (486, 13) (C3); complex128, one right-hand side.  Returns false if no plan
+// matches (the caller runs the three separate passes).  AIM_YZ_FUSED=0
+// disables it (A/B and parity tests).
+bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, const void* spec, const FftAxis& ay,
+                   cudaStream_t s) {
+    const char* env = getenv("AIM_YZ_FUSED");
+    const bool off = env && env[0] == '0';
+    if (off || prec != 0 || R != 1) return false;
+    int dev = 0;
+    AIM_CUDA(cudaGetDevice(&dev));
+    const int planes = 4 * Px;
+    const int PyH = Py / 2 + 1;
+#define YM2_CASE(PP, A, B, C, NZ, NT, MINB)                                                                   \
+    if (Py == PP && Nz == NZ) {                                                                               \
+        const size_t smem = sizeof(double2) * (size_t)PP * (NZ + 1);                                          \
+        static unsigned long long mask = 0; /* cudaFuncSetAttribute is per device */                         \
+        if (!(mask >> (dev & 63) & 1ULL)) {                                                                   \
+            AIM_CUDA(cudaFuncSetAttribute(ymode2_kernel<PP, A, B, C, NZ, NT, MINB>,                           \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+            mask |= 1ULL << (dev & 63);                                                                       \
+        }                                                                                                     \
+        ymode2_kernel<PP, A, B, C, NZ, NT, MINB><<<148 * MINB, NT, smem, s>>>(                                \
+            (double2*)W, Ny, Px, PyH, (const double2*)spec, ay.tw, planes);                                   \
+        note_launch("ymode2");                                                                                \
+        return true;                                                                                          \
+    }
+    YM2_CASE(784, 16, 7, 7, 14, 448, 1)
+    YM2_CASE(486, 9, 9, 6, 13, 256, 2)
+#undef YM2_CASE
+    return false;
+}
