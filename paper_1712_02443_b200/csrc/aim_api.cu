@@ -24,6 +24,8 @@ static thread_local std::string g_err;
 static thread_local long long g_launches = 0;
 
 std::string& last_error() { return g_err; }
+long long launch_counter() { return g_launches; }
+void add_launches(long long n) { g_launches += n; }
 
 void note_launch(const char* name) {
     ++g_launches;
@@ -229,7 +231,13 @@ void destroy_plan(aim_plan* p) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
-    cudaDeviceSynchronize();
+    // the plan's own work is on its streams; the caller orders (or has
+    // finished) the products it queued on its streams before destroying
+    for (cudaStream_t st : {p->stream, p->side, p->hp_in, p->hp_out})
+        if (st) cudaStreamSynchronize(st);
+    for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
+    if (p->gx_fork) cudaEventDestroy(p->gx_fork);
+    if (p->gx_join) cudaEventDestroy(p->gx_join);
     for (auto& a : p->allocs) cudaFree(a.first);
     for (int d = 0; d < 3; ++d)
         if (p->ax[d].tw) cudaFree(p->ax[d].tw);

@@ -39,6 +39,8 @@ inline void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
 }
 
 void note_launch(const char* name);  // counts launches, checks launch errors
+long long launch_counter();          // kernels launched by this thread (aim_launch_count)
+void add_launches(long long n);      // graph replays count their captured kernels
 std::string& last_error();           // thread-local message behind aim_last_error()
 
 inline int fail(int status, const std::string& msg) {
@@ -273,6 +275,18 @@ struct aim_plan {
     int hs_nrhs = 0;
     double2* hx = nullptr;
     double2* hy = nullptr;
+
+    // aim_matvec as CUDA graphs (k_matvec.cu matvec): one per (x, y, nrhs)
+    struct MvGraph {
+        const void* x;
+        void* y;
+        int R;
+        cudaGraphExec_t exec;
+        long long kernels;
+    };
+    std::vector<MvGraph> graphs;
+    std::vector<char> mv_warm;    // an eager product has run for this nrhs
+    cudaEvent_t gx_fork = nullptr, gx_join = nullptr;
 
     // aim_matvec_host_steps: double-buffered device vectors, copy streams, events
     int hp_nrhs = 0;

@@ -867,11 +867,11 @@ static void launch_interp_t(aim_plan* p, const C* Phi, C* y, int R, bool accumul
             const double keta = p->k * eta0();
 #define IM_CALL(MT, NT)                                                                                            \
     {                                                                                                              \
-        static bool attr = false;                                                                                  \
-        if (!attr) {                                                                                               \
+        static unsigned long long attr = 0; /* per device */                                                      \
+        if (!(attr >> (p->device & 63) & 1ULL)) {                                                                  \
             AIM_CUDA(cudaFuncSetAttribute(interp_mma_kernel<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                           (int)interp_mma_smem<MT, NT>()));                                        \
-            attr = true;                                                                                           \
+            attr |= 1ULL << (p->device & 63);                                                                      \
         }                                                                                                          \
         interp_mma_kernel<MT, NT><<<nblk(p->im_count, kNmWarps), 32 * kNmWarps, interp_mma_smem<MT, NT>(), s>>>(   \
             p->im_rows, p->im_cptr, p->im_vptr, p->im_mask, p->im_node, p->im_val, (const double2*)Phi, p->Ng,     \
@@ -948,11 +948,11 @@ static void launch_near_t(aim_plan* p, const C* x, C* y, int R, cudaStream_t s) 
             if (p->N * (long long)R >= (1LL << 31)) throw Error(AIM_E_ARG, "near_mma: N * nrhs exceeds 2^31");
 #define NM_CALL(MT, NT)                                                                                        \
     {                                                                                                          \
-        static bool attr = false;                                                                              \
-        if (!attr) {                                                                                           \
+        static unsigned long long attr = 0; /* per device */                                                  \
+        if (!(attr >> (p->device & 63) & 1ULL)) {                                                              \
             AIM_CUDA(cudaFuncSetAttribute(near_mma_kernel<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                           (int)near_mma_smem<MT, NT>()));                                      \
-            attr = true;                                                                                       \
+            attr |= 1ULL << (p->device & 63);                                                                  \
         }                                                                                                      \
         near_mma_kernel<MT, NT><<<nblk(p->nm_count, kNmWarps), 32 * kNmWarps, near_mma_smem<MT, NT>(), s>>>(   \
             p->nm_rows, p->nm_cptr, p->nm_vptr, p->nm_mask, p->nm_col, p->nm_val, (const double2*)x,           \
@@ -1047,6 +1047,8 @@ void ensure_workspace(aim_plan* p, int R) {
     p->W1 = (double2*)p->alloc<float2>(es * 4 * Px * Ny * Nz * R);
     if (p->planar != 1) p->W2 = (double2*)p->alloc<float2>(es * 4 * Px * Py * Nz * R);
     p->ws_nrhs = R;
+    for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);   // they captured the old buffers
+    p->graphs.clear();
 }
 
 struct Prof {
@@ -1132,8 +1134,7 @@ void convolve(aim_plan* p, const void* Q, void* Phi, int R, cudaStream_t s) {
 // interpolation, which accumulates the far field into y.  (Running the SpMV
 // on a side stream bought nothing: its 14k CTAs occupy every SM and the
 // persistent FFT CTAs queue behind them.)
-void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
-    ensure_workspace(p, R);
+static void matvec_body(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
     Prof pr(p);
     pr.mark(0, s);
     pr.mark(7, s);
@@ -1145,6 +1146,63 @@ void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
     pr.mark(5, s);
     launch_interp(p, p->Q, y, R, true, s);
     pr.mark(6, s);
+}
+
+// The product as a CUDA graph (small products are launch
+// bound): the first product for an nrhs runs eagerly (it builds lazily
+// created tables and sets kernel attributes); later products are captured
+// once per (x, y, nrhs) on the plan's stream, instantiated, and replayed with
+// an event fork/join onto the caller's stream.  Profiling (aim_profile) and
+// AIM_GRAPH=0 run eagerly.
+void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
+    ensure_workspace(p, R);
+    const char* env = getenv("AIM_GRAPH");
+    const bool graphs = !(env && env[0] == '0');
+    const bool warm = R < (int)p->mv_warm.size() && p->mv_warm[R];
+    if (!graphs || p->prof || !warm) {
+        matvec_body(p, x, y, R, s);
+        if (R >= (int)p->mv_warm.size()) p->mv_warm.resize(R + 1, 0);
+        p->mv_warm[R] = 1;
+        return;
+    }
+    aim_plan::MvGraph* g = nullptr;
+    for (auto& q : p->graphs)
+        if (q.x == x && q.y == y && q.R == R) g = &q;
+    if (!g) {
+        if (p->graphs.size() >= 128) {
+            cudaGraphExecDestroy(p->graphs.front().exec);
+            p->graphs.erase(p->graphs.begin());
+        }
+        cudaGraph_t graph;
+        const long long before = launch_counter();
+        AIM_CUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            matvec_body(p, x, y, R, p->stream);
+        } catch (...) {
+            cudaStreamEndCapture(p->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        AIM_CUDA(cudaStreamEndCapture(p->stream, &graph));
+        cudaGraphExec_t exec;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        AIM_CUDA(e);
+        const long long nk = launch_counter() - before;
+        add_launches(-nk);      // counted when the graph is launched
+        p->graphs.push_back({x, y, R, exec, nk});
+        g = &p->graphs.back();
+    }
+    if (!p->gx_fork) {
+        AIM_CUDA(cudaEventCreateWithFlags(&p->gx_fork, cudaEventDisableTiming));
+        AIM_CUDA(cudaEventCreateWithFlags(&p->gx_join, cudaEventDisableTiming));
+    }
+    AIM_CUDA(cudaEventRecord(p->gx_fork, s));
+    AIM_CUDA(cudaStreamWaitEvent(p->stream, p->gx_fork, 0));
+    AIM_CUDA(cudaGraphLaunch(g->exec, p->stream));
+    AIM_CUDA(cudaEventRecord(p->gx_join, p->stream));
+    AIM_CUDA(cudaStreamWaitEvent(s, p->gx_join, 0));
+    add_launches(g->kernels);
 }
 
 }  // namespace aim

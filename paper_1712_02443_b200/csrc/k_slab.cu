@@ -60,6 +60,10 @@ struct NcclApi {
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     const char* (*ErrStr)(ncclResult_t) = nullptr;
 };
 
@@ -81,6 +85,9 @@ static NcclApi& nccl() {
     a.Send = (decltype(a.Send))sym("ncclSend");
     a.Recv = (decltype(a.Recv))sym("ncclRecv");
     a.Bcast = (decltype(a.Bcast))sym("ncclBroadcast");
+    a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
+    a.CommGetAsyncError = (decltype(a.CommGetAsyncError))sym("ncclCommGetAsyncError");
+    a.CommAbort = (decltype(a.CommAbort))sym("ncclCommAbort");
     a.ErrStr = (decltype(a.ErrStr))sym("ncclGetErrorString");
     a.h = h;
     return a;
@@ -271,6 +278,9 @@ struct aim_slab {
     cudaEvent_t ev_x = nullptr, ev_n = nullptr;
     std::vector<std::pair<void*, size_t>> allocs;
     int64_t bytes_a2a = 0, bytes_halo = 0;   // per matvec and RHS, per rank (max)
+    double2* gm_b = nullptr;              // distributed GMRES: local right-hand side / solution
+    double2* gm_x = nullptr;
+    long long gm_n = 0;
 
     template <class T>
     T* alloc(size_t n) {
@@ -568,16 +578,77 @@ static void halo_copy(aim_slab* S, const aim_slab_rank& Rk, double2* grid, doubl
     }
 }
 
-static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaStream_t s) {
-    slab_workspace(S, R);
+static void check_nccl(aim_slab* S);
+
+// Point-to-point exchanges of one phase: every rank this
+// process holds posts its sends and receives, then run() executes them --
+// over NCCL (one rank per process: grouped ncclSend/ncclRecv, then an async
+// error check that aborts the communicator so peers do not hang), or, with
+// all ranks in this process, as device copies matching each receive with the
+// send posted for it.  Both modes walk the same schedule, buffers and offsets.
+struct Transport {
+    aim_slab* S;
+    cudaStream_t s;
+    struct Op {
+        int self, peer;
+        double2* buf;
+        size_t n;   // doubles
+    };
+    std::vector<Op> sends, recvs;
+    void send(int self, const double2* buf, size_t n, int to) { sends.push_back({self, to, (double2*)buf, n}); }
+    void recv(int self, double2* buf, size_t n, int from) { recvs.push_back({self, from, buf, n}); }
+    void run() {
+        if (!S->virt) {
+            NcclApi& nc = nccl();
+            AIM_NCCL(nc.GroupStart());
+            for (size_t i = 0; i < std::max(sends.size(), recvs.size()); ++i) {
+                if (i < sends.size() && sends[i].n)
+                    AIM_NCCL(nc.Send(sends[i].buf, sends[i].n, ncclDouble, sends[i].peer, S->comm, s));
+                if (i < recvs.size() && recvs[i].n)
+                    AIM_NCCL(nc.Recv(recvs[i].buf, recvs[i].n, ncclDouble, recvs[i].peer, S->comm, s));
+            }
+            AIM_NCCL(nc.GroupEnd());
+            check_nccl(S);
+        } else {
+            std::vector<char> used(sends.size(), 0);
+            for (const Op& r : recvs) {
+                size_t k = 0;
+                while (k < sends.size() && (used[k] || sends[k].self != r.peer || sends[k].peer != r.self)) ++k;
+                if (k == sends.size() || sends[k].n != r.n)
+                    throw Error(AIM_E_ARG, "slab exchange: receive " + std::to_string(r.peer) + " -> " +
+                                               std::to_string(r.self) + " has no matching send");
+                used[k] = 1;
+                if (r.n)
+                    AIM_CUDA(cudaMemcpyAsync(r.buf, sends[k].buf, sizeof(double) * r.n, cudaMemcpyDeviceToDevice, s));
+            }
+            for (char u : used)
+                if (!u) throw Error(AIM_E_ARG, "slab exchange: a send without a matching receive");
+        }
+        sends.clear();
+        recvs.clear();
+    }
+};
+
+// After NCCL work is enqueued: a failed or timed-out peer shows up as an
+// asynchronous error; abort the communicator so the other ranks do not hang.
+static void check_nccl(aim_slab* S) {
+    if (S->virt || !S->comm) return;
+    ncclResult_t st = ncclSuccess;
+    AIM_NCCL(nccl().CommGetAsyncError(S->comm, &st));
+    if (st != ncclSuccess && st != ncclInProgress) {
+        nccl().CommAbort(S->comm);
+        S->comm = nullptr;
+        throw Error(AIM_E_NCCL, std::string("NCCL asynchronous error: ") + nccl().ErrStr(st));
+    }
+}
+
+// The slab product on permuted, replicated x (S->xp): rows [n0, n1) of every
+// held rank are written to S->yp.
+static void slab_core(aim_slab* S, int R, cudaStream_t s) {
     const int G = S->world, M = S->M;
-    const long long N = S->N, NzR = (long long)S->Nz * R, ZR = (long long)S->Zc * R;
+    const long long NzR = (long long)S->Nz * R, ZR = (long long)S->Zc * R;
     const size_t esz = sizeof(double2);
-    NcclApi* nc = S->virt ? nullptr : &nccl();
-    // x in permuted order (replicated)
-    permute_rows_kernel<false><<<nblk(N * 2 * R, 256), 256, 0, s>>>((const double*)x, S->perm, N, 2 * R,
-                                                                     (double*)S->xp);
-    note_launch("slab_permute");
+    Transport T{S, s, {}, {}};
     // near rows on the side stream (they overlap the projection, the FFT passes
     // and the all-to-alls; interpolation waits for them), projection on `s`
     AIM_CUDA(cudaEventRecord(S->ev_x, s));
@@ -592,34 +663,24 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
             AIM_CUDA(cudaMemsetAsync(Rk.Qh, 0, esz * 4 * Rk.Xh * S->Ny * NzR, s));
         }
     }
-    // halo reduce: rank w's planes [Xl, Xh) are added into rank w+1's [0, Xh - Xl)
-    if (S->virt) {
-        for (int w = 0; w + 1 < G; ++w) {
-            aim_slab_rank *A = rank_of(S, w), *Bn = rank_of(S, w + 1);
-            const int hp = A->Xh - A->Xl;
-            halo_copy(S, *A, A->Qh, A->hb, true, A->Xl, hp, R, s);
-            halo_copy(S, *Bn, Bn->Qh, Bn->rb, true, 0, hp, R, s);
-            add_kernel<<<nblk(4LL * hp * S->Ny * NzR, 256), 256, 0, s>>>(Bn->rb, A->hb, 4LL * hp * S->Ny * NzR);
-            note_launch("slab_halo_add");
-            halo_copy(S, *Bn, Bn->Qh, Bn->rb, false, 0, hp, R, s);
-        }
-    } else {
-        // every halo is exactly M planes wide (slabs are >= M wide), except that
-        // the last slab has none
-        aim_slab_rank& Rk = S->ranks[0];
+    // halo reduce: planes [Xl, Xl + M) of rank w are added into planes [0, M)
+    // of rank w+1 (every slab is >= M planes wide; the last has no halo)
+    const size_t hcnt = 2 * (size_t)4 * M * S->Ny * NzR;   // doubles
+    for (auto& Rk : S->ranks) {
         const int w = Rk.rank;
-        const size_t hcnt = 2 * (size_t)4 * M * S->Ny * NzR;   // doubles
-        if (w + 1 < G) halo_copy(S, Rk, Rk.Qh, Rk.hb, true, Rk.Xl, M, R, s);
-        AIM_NCCL(nc->GroupStart());
-        if (w + 1 < G) AIM_NCCL(nc->Send(Rk.hb, hcnt, ncclDouble, w + 1, S->comm, s));
-        if (w > 0) AIM_NCCL(nc->Recv(Rk.rb, hcnt, ncclDouble, w - 1, S->comm, s));
-        AIM_NCCL(nc->GroupEnd());
-        if (w > 0) {
-            halo_copy(S, Rk, Rk.Qh, Rk.sb, true, 0, M, R, s);
-            add_kernel<<<nblk(hcnt / 2, 256), 256, 0, s>>>(Rk.sb, Rk.rb, (long long)(hcnt / 2));
-            note_launch("slab_halo_add");
-            halo_copy(S, Rk, Rk.Qh, Rk.sb, false, 0, M, R, s);
+        if (w + 1 < G) {
+            halo_copy(S, Rk, Rk.Qh, Rk.hb, true, Rk.Xl, M, R, s);
+            T.send(w, Rk.hb, hcnt, w + 1);
         }
+        if (w > 0) T.recv(w, Rk.rb, hcnt, w - 1);
+    }
+    T.run();
+    for (auto& Rk : S->ranks) {
+        if (Rk.rank == 0) continue;
+        halo_copy(S, Rk, Rk.Qh, Rk.sb, true, 0, M, R, s);
+        add_kernel<<<nblk(hcnt / 2, 256), 256, 0, s>>>(Rk.sb, Rk.rb, (long long)(hcnt / 2));
+        note_launch("slab_halo_add");
+        halo_copy(S, Rk, Rk.Qh, Rk.sb, false, 0, M, R, s);
     }
     // y (3-D: and z) forward on the owned planes, pack for all-to-all #1
     for (auto& Rk : S->ranks) {
@@ -630,11 +691,18 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
                                                                 Rk.d_off1);
         note_launch("slab_pack");
     }
-    // all-to-all #1: block (w -> v) = [4 kys_v][Xl_w][ZR] at sb(w) offset off1_w[v]; lands in T_v at x = X_w
+    // all-to-all #1: block (w -> v) = [4 kys_v][Xl_w][ZR] at sb(w) offset off1(w, v);
+    // rank v receives the blocks of w = 0 .. G-1 back to back in rb and places
+    // each at x = X_w of its pencils T
     auto blk1 = [&](int w, int v) { return 4LL * (S->KY[v + 1] - S->KY[v]) * (S->X[w + 1] - S->X[w]) * ZR; };
     auto off1 = [&](int w, int v) {
         long long o = 0;
         for (int u = 0; u < v; ++u) o += blk1(w, u);
+        return o;
+    };
+    auto offr = [&](int v, int w) {   // receive offset of the block from w on rank v
+        long long o = 0;
+        for (int u = 0; u < w; ++u) o += blk1(u, v);
         return o;
     };
     auto place = [&](aim_slab_rank& Dv, const double2* src, int w, bool into_T) {
@@ -645,26 +713,16 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
         if (into_T) AIM_CUDA(cudaMemcpy2DAsync(t, tp, src, wb, wb, 4 * kys, cudaMemcpyDeviceToDevice, s));
         else AIM_CUDA(cudaMemcpy2DAsync((void*)src, wb, t, tp, wb, 4 * kys, cudaMemcpyDeviceToDevice, s));
     };
-    if (S->virt) {
-        for (int w = 0; w < G; ++w)
-            for (int v = 0; v < G; ++v) place(*rank_of(S, v), rank_of(S, w)->sb + off1(w, v), w, true);
-    } else {
-        aim_slab_rank& Rk = S->ranks[0];
+    for (auto& Rk : S->ranks) {
         const int w = Rk.rank;
-        long long ro = 0;
-        AIM_NCCL(nc->GroupStart());
         for (int v = 0; v < G; ++v) {
-            AIM_NCCL(nc->Send(Rk.sb + off1(w, v), 2 * (size_t)blk1(w, v), ncclDouble, v, S->comm, s));
-            AIM_NCCL(nc->Recv(Rk.rb + ro, 2 * (size_t)blk1(v, w), ncclDouble, v, S->comm, s));
-            ro += blk1(v, w);
-        }
-        AIM_NCCL(nc->GroupEnd());
-        ro = 0;
-        for (int v = 0; v < G; ++v) {
-            place(Rk, Rk.rb + ro, v, true);
-            ro += blk1(v, w);
+            T.send(w, Rk.sb + off1(w, v), 2 * (size_t)blk1(w, v), v);
+            T.recv(w, Rk.rb + offr(w, v), 2 * (size_t)blk1(v, w), v);
         }
     }
+    T.run();
+    for (auto& Rk : S->ranks)
+        for (int v = 0; v < G; ++v) place(Rk, Rk.rb + offr(Rk.rank, v), v, true);
     // x forward, z Toeplitz x G2 (3-D: x G^), x inverse on the ky pencils
     for (auto& Rk : S->ranks) {
         if (S->planar == 2) {
@@ -718,27 +776,19 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
         q.Pfold = S->Py;
         if (q.Px > 0) launch_planar_yz(q, s);
     }
-    // all-to-all #2 (reverse): T_v rows at x = X_w -> rank w, unpacked into Wy_w
-    if (S->virt) {
-        for (int w = 0; w < G; ++w)
-            for (int v = 0; v < G; ++v) place(*rank_of(S, v), rank_of(S, w)->rb + off1(w, v), w, false);
-    } else {
-        aim_slab_rank& Rk = S->ranks[0];
-        const int w = Rk.rank;
-        long long so = 0;
-        for (int v = 0; v < G; ++v) {
-            place(Rk, Rk.sb + so, v, false);
-            so += blk1(v, w);
+    // all-to-all #2 (reverse): rank v packs its pencil rows at x = X_w back to
+    // back in sb (offset offr(v, w)) and sends them to w, which receives them at
+    // rb offset off1(w, v) -- the layout all-to-all #1 read from -- and unpacks
+    for (auto& Rk : S->ranks)
+        for (int w = 0; w < G; ++w) place(Rk, Rk.sb + offr(Rk.rank, w), w, false);
+    for (auto& Rk : S->ranks) {
+        const int v = Rk.rank;
+        for (int w = 0; w < G; ++w) {
+            T.send(v, Rk.sb + offr(v, w), 2 * (size_t)blk1(w, v), w);
+            T.recv(v, Rk.rb + off1(v, w), 2 * (size_t)blk1(v, w), w);
         }
-        so = 0;
-        AIM_NCCL(nc->GroupStart());
-        for (int v = 0; v < G; ++v) {
-            AIM_NCCL(nc->Send(Rk.sb + so, 2 * (size_t)blk1(v, w), ncclDouble, v, S->comm, s));
-            AIM_NCCL(nc->Recv(Rk.rb + off1(w, v), 2 * (size_t)blk1(w, v), ncclDouble, v, S->comm, s));
-            so += blk1(v, w);
-        }
-        AIM_NCCL(nc->GroupEnd());
     }
+    T.run();
     for (auto& Rk : S->ranks) {
         const long long tot = 4LL * Rk.Xl * S->Py * ZR;
         slab_pack_kernel<true><<<nblk(tot, 256), 256, 0, s>>>(Rk.Wy, Rk.rb, Rk.Xl, S->Py, ZR, S->kyown, S->d_KY,
@@ -747,42 +797,98 @@ static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaSt
         if (!S->planar) slab_zpass(S, Rk, R, true, s);
         slab_ypass(S, Rk, R, true, s);   // Phi on the owned planes, into Qh
     }
-    // Phi halo: planes [Xl, Xh) of rank w <- planes [0, Xh - Xl) of rank w+1
-    if (S->virt) {
-        for (int w = 0; w + 1 < G; ++w) {
-            aim_slab_rank *A = rank_of(S, w), *Bn = rank_of(S, w + 1);
-            const int hp = A->Xh - A->Xl;
-            halo_copy(S, *Bn, Bn->Qh, A->hb, true, 0, hp, R, s);
-            halo_copy(S, *A, A->Qh, A->hb, false, A->Xl, hp, R, s);
-        }
-    } else {
-        aim_slab_rank& Rk = S->ranks[0];
+    // Phi halo: planes [Xl, Xl + M) of rank w <- planes [0, M) of rank w+1
+    for (auto& Rk : S->ranks) {
         const int w = Rk.rank;
-        const size_t hcnt = 2 * (size_t)4 * M * S->Ny * NzR;   // doubles
-        if (w > 0) halo_copy(S, Rk, Rk.Qh, Rk.rb, true, 0, M, R, s);
-        AIM_NCCL(nc->GroupStart());
-        if (w > 0) AIM_NCCL(nc->Send(Rk.rb, hcnt, ncclDouble, w - 1, S->comm, s));
-        if (w + 1 < G) AIM_NCCL(nc->Recv(Rk.hb, hcnt, ncclDouble, w + 1, S->comm, s));
-        AIM_NCCL(nc->GroupEnd());
-        if (w + 1 < G) halo_copy(S, Rk, Rk.Qh, Rk.hb, false, Rk.Xl, M, R, s);
+        if (w > 0) {
+            halo_copy(S, Rk, Rk.Qh, Rk.rb, true, 0, M, R, s);
+            T.send(w, Rk.rb, hcnt, w - 1);
+        }
+        if (w + 1 < G) T.recv(w, Rk.hb, hcnt, w + 1);
     }
+    T.run();
+    for (auto& Rk : S->ranks)
+        if (Rk.rank + 1 < G) halo_copy(S, Rk, Rk.Qh, Rk.hb, false, Rk.Xl, M, R, s);
     // interpolation of the owned RWGs onto their near rows
     AIM_CUDA(cudaStreamWaitEvent(s, S->ev_n, 0));
     for (auto& Rk : S->ranks)
         if (Rk.n1 > Rk.n0) launch_interp(Rk.sub, Rk.Qh, S->yp + Rk.n0 * R, R, true, s);
-    // every rank gets all rows
-    if (!S->virt) {
-        AIM_NCCL(nc->GroupStart());
-        for (int v = 0; v < G; ++v) {
-            double2* blk = S->yp + S->nstart[v] * R;
-            const size_t cnt = 2 * (size_t)(S->nstart[v + 1] - S->nstart[v]) * R;
-            if (cnt) AIM_NCCL(nc->Bcast(blk, blk, cnt, ncclDouble, v, S->comm, s));
-        }
-        AIM_NCCL(nc->GroupEnd());
+}
+
+// every rank receives all rows of a permuted row vector (NCCL: a broadcast
+// from each owner; in-process the ranks share the vector already)
+static void slab_allgather_rows(aim_slab* S, double2* v, int R, cudaStream_t s) {
+    if (S->virt) return;
+    NcclApi& nc = nccl();
+    AIM_NCCL(nc.GroupStart());
+    for (int w = 0; w < S->world; ++w) {
+        double2* blk = v + S->nstart[w] * R;
+        const size_t cnt = 2 * (size_t)(S->nstart[w + 1] - S->nstart[w]) * R;
+        if (cnt) AIM_NCCL(nc.Bcast(blk, blk, cnt, ncclDouble, w, S->comm, s));
     }
+    AIM_NCCL(nc.GroupEnd());
+    check_nccl(S);
+}
+
+static void slab_matvec(aim_slab* S, const double2* x, double2* y, int R, cudaStream_t s) {
+    slab_workspace(S, R);
+    const long long N = S->N;
+    permute_rows_kernel<false><<<nblk(N * 2 * R, 256), 256, 0, s>>>((const double*)x, S->perm, N, 2 * R,
+                                                                     (double*)S->xp);
+    note_launch("slab_permute");
+    slab_core(S, R, s);
+    slab_allgather_rows(S, S->yp, R, s);
     permute_rows_kernel<true><<<nblk(N * 2 * R, 256), 256, 0, s>>>((const double*)S->yp, S->perm, N, 2 * R,
                                                                     (double*)y);
     note_launch("slab_unpermute");
+}
+
+// GMRES on the slab operator (D15) with the Krylov vectors partitioned by
+// owning rank: each rank keeps its rows [n0, n1) of the
+// permuted order; a product gathers the rank's rows of its input into every
+// rank's x (one broadcast per owner), runs the slab product and keeps its
+// own rows; dot products are local partial sums followed by an NCCL
+// all-reduce of the (j+1) coefficients.  In-process (all ranks held) the
+// vectors span all rows and no reduction is needed.
+static int slab_gmres(aim_slab* S, const double2* V, double2* J, int restart, double tol, int max_iters,
+                      int fixed_iters, int* iters, double* rel_res) {
+    cudaStream_t s = S->base->stream;
+    slab_workspace(S, 1);
+    const long long N = S->N;
+    const long long n0 = S->virt ? 0 : S->ranks[0].n0;
+    const long long nl = S->virt ? N : S->ranks[0].n1 - S->ranks[0].n0;
+    // permuted right-hand side, local rows
+    permute_rows_kernel<false><<<nblk(N * 2, 256), 256, 0, s>>>((const double*)V, S->perm, N, 2, (double*)S->yp);
+    note_launch("slab_permute");
+    if (S->gm_n < nl) {
+        S->release(S->gm_b);
+        S->release(S->gm_x);
+        S->gm_b = S->alloc<double2>(std::max<long long>(1, nl));
+        S->gm_x = S->alloc<double2>(std::max<long long>(1, nl));
+        S->gm_n = nl;
+    }
+    AIM_CUDA(cudaMemcpyAsync(S->gm_b, S->yp + n0, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, s));
+    GmresOps ops;
+    ops.n = nl;
+    ops.matvec = [S, n0, nl](const double2* in, double2* out, cudaStream_t st) {
+        AIM_CUDA(cudaMemcpyAsync(S->xp + n0, in, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, st));
+        slab_allgather_rows(S, S->xp, 1, st);
+        slab_core(S, 1, st);
+        AIM_CUDA(cudaMemcpyAsync(out, S->yp + n0, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, st));
+    };
+    if (!S->virt)
+        ops.allreduce = [S](double2* d, int n, cudaStream_t st) {
+            AIM_NCCL(nccl().AllReduce(d, d, 2 * (size_t)n, ncclDouble, ncclSum, S->comm, st));
+            check_nccl(S);
+        };
+    const int st = gmres_core(S->base, ops, S->gm_b, S->gm_x, restart, tol, max_iters, fixed_iters, iters, rel_res);
+    // J replicated in the caller's order
+    AIM_CUDA(cudaMemcpyAsync(S->yp + n0, S->gm_x, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, s));
+    slab_allgather_rows(S, S->yp, 1, s);
+    permute_rows_kernel<true><<<nblk(N * 2, 256), 256, 0, s>>>((const double*)S->yp, S->perm, N, 2, (double*)J);
+    note_launch("slab_unpermute");
+    AIM_CUDA(cudaStreamSynchronize(s));
+    return st;
 }
 
 }  // namespace aim
@@ -842,29 +948,37 @@ int aim_slab_create(const double* vertices, int64_t nv, const int32_t* triangles
     return AIM_OK;
 }
 
+// A rank that fails after its peers entered a collective would leave them
+// blocked: abort the communicator on any error of a collective entry point.
+static int abort_on_error(aim_slab* S, int st) {
+    if (st < 0 && S && !S->virt && S->comm) {
+        nccl().CommAbort(S->comm);
+        S->comm = nullptr;
+    }
+    return st;
+}
+
 int aim_slab_matvec(aim_slab* S, const void* x, void* y, int32_t nrhs, void* stream) {
     if (!S || !x || !y || nrhs < 1 || x == y) return fail(AIM_E_ARG, "bad argument");
-    return guarded([&] {
+    if (!S->virt && !S->comm) return fail(AIM_E_NCCL, "the communicator was aborted after an earlier error");
+    return abort_on_error(S, guarded([&] {
         slab_matvec(S, (const double2*)x, (double2*)y, nrhs, (cudaStream_t)stream);
         return AIM_OK;
-    });
+    }));
 }
 
 int aim_slab_gmres(aim_slab* S, const void* V, void* J, int32_t restart, double tol, int32_t max_iters,
                    int32_t fixed_iters, int32_t* iters, double* rel_res) {
     if (!S || !V || !J || restart < 1 || !(tol >= 0)) return fail(AIM_E_ARG, "bad argument");
-    return guarded([&] {
+    if (!S->virt && !S->comm) return fail(AIM_E_NCCL, "the communicator was aborted after an earlier error");
+    return abort_on_error(S, guarded([&] {
         int it = 0;
         double rr = 0;
-        GmresOps ops;
-        ops.n = S->base->N;
-        ops.matvec = [S](const double2* in, double2* out, cudaStream_t s) { slab_matvec(S, in, out, 1, s); };
-        const int st = gmres_core(S->base, ops, (const double2*)V, (double2*)J, restart, tol, max_iters,
-                                  fixed_iters, &it, &rr);
+        const int st = slab_gmres(S, (const double2*)V, (double2*)J, restart, tol, max_iters, fixed_iters, &it, &rr);
         if (iters) *iters = it;
         if (rel_res) *rel_res = rr;
         return st;
-    });
+    }));
 }
 
 int aim_slab_query(const aim_slab* S, int32_t rank, int64_t* out) {

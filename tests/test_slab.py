@@ -201,3 +201,78 @@ def test_slab_gmres_matches_single_plan(name, world):
     assert np.linalg.norm(Vh - O.matvec(Jg.cpu().numpy())) / np.linalg.norm(Vh) <= 1e-4 * (1 + 1e-6)
     slab.close()
     single.close()
+
+
+def _nccl_worker(rank, world, port, name, q):
+    """One rank of the multi-process NCCL slab test (one GPU per process)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan
+    from paper_1712_02443_b200.api import slab_nccl_id
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    nid = slab_nccl_id()
+    slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world, rank, nid)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    x = torch.from_numpy(make_vectors(mesh.n_rwg, 3, 5)).cuda()
+    e_mv = float((slab.matvec(x) - single.matvec(x)).norm() / single.matvec(x).norm())
+    V = single.planewave_rhs()
+    J1, it1, _, _ = single.gmres(V, restart=50, tol=1e-4)
+    Jg, itg, _, st = slab.gmres(V, restart=50, tol=1e-4)
+    e_j = float((Jg - J1).norm() / J1.norm())
+    q.put((rank, e_mv, it1, itg, st, e_j))
+    slab.close()
+    single.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "t_m3"])
+def test_slab_nccl_two_ranks(name):
+    """Two processes, one GPU each, NCCL exchanges (halo send/recv, both
+    all-to-alls with real peers, the y gather) and the distributed GMRES
+    (Krylov vectors split by owner, all-reduced dots): equal to the single
+    plan to 1e-13 (product) and +-1 iterations / 1e-5 (GMRES).  Needs two
+    GPUs; skipped on a one-GPU box."""
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_nccl_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, e_mv, it1, itg, st, e_j in res:
+        assert e_mv <= 1e-13 and st == "AIM_OK" and abs(it1 - itg) <= 1 and e_j <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_slab_gmres_virtual_worlds_c2(world):
+    """The in-process transport walks the NCCL schedule (per-peer offsets of
+    both all-to-alls, halos): C2 at full size, G = 2, 3, 8 slabs, the slab
+    GMRES on 60 fixed iterations equals the single plan's to 1e-10."""
+    import torch
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan
+    cfg = get_config("c2")
+    mesh = make_mesh(cfg)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    V = single.planewave_rhs()
+    J1, _, rr1, _ = single.gmres(V, restart=50, tol=1e-4, fixed_iters=60)
+    single.close()
+    slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
+    Jg, itg, rrg, _ = slab.gmres(V, restart=50, tol=1e-4, fixed_iters=60)
+    assert itg == 60
+    assert float((Jg - J1).norm() / J1.norm()) <= 1e-10
+    assert abs(rrg - rr1) <= 1e-8 * rr1
+    slab.close()
