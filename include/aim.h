@@ -205,6 +205,26 @@ int aim_precond_apply(aim_plan* plan, const void* x, void* y, void* stream);
  * bytes of the inverses}. */
 int aim_precond_info(const aim_plan* plan, int64_t* out);
 
+/* ---- repetition-compressed near field (NEXT-3) ------------------------- */
+/*
+ * aim_plan_compress -- mode 1: build and use a repetition-compressed copy of
+ * the precorrected near field ("matrices ... only need to be calculated once
+ * for each distinct element").  Elements (connected
+ * surfaces) that are translates of each other by integer multiples of h sit
+ * identically on the grid, so the near block between elements e and f depends
+ * only on (group(e), group(f), lattice offset f - e): one dictionary block per
+ * key, plus per element its neighbour elements and their keys.  Every
+ * occurrence's structure is verified equal to its block's; the values are
+ * those of the key's first occurrence (other occurrences differ by rounding
+ * only).  aim_matvec then reads the dictionary instead of the near CSR.
+ * mode 0: back to the general near CSR.  Synchronous.  Errors: AIM_E_ARG
+ * (AIM_C64 plan; a structure mismatch -- the plan is left uncompressed).
+ */
+int aim_plan_compress(aim_plan* plan, int32_t mode);
+/* Host: out[4] = {compressed (0/1), dictionary blocks, dictionary entries,
+ * near entries of the general CSR}. */
+int aim_compress_info(const aim_plan* plan, int64_t* out);
+
 /* ---- array elements and the reduced (macromodel) system (NEXT-2) -------- */
 /*
  * aim_plan_elements -- the array elements as the library enumerates them: the

@@ -41,6 +41,8 @@ SIGNATURES = [
     ("aim_precond_build", I32, [P, I32]),
     ("aim_precond_apply", I32, [P, P, P, P]),
     ("aim_precond_info", I32, [P, P]),
+    ("aim_plan_compress", I32, [P, I32]),
+    ("aim_compress_info", I32, [P, P]),
     ("aim_plan_elements", I32, [P, P, P, ctypes.POINTER(I32)]),
     ("aim_reduced_set", I32, [P, I32, P, P, P, P, P, P, P, I32]),
     ("aim_reduced_matvec", I32, [P, P, P, P]),

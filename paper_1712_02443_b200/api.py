@@ -178,6 +178,17 @@ class AimPlan:
         _check(_lib.load().aim_precond_apply(self._p, _dev_ptr(x, self.N, 1), _dev_ptr(y, self.N, 1), _stream()))
         return y
 
+    # ---- repetition-compressed near field
+    def compress(self, mode: int = 1) -> dict:
+        """aim_plan_compress: 1 = use the repetition-compressed near field, 0 = the general CSR."""
+        _check(_lib.load().aim_plan_compress(self._p, int(mode)))
+        return self.compress_info()
+
+    def compress_info(self) -> dict:
+        out = np.zeros(4, dtype=np.int64)
+        _check(_lib.load().aim_compress_info(self._p, out.ctypes.data))
+        return dict(zip(("on", "blocks", "dict_nnz", "nnz_near"), (int(v) for v in out)))
+
     # ---- array elements and the reduced (macromodel) system
     def elements(self):
         """aim_plan_elements: (element of every RWG [N], translate group of every element)."""

@@ -554,6 +554,27 @@ int aim_precond_info(const aim_plan* p, int64_t* out) {
     return AIM_OK;
 }
 
+int aim_plan_compress(aim_plan* p, int32_t mode) {
+    if (!p || mode < 0 || mode > 1) return fail(AIM_E_ARG, "bad argument");
+    return guarded([&] {
+        if (mode == 0) free_compressed(p);
+        else build_compressed(p, p->stream);
+        for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);   // captured the other near kernel
+        p->graphs.clear();
+        p->mv_warm.clear();
+        return AIM_OK;
+    });
+}
+
+int aim_compress_info(const aim_plan* p, int64_t* out) {
+    if (!p || !out) return fail(AIM_E_ARG, "bad argument");
+    out[0] = p->cmp_on;
+    out[1] = p->cmp_blocks;
+    out[2] = p->cmp_nnz;
+    out[3] = p->nnzN;
+    return AIM_OK;
+}
+
 int aim_plan_elements(aim_plan* p, int32_t* elem_of_rwg, int32_t* group, int32_t* n_elements) {
     if (!p || !n_elements) return fail(AIM_E_ARG, "bad argument");
     return guarded([&] {

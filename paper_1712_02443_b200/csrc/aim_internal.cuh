@@ -262,6 +262,24 @@ struct aim_plan {
     std::vector<int32_t> el_reps_h;   // [groups] representative element of each group
     int32_t* el_rows = nullptr;   // device copies
     int64_t* el_rptr = nullptr;
+    // repetition-compressed near field (aim_plan_compress, k_compress.cu)
+    int cmp_on = 0, cz_contig = 0, cz_max_slots = 0;
+    int64_t cmp_nnz = 0, cmp_blocks = 0;
+    int32_t* cz_el_of = nullptr;  // [N] element of every RWG
+    int32_t* cz_loc = nullptr;    // [N] local row of every RWG in its element
+    int64_t* cz_slot_ptr = nullptr;   // [elements+1] neighbour slots
+    int32_t* cz_slot_f = nullptr;     // [slots] neighbour element
+    int32_t* cz_slot_b = nullptr;     // [slots] dictionary block
+    int64_t* cz_brow = nullptr;   // [blocks] offset of the block's row pointers in cz_rowptr
+    int64_t* cz_rowptr = nullptr; // concatenated block row pointers (absolute into cz_col / cz_val)
+    int32_t* cz_col = nullptr;    // local column of the neighbour element
+    double2* cz_val = nullptr;
+    std::vector<int64_t> cz_brow_h;
+    // single element group: sparse x dense form over the element pairs of each block
+    int cz_spmm = 0, cz_n = 0;
+    int32_t *cz_pe = nullptr, *cz_pf = nullptr, *cz_first = nullptr;   // pairs (e, f); first RWG of e
+    std::vector<std::pair<int64_t, int64_t>> cz_pairs;               // per block: (offset, count) of its pairs
+    double2 *cz_xt = nullptr, *cz_yt = nullptr;                      // [n][elements] transposed x, y
     // block-Jacobi preconditioner (aim_precond_build): one dense inverse per
     // translate group
     int prec_on = 0;
@@ -394,6 +412,10 @@ void zgemm_rm(const double2* A, const double2* B, double2* C, int m, int n, int 
 void build_precond(aim_plan* p, cudaStream_t s);
 void apply_precond(aim_plan* p, const double2* in, double2* out, cudaStream_t s);
 void free_precond(aim_plan* p);
+// ---- repetition-compressed near field (k_compress.cu)
+void build_compressed(aim_plan* p, cudaStream_t s);
+void free_compressed(aim_plan* p);
+void launch_near_cmp(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
 // ---- reduced (macromodel) system (k_reduced.cu)
 void reduced_set(aim_plan* p, int ntypes, const int32_t* nhat, const int32_t* nint, const double2* D,
                  const double2* T, const double2* A, const double2* B, const int32_t* elem_type, int nelem);

@@ -1,0 +1,486 @@
+// Repetition-compressed near field.
+//
+// "In most array problems, many elements are identical.  Therefore, matrices
+// T_m, A_m and B_m only need to be calculated once for each distinct element"
+// (also PAPER.md:77-78).  Applied to the AIM operator: on a
+// grid-commensurate lattice (elements that are translates of one another by
+// integer multiples of h, so their stencils sit identically on the grid), the
+// precorrected near-field block between elements e and f depends only on
+// (group(e), group(f), lattice offset of f from e).  One dictionary block is
+// kept per such key (the entries of its first occurrence in element order);
+// every element lists its neighbour elements with the key of each pair.  The
+// product walks, for row m (element e, local row l), the neighbour slots of e
+// and the dictionary row l of each slot's block, gathering x of the
+// neighbour's RWGs.  C4: 478 M stored entries -> the dictionary of a few
+// blocks (L2-resident); the structure of every occurrence is verified equal
+// to its block's at build time.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "aim_internal.cuh"
+#include "cplx.cuh"
+
+namespace aim {
+
+__global__ void cz_gather_kernel(const double2* __restrict__ src, const int64_t* __restrict__ idx, long long n,
+                                 double2* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+
+// y[m] (+)= sum_slots sum_{entries of block row l} val * x[rwg(f, l')], warp per
+// row (rows walked element-major so a CTA's warps share neighbour blocks in L1)
+template <class C>
+__global__ void __launch_bounds__(256) near_cmp_kernel(const int32_t* __restrict__ el_rows,
+                                                       const int64_t* __restrict__ el_rptr,
+                                                       const int32_t* __restrict__ el_of,
+                                                       const int32_t* __restrict__ loc,
+                                                       const int64_t* __restrict__ slot_ptr,
+                                                       const int32_t* __restrict__ slot_f,
+                                                       const int32_t* __restrict__ slot_b,
+                                                       const int64_t* __restrict__ brow,
+                                                       const int64_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ col, const C* __restrict__ val,
+                                                       int contig, const C* __restrict__ x, long long N, int R,
+                                                       C* __restrict__ y) {
+    const long long q = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (q >= N) return;
+    const int lane = threadIdx.x & 31;
+    const int m = el_rows[q];
+    const int e = el_of[m], l = loc[m];
+    for (int r = 0; r < R; ++r) {
+        C acc = mkc<C>(0, 0);
+        for (long long sl = slot_ptr[e]; sl < slot_ptr[e + 1]; ++sl) {
+            const int f = slot_f[sl];
+            const int64_t* rp = rowptr + brow[slot_b[sl]];
+            const long long e0 = rp[l], e1 = rp[l + 1];
+            const long long fb = el_rptr[f];
+            for (long long b = e0 + lane; b < e1; b += 64) {
+                C z[2], xv[2];
+                int n[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const long long t = b + 32 * u;
+                    const bool v = t < e1;
+                    z[u] = v ? __ldg(&val[t]) : mkc<C>(0, 0);
+                    const int lc = v ? __ldg(&col[t]) : 0;
+                    n[u] = v ? (contig ? (int)(el_rows[fb] + lc) : el_rows[fb + lc]) : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) xv[u] = n[u] >= 0 ? __ldg(&x[(long long)n[u] * R + r]) : mkc<C>(0, 0);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    acc.x = fma(z[u].x, xv[u].x, acc.x); acc.x = fma(-z[u].y, xv[u].y, acc.x);
+                    acc.y = fma(z[u].x, xv[u].y, acc.y); acc.y = fma(z[u].y, xv[u].x, acc.y);
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const C t = shfl_xor2(acc, off);
+            acc.x += t.x; acc.y += t.y;
+        }
+        if (lane == 0) y[(long long)m * R + r] = acc;
+    }
+}
+
+// One right-hand side: warp per row; lanes < (number of slots) first fetch
+// their slot's block row range and the neighbour's first RWG id, then the
+// warp walks the slots with that metadata in registers (shuffles, no
+// dependent loads), lane t taking entries t and t + 32 of each slot's row;
+// four slots are unrolled so their value / column / x loads overlap.
+constexpr int kCzMaxSlots = 32;
+__global__ void __launch_bounds__(256) near_cmp1_kernel(const int32_t* __restrict__ el_rows,
+                                                        const int64_t* __restrict__ el_rptr,
+                                                        const int32_t* __restrict__ el_of,
+                                                        const int32_t* __restrict__ loc,
+                                                        const int64_t* __restrict__ slot_ptr,
+                                                        const int32_t* __restrict__ slot_f,
+                                                        const int32_t* __restrict__ slot_b,
+                                                        const int64_t* __restrict__ brow,
+                                                        const int64_t* __restrict__ rowptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const double2* __restrict__ val,
+                                                        const double2* __restrict__ x, long long N,
+                                                        double2* __restrict__ y) {
+    const long long q = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (q >= N) return;
+    const int lane = threadIdx.x & 31;
+    const int m = el_rows[q];
+    const int e = el_of[m], l = loc[m];
+    const long long s0 = slot_ptr[e];
+    const int ns = (int)(slot_ptr[e + 1] - s0);
+    long long st = 0;
+    int cnt = 0, fb = 0;
+    if (lane < ns) {
+        const int64_t* rp = rowptr + brow[slot_b[s0 + lane]];
+        st = rp[l];
+        cnt = (int)(rp[l + 1] - st);
+        fb = el_rows[el_rptr[slot_f[s0 + lane]]];
+    }
+    double2 acc = make_double2(0, 0);
+    for (int sb = 0; sb < ns; sb += 4) {
+        double2 z[4][2];
+        int n[4][2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int sl = sb + k;
+            const long long st_k = __shfl_sync(0xffffffffu, st, sl & 31);
+            const int cnt_k = sl < ns ? __shfl_sync(0xffffffffu, cnt, sl & 31) : 0;
+            const int fb_k = __shfl_sync(0xffffffffu, fb, sl & 31);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int t = lane + 32 * u;
+                const bool v = t < cnt_k;
+                z[k][u] = v ? __ldg(&val[st_k + t]) : make_double2(0, 0);
+                n[k][u] = v ? fb_k + __ldg(&col[st_k + t]) : -1;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const double2 xv = n[k][u] >= 0 ? __ldg(&x[n[k][u]]) : make_double2(0, 0);
+                acc.x = fma(z[k][u].x, xv.x, acc.x); acc.x = fma(-z[k][u].y, xv.y, acc.x);
+                acc.y = fma(z[k][u].x, xv.y, acc.y); acc.y = fma(z[k][u].y, xv.x, acc.y);
+            }
+        // rows with more than 64 entries in one slot (not in the BASELINE arrays)
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+            const int sl = sb + k;
+            const long long st_k = __shfl_sync(0xffffffffu, st, sl & 31);
+            const int cnt_k = sl < ns ? __shfl_sync(0xffffffffu, cnt, sl & 31) : 0;
+            const int fb_k = __shfl_sync(0xffffffffu, fb, sl & 31);
+            for (int t = 64 + lane; t < cnt_k; t += 32) {
+                const double2 zz = __ldg(&val[st_k + t]);
+                const double2 xv = __ldg(&x[fb_k + __ldg(&col[st_k + t])]);
+                acc.x = fma(zz.x, xv.x, acc.x); acc.x = fma(-zz.y, xv.y, acc.x);
+                acc.y = fma(zz.x, xv.y, acc.y); acc.y = fma(zz.y, xv.x, acc.y);
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) y[m] = acc;
+}
+
+// One element group (every element a lattice translate of the first; C2, C4,
+// C5) and one right-hand side: the near product as a sparse x dense product
+// per dictionary block b,  Yt[l][e_k] += sum_{l'} B[l][l'] Xt[l'][f_k]  over
+// the element pairs (e_k, f_k) that use b, with x and y transposed to
+// [local row][element] so each nonzero of B multiplies a contiguous run of
+// elements (coalesced) instead of one scattered x value per stored entry.
+// Thread (row slot, pair): 64 consecutive pairs per CTA column tile; the
+// 4 row slots of a CTA walk rows l0 .. l0 + 15.
+constexpr int kSpRows = 16;
+__global__ void cz_transpose_kernel(const double2* __restrict__ x, int n, int ne, int first_stride,
+                                    const int32_t* __restrict__ el_first, double2* __restrict__ xt, int to_t) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n * ne) return;
+    const int l = (int)(t / ne), e = (int)(t - (t / ne) * ne);
+    const long long g = (long long)el_first[e] + l;
+    if (to_t) xt[t] = x[g];
+    else ((double2*)x)[g] = xt[t];
+}
+
+__global__ void __launch_bounds__(256) near_spmm_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                        const double2* __restrict__ val,
+                                                        const int32_t* __restrict__ pe,
+                                                        const int32_t* __restrict__ pf, int m, int n, int ne,
+                                                        const double2* __restrict__ xt, double2* __restrict__ yt) {
+    const int k = blockIdx.y * 64 + (threadIdx.x & 63);
+    const int e = k < m ? pe[k] : -1, f = k < m ? pf[k] : 0;
+    for (int r = threadIdx.x >> 6; r < kSpRows; r += 4) {
+        const int l = blockIdx.x * kSpRows + r;
+        if (l >= n) break;
+        const long long t0 = rp[l], t1 = rp[l + 1];
+        double2 acc = make_double2(0, 0);
+        long long t = t0;
+        for (; t + 4 <= t1; t += 4) {
+            double2 v[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                v[u] = __ldg(&val[t + u]);
+                xv[u] = __ldg(&xt[(long long)__ldg(&col[t + u]) * ne + f]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc.x = fma(v[u].x, xv[u].x, acc.x); acc.x = fma(-v[u].y, xv[u].y, acc.x);
+                acc.y = fma(v[u].x, xv[u].y, acc.y); acc.y = fma(v[u].y, xv[u].x, acc.y);
+            }
+        }
+        for (; t < t1; ++t) {
+            const double2 v = __ldg(&val[t]), xv = __ldg(&xt[(long long)__ldg(&col[t]) * ne + f]);
+            acc.x = fma(v.x, xv.x, acc.x); acc.x = fma(-v.y, xv.y, acc.x);
+            acc.y = fma(v.x, xv.y, acc.y); acc.y = fma(v.y, xv.x, acc.y);
+        }
+        if (e >= 0) {
+            double2* o = &yt[(long long)l * ne + e];
+            *o = make_double2(o->x + acc.x, o->y + acc.y);
+        }
+    }
+}
+
+void free_compressed(aim_plan* p) {
+    for (void* q : {(void*)p->cz_el_of, (void*)p->cz_loc, (void*)p->cz_slot_ptr, (void*)p->cz_slot_f,
+                    (void*)p->cz_slot_b, (void*)p->cz_brow, (void*)p->cz_rowptr, (void*)p->cz_col,
+                    (void*)p->cz_val})
+        p->release(q);
+    p->cz_el_of = p->cz_loc = p->cz_slot_f = p->cz_slot_b = p->cz_col = nullptr;
+    p->cz_slot_ptr = p->cz_brow = p->cz_rowptr = nullptr;
+    p->cz_val = nullptr;
+    for (void* q : {(void*)p->cz_pe, (void*)p->cz_pf, (void*)p->cz_first, (void*)p->cz_xt, (void*)p->cz_yt})
+        p->release(q);
+    p->cz_pe = p->cz_pf = p->cz_first = nullptr;
+    p->cz_xt = p->cz_yt = nullptr;
+    p->cz_pairs.clear();
+    p->cmp_on = 0;
+    p->cmp_nnz = p->cmp_blocks = 0;
+}
+
+void build_compressed(aim_plan* p, cudaStream_t s) {
+    if (p->prec != AIM_C128) throw Error(AIM_E_ARG, "compression needs an AIM_C128 plan");
+    free_compressed(p);
+    ensure_elements(p, s);
+    const long long N = p->N;
+    const int ne = p->el_count;
+    const auto& rows = p->el_rows_h;
+    const auto& rptr = p->el_rptr_h;
+    std::vector<int32_t> el_of(N), loc(N), base(3 * N);
+    for (int e = 0; e < ne; ++e)
+        for (int64_t q = rptr[e]; q < rptr[e + 1]; ++q) {
+            el_of[rows[q]] = e;
+            loc[rows[q]] = (int32_t)(q - rptr[e]);
+        }
+    AIM_CUDA(cudaMemcpy(base.data(), p->base, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToHost));
+    // groups: translate groups whose members sit on the grid like their
+    // representative (stencil bases shifted by one integer vector); a member
+    // that does not is its own group
+    std::vector<int32_t> grp(ne), shift(3 * ne, 0);
+    int ng = (int)p->el_reps_h.size();
+    for (int e = 0; e < ne; ++e) {
+        const int d = p->el_group_h[e], r = p->el_reps_h[d];
+        grp[e] = d;
+        bool ok = true;
+        for (int c = 0; c < 3; ++c) shift[3 * e + c] = base[3 * rows[rptr[e]] + c] - base[3 * rows[rptr[r]] + c];
+        for (int64_t l = 0; ok && l < rptr[e + 1] - rptr[e]; ++l)
+            for (int c = 0; c < 3; ++c)
+                if (base[3 * rows[rptr[e] + l] + c] - base[3 * rows[rptr[r] + l] + c] != shift[3 * e + c]) ok = false;
+        if (!ok) {
+            grp[e] = ng++;
+            shift[3 * e] = shift[3 * e + 1] = shift[3 * e + 2] = 0;
+        }
+    }
+    // general near CSR on the host (structure only)
+    std::vector<int64_t> nrow(N + 1);
+    std::vector<int32_t> ncol(p->nnzN);
+    AIM_CUDA(cudaMemcpy(nrow.data(), p->nrow, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost));
+    AIM_CUDA(cudaMemcpy(ncol.data(), p->ncol, sizeof(int32_t) * p->nnzN, cudaMemcpyDeviceToHost));
+    struct Block {
+        int ge, nrows;
+        std::vector<int64_t> rowptr;   // local
+        std::vector<int32_t> col;
+        std::vector<int64_t> src;      // index into the general CSR
+    };
+    std::map<std::tuple<int, int, int, int, int>, int> key_of;
+    std::vector<Block> blocks;
+    std::vector<int64_t> slot_ptr(ne + 1, 0);
+    std::vector<int32_t> slot_f, slot_b;
+    for (int e = 0; e < ne; ++e) {
+        const int ne_rows = (int)(rptr[e + 1] - rptr[e]);
+        std::vector<int> fs, bs;          // this element's slots
+        std::vector<char> filling;        // block first seen here (filled from e's rows)
+        std::vector<int64_t> cursor;      // verification cursor per slot (entries of the block row)
+        for (int l = 0; l < ne_rows; ++l) {
+            const int m = rows[rptr[e] + l];
+            // entries of row m grouped by neighbour element, in column order
+            for (int64_t t = nrow[m]; t < nrow[m + 1]; ++t) {
+                const int n = ncol[t], f = el_of[n];
+                size_t k = 0;
+                while (k < fs.size() && fs[k] != f) ++k;
+                if (k == fs.size()) {
+                    const auto key = std::make_tuple(grp[e], grp[f], shift[3 * f] - shift[3 * e],
+                                                     shift[3 * f + 1] - shift[3 * e + 1],
+                                                     shift[3 * f + 2] - shift[3 * e + 2]);
+                    auto it = key_of.find(key);
+                    int b;
+                    if (it == key_of.end()) {
+                        b = (int)blocks.size();
+                        key_of[key] = b;
+                        Block B;
+                        B.ge = grp[e];
+                        B.nrows = ne_rows;
+                        B.rowptr.assign(ne_rows + 1, -1);
+                        B.rowptr[0] = 0;
+                        blocks.push_back(std::move(B));
+                        filling.push_back(1);
+                    } else {
+                        b = it->second;
+                        filling.push_back(0);
+                        if (blocks[b].rowptr[l] != 0)   // the block has entries in rows this occurrence lacks
+                            throw Error(AIM_E_ARG, "near field not repetition-compressible (element " +
+                                                       std::to_string(e) + ")");
+                    }
+                    fs.push_back(f);
+                    bs.push_back(b);
+                    cursor.push_back(0);
+                }
+                Block& B = blocks[bs[k]];
+                if (filling[k]) {
+                    B.col.push_back(loc[n]);
+                    B.src.push_back(t);
+                } else {
+                    // the occurrence must have its block's structure
+                    const int64_t c = B.rowptr[l] + cursor[k]++;
+                    if (B.rowptr[l] < 0 || c >= B.rowptr[l + 1] || B.col[c] != loc[n])
+                        throw Error(AIM_E_ARG, "near field not repetition-compressible (element " +
+                                                   std::to_string(e) + ", row " + std::to_string(l) + ")");
+                }
+            }
+            // close row l of the blocks being filled; check row lengths of the others
+            for (size_t k = 0; k < fs.size(); ++k) {
+                Block& B = blocks[bs[k]];
+                if (filling[k]) {
+                    B.rowptr[l + 1] = (int64_t)B.col.size();
+                } else {
+                    if (B.rowptr[l] + cursor[k] != B.rowptr[l + 1])
+                        throw Error(AIM_E_ARG, "near field not repetition-compressible (row length)");
+                    cursor[k] = 0;
+                }
+            }
+        }
+        // blocks first seen after row 0 have unset row pointers before their
+        // first row: fill forward (empty rows)
+        for (size_t k = 0; k < fs.size(); ++k)
+            if (filling[k]) {
+                Block& B = blocks[bs[k]];
+                for (int l = 0; l < ne_rows; ++l)
+                    if (B.rowptr[l + 1] < 0) B.rowptr[l + 1] = B.rowptr[l];
+            }
+        for (size_t k = 0; k < fs.size(); ++k) {
+            slot_f.push_back(fs[k]);
+            slot_b.push_back(bs[k]);
+        }
+        slot_ptr[e + 1] = (int64_t)slot_f.size();
+    }
+    // concatenate the dictionary
+    std::vector<int64_t> brow(blocks.size()), rowptr, src;
+    std::vector<int32_t> col;
+    for (size_t b = 0; b < blocks.size(); ++b) {
+        brow[b] = (int64_t)rowptr.size();
+        const int64_t o = (int64_t)col.size();
+        for (int64_t v : blocks[b].rowptr) rowptr.push_back(o + v);
+        col.insert(col.end(), blocks[b].col.begin(), blocks[b].col.end());
+        src.insert(src.end(), blocks[b].src.begin(), blocks[b].src.end());
+    }
+    bool contig = true;
+    for (int e = 0; e < ne && contig; ++e)
+        for (int64_t q = rptr[e]; q < rptr[e + 1]; ++q)
+            if (rows[q] != rows[rptr[e]] + (q - rptr[e])) {
+                contig = false;
+                break;
+            }
+    auto up32 = [&](const std::vector<int32_t>& v) {
+        int32_t* d = p->alloc<int32_t>(std::max<size_t>(1, v.size()));
+        if (!v.empty()) h2d(d, v.data(), sizeof(int32_t) * v.size(), s);
+        return d;
+    };
+    auto up64 = [&](const std::vector<int64_t>& v) {
+        int64_t* d = p->alloc<int64_t>(std::max<size_t>(1, v.size()));
+        if (!v.empty()) h2d(d, v.data(), sizeof(int64_t) * v.size(), s);
+        return d;
+    };
+    p->cz_el_of = up32(el_of);
+    p->cz_loc = up32(loc);
+    p->cz_slot_ptr = up64(slot_ptr);
+    p->cz_slot_f = up32(slot_f);
+    p->cz_slot_b = up32(slot_b);
+    p->cz_brow = up64(brow);
+    p->cz_brow_h = brow;
+    p->cz_rowptr = up64(rowptr);
+    p->cz_col = up32(col);
+    p->cz_val = p->alloc<double2>(std::max<size_t>(1, src.size()));
+    if (!src.empty()) {
+        int64_t* d_src = up64(src);
+        cz_gather_kernel<<<(unsigned)((src.size() + 255) / 256), 256, 0, s>>>(p->nval, d_src, (long long)src.size(),
+                                                                             p->cz_val);
+        note_launch("cz_gather");
+        AIM_CUDA(cudaStreamSynchronize(s));
+        p->release(d_src);
+    }
+    p->cz_contig = contig ? 1 : 0;
+    p->cz_max_slots = 0;
+    for (int e = 0; e < ne; ++e) p->cz_max_slots = std::max<int>(p->cz_max_slots, (int)(slot_ptr[e + 1] - slot_ptr[e]));
+    p->cmp_nnz = (int64_t)col.size();
+    p->cmp_blocks = (int64_t)blocks.size();
+    // single group, contiguous elements: the SpMM form (pairs of every block)
+    p->cz_spmm = 0;
+    if (contig && ng == 1 && getenv("AIM_CZ_SPMM") == nullptr) {
+        std::vector<std::vector<int32_t>> pe(blocks.size()), pf(blocks.size());
+        for (int e = 0; e < ne; ++e)
+            for (int64_t sl = slot_ptr[e]; sl < slot_ptr[e + 1]; ++sl) {
+                pe[slot_b[sl]].push_back(e);
+                pf[slot_b[sl]].push_back(slot_f[sl]);
+            }
+        std::vector<int32_t> ape, apf, first(ne);
+        p->cz_pairs.clear();
+        for (size_t b = 0; b < blocks.size(); ++b) {
+            p->cz_pairs.push_back({(int64_t)ape.size(), (int64_t)pe[b].size()});
+            ape.insert(ape.end(), pe[b].begin(), pe[b].end());
+            apf.insert(apf.end(), pf[b].begin(), pf[b].end());
+        }
+        for (int e = 0; e < ne; ++e) first[e] = rows[rptr[e]];
+        p->cz_pe = up32(ape);
+        p->cz_pf = up32(apf);
+        p->cz_first = up32(first);
+        p->cz_n = (int)(rptr[1] - rptr[0]);
+        p->cz_xt = p->alloc<double2>((size_t)p->cz_n * ne);
+        p->cz_yt = p->alloc<double2>((size_t)p->cz_n * ne);
+        p->cz_spmm = 1;
+    }
+    p->cmp_on = 1;
+}
+
+void launch_near_cmp(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
+    const unsigned grid = (unsigned)((p->N * 32 + 255) / 256);
+    if (R == 1 && p->cz_spmm) {
+        const int n = p->cz_n, ne = p->el_count;
+        const long long tot = (long long)n * ne;
+        const unsigned gt = (unsigned)((tot + 255) / 256);
+        cz_transpose_kernel<<<gt, 256, 0, s>>>((const double2*)x, n, ne, n, p->cz_first, p->cz_xt, 1);
+        note_launch("cz_transpose");
+        AIM_CUDA(cudaMemsetAsync(p->cz_yt, 0, sizeof(double2) * tot, s));
+        for (size_t b = 0; b < p->cz_pairs.size(); ++b) {
+            const int m = (int)p->cz_pairs[b].second;
+            if (!m) continue;
+            // block b's row pointers: brow is on the device; the host copy is kept
+            const dim3 g2((unsigned)((n + kSpRows - 1) / kSpRows), (unsigned)((m + 63) / 64));
+            near_spmm_kernel<<<g2, 256, 0, s>>>(p->cz_rowptr + p->cz_brow_h[b], p->cz_col, p->cz_val,
+                                                p->cz_pe + p->cz_pairs[b].first, p->cz_pf + p->cz_pairs[b].first, m, n,
+                                                ne, p->cz_xt, p->cz_yt);
+            note_launch("near_spmm");
+        }
+        cz_transpose_kernel<<<gt, 256, 0, s>>>((const double2*)y, n, ne, n, p->cz_first, p->cz_yt, 0);
+        note_launch("cz_transpose");
+        return;
+    }
+    if (R == 1 && p->cz_contig && p->cz_max_slots <= kCzMaxSlots) {
+        near_cmp1_kernel<<<grid, 256, 0, s>>>(p->el_rows, p->el_rptr, p->cz_el_of, p->cz_loc, p->cz_slot_ptr,
+                                              p->cz_slot_f, p->cz_slot_b, p->cz_brow, p->cz_rowptr, p->cz_col,
+                                              p->cz_val, (const double2*)x, p->N, (double2*)y);
+        note_launch("near_cmp1");
+        return;
+    }
+    near_cmp_kernel<double2><<<grid, 256, 0, s>>>(p->el_rows, p->el_rptr, p->cz_el_of, p->cz_loc, p->cz_slot_ptr,
+                                                  p->cz_slot_f, p->cz_slot_b, p->cz_brow, p->cz_rowptr, p->cz_col,
+                                                  p->cz_val, p->cz_contig, (const double2*)x, p->N, R, (double2*)y);
+    note_launch("near_cmp");
+}
+
+}  // namespace aim

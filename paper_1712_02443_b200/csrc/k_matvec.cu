@@ -993,6 +993,10 @@ static void launch_near_t(aim_plan* p, const C* x, C* y, int R, cudaStream_t s) 
 }
 
 void launch_near(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
+    if (p->cmp_on) {      // repetition-compressed near field (NEXT-3, k_compress.cu)
+        launch_near_cmp(p, x, y, R, s);
+        return;
+    }
     if (p->prec == AIM_C64) launch_near_t(p, (const float2*)x, (float2*)y, R, s);
     else launch_near_t(p, (const double2*)x, (double2*)y, R, s);
     note_launch("near");

@@ -410,3 +410,43 @@ def test_fused_mode2_convolution_full_size(name, monkeypatch):
     assert rel(fused.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
     assert rel(y1.cpu().numpy(), y3.cpu().numpy()) <= 1e-13
     G.close()
+
+
+@pytest.mark.parametrize("name,nrhs,blocks_max", [("c1", 1, 16), ("c1", 3, 16), ("t_vol", 2, 64),
+                                                  ("t_dissim", 1, 81), ("t_m3", 1, 36)])
+def test_compressed_near_small(name, nrhs, blocks_max):
+    """NEXT-3: the repetition-compressed near field (dictionary blocks per
+    (group, group, lattice offset)) gives the general path's product to 1e-13
+    and the oracle's to 1e-10; switching back restores the general path."""
+    G, O = gpu_plan(name), oracle_plan(name)
+    x = make_vectors(O.N, nrhs, 8)
+    xt = torch.from_numpy(x).cuda()
+    y0 = G.matvec(xt).cpu().numpy()
+    info = G.compress(1)
+    assert info["on"] == 1 and 1 <= info["blocks"] <= blocks_max
+    y1 = G.matvec(xt).cpu().numpy()
+    y1b = G.matvec(xt).cpu().numpy()       # graph replay
+    assert np.array_equal(y1, y1b)
+    assert rel(y1, y0) <= 1e-13
+    assert rel(y1, O.matvec(x)) <= 1e-10
+    G.compress(0)
+    assert np.array_equal(G.matvec(xt).cpu().numpy(), y0)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_compressed_near_full_size(name):
+    """NEXT-3 on the grid-commensurate BASELINE arrays: the dictionary is a
+    small fraction of the near matrix and the product equals the general
+    path's to 1e-11 (entries of translated elements differ by rounding only)."""
+    from paper_1712_02443_b200 import AimPlan
+    cfg = get_config(name)
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    x = torch.from_numpy(make_vectors(G.N, cfg.nrhs, 1)).cuda()
+    if cfg.nrhs == 1:
+        x = x[:, 0].contiguous()
+    y0 = G.matvec(x)
+    info = G.compress(1)
+    assert info["dict_nnz"] * 50 <= info["nnz_near"]
+    y1 = G.matvec(x)
+    assert float((y1 - y0).norm() / y0.norm()) <= 1e-11
+    G.close()

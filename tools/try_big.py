@@ -11,6 +11,7 @@ from workloads import get_config, make_mesh, make_vectors  # noqa: E402
 
 args = sys.argv[1:]
 prec = 1 if "--c64" in args else 0          # AIM_C64 plans (reading D16)
+cmp = "--compress" in args                     # repetition-compressed near field (NEXT-3)
 for name in [a for a in args if not a.startswith("--")]:
     cfg = get_config(name)
     t0 = time.time()
@@ -18,6 +19,10 @@ for name in [a for a in args if not a.startswith("--")]:
     t1 = time.time()
     plan = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, precision=prec)
     inf = plan.info
+    if cmp:
+        t2 = time.time()
+        ci = plan.compress(1)
+        print(name, "compress", ci, "%.2fs" % (time.time() - t2), flush=True)
     x = torch.from_numpy(make_vectors(plan.N, 1, 0)).to(plan.dtype).cuda()
     y = plan.matvec(x)
     torch.cuda.synchronize()
