@@ -114,7 +114,8 @@ def kernel_names(info, R):
         "interp": "interp1_kernel (H5 interpolation)" if R == 1 else "interp_kernel (H5 interpolation)",
         "fft_x": "fft_ct/fft_pp kernel (H2 x forward, zero-pad fused)",
         "fft_yz": {1: "planar4_kernel (y fwd, z Toeplitz x G2, y inv, fused)",
-                   2: "planar_yz2 (y fwd, z Toeplitz x G2, y inv)",
+                   2: "ymode2_kernel (y fwd, z Toeplitz x G2, y inv fused; TMA bulk copies)" if R == 1
+                   else "y passes + ztoeplitz_kernel (mode 2)",
                    0: "fft passes y fwd, z turnaround x G, y inv"}[mode],
         "ifft_x": "fft_ct/fft_pp kernel (H4 x inverse, pruned)",
     }
@@ -262,7 +263,66 @@ def cufft_compare(info, R, ours_conv_ms, reps=10):
     return out
 
 
-def measure_config(name, precision, steps, warmup, local, e2e_steps=0, cufft=False):
+def measure_extras(plan, x, y, steps, warmup, local, gm_iters=50):
+    """On the headline plan (one RHS): GMRES per-iteration cost (D15; CGS2
+    vector passes beside the product), the block-Jacobi preconditioner
+    (NEXT-4: build time, preconditioned iteration cost), the reduced
+    macromodel system product (NEXT-2, seeded synthetic blocks of the paper's
+    shapes, N_m = 4 N^_m) and the repetition-compressed near field (NEXT-3)."""
+    import numpy as np
+    import torch
+    from workloads.macromodel import type_blocks
+    out = {}
+    V = plan.planewave_rhs()
+    plan.gmres(V, restart=50, tol=1e-12, fixed_iters=2)      # workspace (Krylov basis) allocated untimed
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, it, rr, _ = plan.gmres(V, restart=50, tol=1e-12, fixed_iters=gm_iters)
+    t_gm = time.perf_counter() - t0
+    mv_ms = None
+    t, _ = timed_steps(lambda: plan.matvec(x, y), 10, 2, preheat_s=0.0)
+    mv_ms = 1e3 * t / 10
+    gm = {"iters": it, "ms_per_iter": 1e3 * t_gm / it, "matvec_ms": mv_ms,
+          "vector_ms_per_iter": 1e3 * t_gm / it - mv_ms * (1 + 1.0 / 50),
+          "what": f"GMRES(50), {gm_iters} fixed iterations from J0 = 0 on the D14 plane wave (one true-residual "
+                  "product per restart cycle included), host wall clock around aim_gmres"}
+    t0 = time.perf_counter()
+    pc = plan.precond_build(1)
+    pc["build_seconds"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, it, _, _ = plan.gmres(V, restart=50, tol=1e-12, fixed_iters=gm_iters)
+    pc["ms_per_iter"] = 1e3 * (time.perf_counter() - t0) / it
+    plan.precond_build(0)
+    gm["block_jacobi"] = pc
+    out["gmres"] = gm
+    eo, grp = plan.elements()
+    sizes = [int((eo == e).sum()) for e in [list(grp).index(d) for d in range(int(grp.max()) + 1)]]
+    if len(sizes) <= 4:
+        blocks = type_blocks(sizes, ratio=4, seed=11)
+        t0 = time.perf_counter()
+        plan.reduced_set(grp, blocks)
+        t_set = time.perf_counter() - t0
+        del blocks
+        ry = torch.empty_like(x)
+        t, _ = timed_steps(lambda: plan.reduced_matvec(x, ry), 10, 2, preheat_s=0.0)
+        out["reduced"] = {"ms_per_product": 1e3 * t / 10, "products_per_s": 10 / t, "set_seconds": t_set,
+                          "types": len(sizes), "elements": int(grp.size), "nhat": sizes, "nint": [4 * s for s in sizes],
+                          "what": "(D - G T A^-1 B) Y, PAPER.md eq. MV_product1: two per-type block GEMMs (D, "
+                                  "K = T A^-1 B, FP64) around one aim_matvec; seeded synthetic blocks"}
+    t0 = time.perf_counter()
+    ci = plan.compress(1)
+    ci["build_seconds"] = time.perf_counter() - t0
+    t, clk = timed_steps(lambda: plan.matvec(x, y), steps, warmup, clocks_dev=local)
+    ci.update({"value": steps / t, "ms_per_step": 1e3 * t / steps, "clocks": clk,
+               "stage_ms": profile_stages(plan, x, y, max(3, min(steps, 20))),
+               "what": "near field read from the repetition-compressed dictionary (sparse x dense over element "
+                       "pairs); every other stage as the headline"})
+    plan.compress(0)
+    out["compressed"] = ci
+    return out
+
+
+def measure_config(name, precision, steps, warmup, local, e2e_steps=0, cufft=False, extras=False):
     """One plan, one timed loop (profiling off), a profiled pass; returns a dict."""
     import numpy as np
     import torch
@@ -323,8 +383,9 @@ def measure_config(name, precision, steps, warmup, local, e2e_steps=0, cufft=Fal
                                                                  "(copy in, product, copy out, synchronise)"}}
     if cufft:
         conv = sum(stage_ms.get(k, 0.0) for k in ("fft_x", "fft_yz", "ifft_x"))
-        del x, y
         res["cufft"] = cufft_compare(info, R, conv)
+    if extras and R == 1 and precision == 0:
+        res.update(measure_extras(plan, x, y, steps, warmup, local))
     plan.close()
     torch.cuda.empty_cache()
     return res
@@ -595,7 +656,7 @@ def run_ours(args, ws, rank, local):
     cfg = get_config(args.config)
     N1 = ws == 1
     head = measure_config(args.config, 0, args.steps, args.warmup, local, e2e_steps=args.e2e_steps if N1 else 0,
-                          cufft=N1) if N1 else None
+                          cufft=N1, extras=N1 and not args.no_extra) if N1 else None
     if not N1:
         # --replicas: one independent plan per GPU on its own input (weak scaling)
         mesh = make_mesh(cfg)
@@ -626,8 +687,10 @@ def run_ours(args, ws, rank, local):
         line["config"].update({k: head[k] for k in ("grid", "fft", "conv_mode", "nnz_proj", "nnz_near", "nrhs")})
         line["config"]["N"] = head["_info"]["n_rwg"]
         line["roofline"] = roofline_of(head, args.config)
-        for k in ("matvec_roofline", "stage_ms", "stage_alg_gbs", "e2e", "cufft", "plan_seconds", "device_bytes"):
-            line[k] = head[k]
+        for k in ("matvec_roofline", "stage_ms", "stage_alg_gbs", "e2e", "cufft", "plan_seconds", "device_bytes",
+                  "gmres", "reduced", "compressed"):
+            if k in head:
+                line[k] = head[k]
         if not args.no_extra:
             extra = {}
             for name, prec in (("c2", 0), ("c3", 0), ("c5", 0), ("c5", 1)):
