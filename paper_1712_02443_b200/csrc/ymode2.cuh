@@ -173,6 +173,194 @@ __global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ 
     if (threadIdx.x == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------- 2-CTA cluster version
+// The same pass with each plane split over a cluster of two CTAs (two SMs):
+// CTA q holds z columns [q NH, q NH + n_q) of the plane (NH = ceil(Nz/2)),
+// loaded and stored with one TMA bulk copy per row, and runs the y FFTs on
+// them; the z Toeplitz of ky line p needs all Nz values, so the peer's
+// columns are read from its shared memory (DSMEM, ld.shared::cluster), one
+// cluster barrier per round of lines separating the reads from the in-place
+// writes.  Half the shared memory per CTA (C4: 88 KB) -> two CTAs per SM.
+__device__ __forceinline__ unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%clusterid.x;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cl_count() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
+    unsigned a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+    return a;
+}
+__device__ __forceinline__ double2 ld_dsmem(unsigned addr) {
+    double2 v;
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+// radix-R stage over the first nq of NH columns (row stride NH)
+template <int P, int R, int ST, int NH, bool DIF>
+__device__ __forceinline__ void ym2c_stage(double2* tile, const double2* tw, int nq) {
+    constexpr int NB = P / R;
+    constexpr int TWS = P / (R * ST);
+#pragma unroll 1
+    for (int q = threadIdx.x; q < NB * nq; q += blockDim.x) {
+        const int j = q / nq, l = q - (q / nq) * nq;
+        const int m = j % ST;
+        const int base = (j / ST) * R * ST + m;
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = tile[(base + t * ST) * NH + l];
+        if constexpr (DIF) {
+            dft<R>(a, -1.0);
+#pragma unroll
+            for (int k = 1; k < R; ++k) {
+                const int e = (m * k * TWS) % P;
+                if (e) a[k] = cmul(a[k], tw[e]);
+            }
+        } else {
+#pragma unroll
+            for (int t = 1; t < R; ++t) {
+                const int e = (m * t * TWS) % P;
+                if (e) {
+                    const double2 w = tw[e];
+                    a[t] = cmul(a[t], make_double2(w.x, -w.y));
+                }
+            }
+            dft<R>(a, 1.0);
+        }
+#pragma unroll
+        for (int t = 0; t < R; ++t) tile[(base + t * ST) * NH + l] = a[t];
+    }
+}
+
+// z Toeplitz of ky line p for the columns of cluster rank Q (compile-time
+// column ranges, so the line stays in registers): out[j] = sum_z' G2(|z - z'|)
+// in[z'], z = Q NH + j; the peer's columns come from its shared memory.
+template <int NZ, int Q>
+__device__ __forceinline__ void ym2c_toeplitz(const double2* tile, unsigned peer, int p, const double2* g,
+                                              double2* out) {
+    constexpr int NH = (NZ + 1) / 2;
+    constexpr int z0 = Q * NH, nq = Q ? NZ - NH : NH;
+    constexpr int z0p = Q ? 0 : NH, nqp = Q ? NH : NZ - NH;
+    double2 in[NZ];
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) {
+        if (z >= z0 && z < z0 + nq) in[z] = tile[p * NH + z - z0];
+        else if (z >= z0p && z < z0p + nqp) in[z] = ld_dsmem(peer + (unsigned)((p * NH + z - z0p) * 16));
+        else in[z] = make_double2(0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < NH; ++j) out[j] = make_double2(0, 0);
+#pragma unroll
+    for (int d = 0; d < NZ; ++d) {
+        const double2 gd = __ldg(&g[d]);
+#pragma unroll
+        for (int j = 0; j < nq; ++j) {
+            const int z = z0 + j;
+            if (z - d < 0 && (d == 0 || z + d >= NZ)) continue;
+            double2 sum = z - d >= 0 ? in[z - d] : make_double2(0, 0);
+            if (d && z + d < NZ) sum = z - d >= 0 ? cadd(sum, in[z + d]) : in[z + d];
+            out[j].x = fma(gd.x, sum.x, fma(-gd.y, sum.y, out[j].x));
+            out[j].y = fma(gd.x, sum.y, fma(gd.y, sum.x, out[j].y));
+        }
+    }
+}
+
+template <int P, int R1, int R2, int R3, int NZ, int NT>
+__global__ void __launch_bounds__(NT, 2) ymode2c_kernel(double2* __restrict__ W, int Ny, int Px, int PyH,
+                                                        const double2* __restrict__ spec,
+                                                        const double2* __restrict__ twg, int planes) {
+    constexpr int NH = (NZ + 1) / 2, S1 = R2 * R3;
+    extern __shared__ __align__(128) unsigned char ym2c_raw[];
+    double2* tile = reinterpret_cast<double2*>(ym2c_raw);    // [P][NH]
+    double2* tw = tile + P * NH;                             // [P]
+    __shared__ __align__(8) uint64_t mbar;
+    const unsigned q = cl_rank();
+    const int z0 = (int)q * NH, nq = q ? NZ - NH : NH;
+    const int z0p = q ? 0 : NH, nqp = q ? NH : NZ - NH;       // the peer's columns
+    for (int e = threadIdx.x; e < P; e += blockDim.x) tw[e] = twg[e];
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    cl_sync();
+    const unsigned peer = cl_map(tile, q ^ 1u);
+    unsigned phase = 0;
+    for (int pl = (int)cl_id(); pl < planes; pl += (int)cl_count()) {
+        double2* plane = W + (long long)pl * Ny * NZ;
+        const int kx = pl % Px;
+        const int ax = min(kx, Px - kx);
+        // 1. load my columns of rows 0 .. Ny-1 (one bulk copy per row), zero the y padding
+        fence_async_smem();
+        bulk_wait_read();            // my previous bulk stores have read the tile
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_expect_tx(&mbar, (unsigned)(Ny * nq * sizeof(double2)));
+        __syncthreads();
+        for (int row = threadIdx.x; row < Ny; row += NT)
+            bulk_g2s(tile + row * NH, plane + (long long)row * NZ + z0, (unsigned)(nq * sizeof(double2)), &mbar);
+        for (int e = Ny * NH + threadIdx.x; e < P * NH; e += NT) tile[e] = make_double2(0, 0);
+        mbar_wait(&mbar, phase);
+        phase ^= 1;
+        __syncthreads();
+        // 2. forward y FFT on my columns
+        ym2c_stage<P, R1, S1, NH, true>(tile, tw, nq);
+        __syncthreads();
+        ym2c_stage<P, R2, R3, NH, true>(tile, tw, nq);
+        __syncthreads();
+        ym2c_stage<P, R3, 1, NH, true>(tile, tw, nq);
+        __syncthreads();
+        cl_sync();                   // the peer's forward transform is complete
+        // 3. z Toeplitz for my columns, rounds of NT lines
+        const double2* g2 = spec + (long long)ax * PyH * NZ;
+#pragma unroll 1
+        for (int p0 = 0; p0 < P; p0 += NT) {
+            const int p = p0 + threadIdx.x;
+            double2 out[NH];
+            if (p < P) {
+                const int k1 = p / S1, k2 = (p / R3) % R2, k3 = p % R3;
+                const int ky = k1 + R1 * k2 + R1 * R2 * k3;
+                const int ay = min(ky, P - ky);
+                const double2* g = g2 + ay * NZ;
+                if (q == 0) ym2c_toeplitz<NZ, 0>(tile, peer, p, g, out);
+                else ym2c_toeplitz<NZ, 1>(tile, peer, p, g, out);
+            }
+            cl_sync();               // every read of this round's lines (both CTAs) is done
+            if (p < P)
+#pragma unroll
+                for (int j = 0; j < NH; ++j)
+                    if (j < nq) tile[p * NH + j] = out[j];
+        }
+        __syncthreads();
+        // 4. inverse y FFT on my columns
+        ym2c_stage<P, R3, 1, NH, false>(tile, tw, nq);
+        __syncthreads();
+        ym2c_stage<P, R2, R3, NH, false>(tile, tw, nq);
+        __syncthreads();
+        ym2c_stage<P, R1, S1, NH, false>(tile, tw, nq);
+        // 5. store rows 0 .. Ny-1 of my columns
+        fence_async_smem();
+        __syncthreads();
+        for (int row = threadIdx.x; row < Ny; row += NT)
+            bulk_s2g(plane + (long long)row * NZ + z0, tile + row * NH, (unsigned)(nq * sizeof(double2)));
+    }
+    bulk_wait_all();
+    cl_sync();                       // no CTA leaves while its peer may read its shared memory
+}
+
 // Fused mode-2 pass for the compiled plans (Py, Nz) = (784, 14) (C4) and
 // (486, 13) (C3); complex128, one right-hand side.  Returns false if no plan
 // matches (the caller runs the three separate passes).  AIM_YZ_FUSED=0
@@ -186,6 +374,40 @@ bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, con
     AIM_CUDA(cudaGetDevice(&dev));
     const int planes = 4 * Px;
     const int PyH = Py / 2 + 1;
+    // the 2-CTA cluster variant is opt-in: measured slower on C4 (1.19 vs 0.63 ms)
+    // and C3 (0.35 vs 0.21 ms) -- 386 row bulk copies per CTA, DSMEM line reads
+    // and four cluster barriers per plane cost more than the doubled occupancy gains
+    const char* envc = getenv("AIM_YZ_CLUSTER");
+    const bool cluster = envc && envc[0] == '1';
+#define YM2C_CASE(PP, A, B, C, NZ, NT)                                                                        \
+    if (cluster && Py == PP && Nz == NZ) {                                                                    \
+        const size_t smem = sizeof(double2) * (size_t)PP * ((NZ + 1) / 2 + 1);                               \
+        static unsigned long long mask = 0; /* cudaFuncSetAttribute is per device */                         \
+        if (!(mask >> (dev & 63) & 1ULL)) {                                                                   \
+            AIM_CUDA(cudaFuncSetAttribute(ymode2c_kernel<PP, A, B, C, NZ, NT>,                                \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+            mask |= 1ULL << (dev & 63);                                                                       \
+        }                                                                                                     \
+        cudaLaunchConfig_t cfg = {};                                                                          \
+        cfg.gridDim = dim3(2 * 148, 1, 1);                                                                    \
+        cfg.blockDim = dim3(NT, 1, 1);                                                                        \
+        cfg.dynamicSmemBytes = smem;                                                                          \
+        cfg.stream = s;                                                                                       \
+        cudaLaunchAttribute at[1];                                                                            \
+        at[0].id = cudaLaunchAttributeClusterDimension;                                                       \
+        at[0].val.clusterDim.x = 2;                                                                           \
+        at[0].val.clusterDim.y = 1;                                                                           \
+        at[0].val.clusterDim.z = 1;                                                                           \
+        cfg.attrs = at;                                                                                       \
+        cfg.numAttrs = 1;                                                                                     \
+        AIM_CUDA(cudaLaunchKernelEx(&cfg, ymode2c_kernel<PP, A, B, C, NZ, NT>, (double2*)W, Ny, Px, PyH,      \
+                                    (const double2*)spec, (const double2*)ay.tw, planes));                    \
+        note_launch("ymode2c");                                                                               \
+        return true;                                                                                          \
+    }
+    YM2C_CASE(784, 16, 7, 7, 14, 256)
+    YM2C_CASE(486, 9, 9, 6, 13, 256)
+#undef YM2C_CASE
 #define YM2_CASE(PP, A, B, C, NZ, NT, MINB)                                                                   \
     if (Py == PP && Nz == NZ) {                                                                               \
         const size_t smem = sizeof(double2) * (size_t)PP * (NZ + 1);                                          \

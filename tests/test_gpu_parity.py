@@ -450,3 +450,19 @@ def test_compressed_near_full_size(name):
     y1 = G.matvec(x)
     assert float((y1 - y0).norm() / y0.norm()) <= 1e-11
     G.close()
+
+
+def test_fused_mode2_cluster_variant_c3(monkeypatch):
+    """The opt-in 2-CTA cluster variant of the fused mode-2 pass (DSMEM
+    Toeplitz, AIM_YZ_CLUSTER=1; measured slower, kept for the record) equals
+    the default single-CTA kernel to 1e-13 on C3."""
+    from paper_1712_02443_b200 import AimPlan
+    cfg = get_config("c3")
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    x = torch.from_numpy(make_vectors(G.N, 1, 4)[:, 0].copy()).cuda()
+    Q = G.project(x).contiguous()
+    a = G.convolve(Q)
+    monkeypatch.setenv("AIM_YZ_CLUSTER", "1")
+    b = G.convolve(Q)
+    assert rel(b.cpu().numpy(), a.cpu().numpy()) <= 1e-13
+    G.close()
