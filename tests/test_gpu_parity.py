@@ -135,18 +135,37 @@ def test_matvec_c2_full_size_sampled_rows():
     G, O = gpu_plan("c2"), oracle_plan("c2")
     x = make_vectors(O.N, 16, 0)
     y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
-    rows = np.unique(np.concatenate([[0, O.N - 1], np.random.default_rng(0).integers(0, O.N, 48)]))
+    rows = _stratified(O, get_config("c2"), n_random=400, min_rows=500)
+    assert rows.size >= 500
     ref = O.matvec_rows(x, rows)
     assert rel(y[rows], ref) <= 1e-10
+    assert np.abs(y[rows] - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def _stratified(O, cfg, n_random=640, min_rows=1000):
+    """>= 1,000 rows: one RWG per grid x-plane, 32 of each D3 tie class (a
+    centre coordinate exactly on a stencil-placement tie), two on either side
+    of every boundary of an 8-slab partition, the first and last, uniform rows."""
+    from paper_1712_02443_b200 import slab_partition
+    from workloads.sketch import stratified_rows
+    t = O.centres / cfg.h - (cfg.M - 1) / 2.0
+    tie = np.abs(t - np.round(t)) <= 1e-6
+    X, _, _ = slab_partition(make_mesh(cfg), cfg.h, cfg.M, 8)
+    while True:
+        rows = stratified_rows(O.bases, n_random=n_random, seed=3, slab_bounds=X[1:-1], tie_mask=tie)
+        if rows.size >= min_rows:
+            return rows
+        n_random += min_rows - rows.size + 16
 
 
 @pytest.mark.parametrize("name", ["c3", "c5", "c4"])
 def test_matvec_full_size_sampled_rows(name):
     """configs[2], [4], [3] at full size (N = 526,068 / 1,119,744 / 1,843,200;
-    one RHS, the launch configuration of their matvec): 32 sampled rows plus
-    the first and last against the oracle (full projection + its own
-    power-of-two FFT convolution, interpolation and exact near rows for the
-    sampled rows only).  The GPU plan is released before the oracle runs."""
+    one RHS, the launch configuration of their matvec) on >= 1,000 stratified
+    rows (every grid x-plane, tie classes, slab boundaries) against the oracle
+    (full projection + its own radix-2 FFT convolution, interpolation and exact
+    near rows for the sampled rows only): relative L2 <= 1e-10 and every row
+    within 1e-10 of the largest.  The GPU plan is released before the oracle runs."""
     from paper_1712_02443_b200 import AimPlan
     cfg = get_config(name)
     mesh = make_mesh(cfg)
@@ -156,9 +175,11 @@ def test_matvec_full_size_sampled_rows(name):
     G.close()
     from oracle.aim import OraclePlan
     O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    rows = np.unique(np.concatenate([[0, O.N - 1], np.random.default_rng(1).integers(0, O.N, 32)]))
+    rows = _stratified(O, cfg)
+    assert rows.size >= 1000 and np.unique(O.bases[rows, 0]).size == np.unique(O.bases[:, 0]).size
     ref = O.matvec_rows(x, rows, method="fft")
     assert rel(y[rows], ref) <= 1e-10
+    assert np.abs(y[rows] - ref).max() <= 1e-10 * np.abs(ref).max()
 
 
 @pytest.mark.parametrize("name,nrhs", [("c1", 1), ("c1", 16), ("t_vol", 1), ("t_m3", 2), ("t_dissim", 5)])
