@@ -103,7 +103,10 @@ using Ct210 = CtpPlan<AIM_CT210_NL, 42 * AIM_CT210_NL, 210, 7, 6, 5>;   // x pas
 using Ct24 = CtpPlan<32, 192, 24, 6, 4>;          // x passes of C1 (1 RHS): 32 lines
 using Ct243 = CtpPlan<8, 216, 243, 9, 9, 3>;      // every axis of C5
 using Ct486 = CtpPlan<4, 216, 486, 9, 9, 6>;      // x and y passes of C3
-using Ct784 = CtpPlan<2, 224, 784, 16, 7, 7>;     // x and y passes of C4
+#ifndef AIM_CT784_NL
+#define AIM_CT784_NL 4   // 4 lines of 784 per tile (x passes 0.16 -> 0.145 ms on C4)
+#endif
+using Ct784 = CtpPlan<AIM_CT784_NL, 112 * AIM_CT784_NL, 784, 16, 7, 7>;   // x passes of C4
 using Ct210z11 = CtpPlan<11, 240, 210, 7, 6, 5>;  // planar y/z of C2, one RHS per tile
 using Ct24z7 = CtpPlan<7, 64, 24, 6, 4>;          // planar y/z of C1, one RHS per tile
 
@@ -903,7 +906,7 @@ static void launch_fft_pass_t(FftPass p, cudaStream_t s) {
     const char* ce = getenv("AIM_FFT_NOCT");   // A/B timing: skip the compile-time plans
     if (!(ce && ce[0] == '1') &&
         (try_ct_pass<C, Ct210, 2>(p, s) || try_ct_pass<C, Ct24, 2>(p, s) || try_ct_pass<C, Ct243, 2>(p, s) ||
-         try_ct_pass<C, Ct486, 2>(p, s) || try_ct_pass<C, Ct784, 2>(p, s)))
+         try_ct_pass<C, Ct486, 2>(p, s) || try_ct_pass<C, Ct784, (AIM_CT784_NL > 2 ? 1 : 2)>(p, s)))
         return;
     // runtime radices: in place when one butterfly per thread per stage suffices for >= 2 lines
     const int nl_inplace = kFftThreads * p.ax.min_radix / P;

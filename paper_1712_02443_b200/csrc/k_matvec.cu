@@ -328,8 +328,20 @@ __global__ void __launch_bounds__(256) interp1_kernel(const C* __restrict__ Phi,
         for (int k = 0; k < K; ++k) {
             const int u = lane + 32 * k;
             const bool v = u < S && g0[q] >= 0;
-            w01[q][k] = v ? __ldcs(W2 + 2 * u) : mkc<C>(0, 0);
-            w23[q][k] = v ? __ldcs(W2 + 2 * u + 1) : mkc<C>(0, 0);
+            if constexpr (sizeof(C) == 16) {
+                // the four weights of entry u in one 256-bit load (sm_100 LDG.E.256): half
+                // the L1 wavefronts of two 128-bit loads
+                double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                if (v)
+                    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                                 : "=d"(a0), "=d"(a1), "=d"(a2), "=d"(a3)
+                                 : "l"(W2 + 2 * u));
+                w01[q][k] = mkc<C>(a0, a1);
+                w23[q][k] = mkc<C>(a2, a3);
+            } else {
+                w01[q][k] = v ? __ldcs(W2 + 2 * u) : mkc<C>(0, 0);
+                w23[q][k] = v ? __ldcs(W2 + 2 * u + 1) : mkc<C>(0, 0);
+            }
         }
     }
     C f[RW][K][4];
