@@ -92,6 +92,20 @@ def alg_bytes(info, R, es=16):
     return matvec, stages
 
 
+def alg_bytes_compressed(info, ci, R=1, es=16):
+    """Compulsory bytes of the repetition-compressed product (NEXT-3): the
+    vectors, the four grid passes and the spectrum as alg_bytes, the near
+    dictionary (value + column) and the projection templates (4 weights + row)
+    read once, and per RWG its grid node and weight-row index (single RHS)."""
+    N, Ng = info["n_rwg"], info["n_nodes"]
+    Px, Py, Pz = info["fft_dims"]
+    Nz = info["grid_dims"][2]
+    spec = es * (Px // 2 + 1) * (Py // 2 + 1) * (Nz if info["conv_mode"] != 0 else Pz // 2 + 1)
+    grid = 4 * es * Ng * R
+    return (2 * es * N * R + 4 * grid + spec + (es + 4) * ci["dict_nnz"] + (4 * es // 2 + 4) * ci.get("tpl_nnz", 0)
+            + 8 * N)
+
+
 def fp64_peak():
     """FP64 FMA peak derived from the unit counts and clock (148 SMs x 64 FP64
     lanes x 2 flop x 1.965 GHz; tools/fp64_peak.cu measures 34.2 TFLOP/s)."""
@@ -313,10 +327,15 @@ def measure_extras(plan, x, y, steps, warmup, local, gm_iters=50):
     ci = plan.compress(1)
     ci["build_seconds"] = time.perf_counter() - t0
     t, clk = timed_steps(lambda: plan.matvec(x, y), steps, warmup, clocks_dev=local)
+    b = alg_bytes_compressed(plan.info, ci)
+    peak, peak_src = load_peaks()
     ci.update({"value": steps / t, "ms_per_step": 1e3 * t / steps, "clocks": clk,
                "stage_ms": profile_stages(plan, x, y, max(3, min(steps, 20))),
-               "what": "near field read from the repetition-compressed dictionary (sparse x dense over element "
-                       "pairs); every other stage as the headline"})
+               "matvec_roofline": {"bound": "hbm", "alg_bytes": b, "achieved": b / (t / steps) / 1e9, "peak": peak,
+                                   "unit": "GB/s", "frac": b / (t / steps) / 1e9 / peak, "peak_source": peak_src},
+               "what": "repetition-compressed operators: near field from the dictionary (sparse x dense over "
+                       "element pairs), projection through the group templates, interpolation with the "
+                       "representative's weight rows; the FFT convolution as the headline"})
     plan.compress(0)
     out["compressed"] = ci
     return out

@@ -205,7 +205,7 @@ int aim_precond_apply(aim_plan* plan, const void* x, void* y, void* stream);
  * bytes of the inverses}. */
 int aim_precond_info(const aim_plan* plan, int64_t* out);
 
-/* ---- repetition-compressed near field (NEXT-3) ------------------------- */
+/* ---- repetition-compressed operators (NEXT-3) -------------------------- */
 /*
  * aim_plan_compress -- mode 1: build and use a repetition-compressed copy of
  * the precorrected near field ("matrices ... only need to be calculated once
@@ -217,12 +217,21 @@ int aim_precond_info(const aim_plan* plan, int64_t* out);
  * occurrence's structure is verified equal to its block's; the values are
  * those of the key's first occurrence (other occurrences differ by rounding
  * only).  aim_matvec then reads the dictionary instead of the near CSR.
- * mode 0: back to the general near CSR.  Synchronous.  Errors: AIM_E_ARG
+ * The same translation fixes the projection weights (D2 weights depend only
+ * on positions relative to the stencil base): when the representatives'
+ * (local row, stencil node) pairs number at most half the projection CSR,
+ * single-RHS products project through one node-sorted template per group
+ * (over the box of the representative's stencil nodes, summed over the
+ * elements whose box holds the node, in ascending element order) and
+ * interpolate with the representative's weight row; products with nrhs > 1
+ * keep the general projection/interpolation tables.
+ * mode 0: back to the general tables.  Synchronous.  Errors: AIM_E_ARG
  * (AIM_C64 plan; a structure mismatch -- the plan is left uncompressed).
  */
 int aim_plan_compress(aim_plan* plan, int32_t mode);
-/* Host: out[4] = {compressed (0/1), dictionary blocks, dictionary entries,
- * near entries of the general CSR}. */
+/* Host: out[6] = {compressed (0/1), dictionary blocks, dictionary entries,
+ * near entries of the general CSR, projection/interpolation compressed (0/1),
+ * projection template entries}. */
 int aim_compress_info(const aim_plan* plan, int64_t* out);
 
 /* ---- array elements and the reduced (macromodel) system (NEXT-2) -------- */

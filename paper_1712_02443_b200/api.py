@@ -180,14 +180,15 @@ class AimPlan:
 
     # ---- repetition-compressed near field
     def compress(self, mode: int = 1) -> dict:
-        """aim_plan_compress: 1 = use the repetition-compressed near field, 0 = the general CSR."""
+        """aim_plan_compress: 1 = use the repetition-compressed near field (and, where it pays,
+        projection/interpolation templates), 0 = the general tables."""
         _check(_lib.load().aim_plan_compress(self._p, int(mode)))
         return self.compress_info()
 
     def compress_info(self) -> dict:
-        out = np.zeros(4, dtype=np.int64)
+        out = np.zeros(6, dtype=np.int64)
         _check(_lib.load().aim_compress_info(self._p, out.ctypes.data))
-        return dict(zip(("on", "blocks", "dict_nnz", "nnz_near"), (int(v) for v in out)))
+        return dict(zip(("on", "blocks", "dict_nnz", "nnz_near", "pi_on", "tpl_nnz"), (int(v) for v in out)))
 
     # ---- array elements and the reduced (macromodel) system
     def elements(self):

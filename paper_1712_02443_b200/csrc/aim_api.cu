@@ -572,6 +572,8 @@ int aim_compress_info(const aim_plan* p, int64_t* out) {
     out[1] = p->cmp_blocks;
     out[2] = p->cmp_nnz;
     out[3] = p->nnzN;
+    out[4] = p->cp_on;
+    out[5] = p->cp_tpl_nnz;
     return AIM_OK;
 }
 

@@ -280,6 +280,21 @@ struct aim_plan {
     int32_t *cz_pe = nullptr, *cz_pf = nullptr, *cz_first = nullptr;   // pairs (e, f); first RWG of e
     std::vector<std::pair<int64_t, int64_t>> cz_pairs;               // per block: (offset, count) of its pairs
     double2 *cz_xt = nullptr, *cz_yt = nullptr;                      // [n][elements] transposed x, y
+    // repetition-compressed projection / interpolation (single RHS): one
+    // node-sorted template per group over the box of its representative's
+    // stencil nodes, and per grid-node chunk (one CTA) the elements whose box
+    // meets it; the interpolation reads the representative's weight row
+    int cp_on = 0, cp_G = 8;
+    int64_t cp_tpl_nnz = 0, cp_chunks = 0;
+    int64_t* cp_cptr = nullptr;   // [chunks+1]
+    int32_t* cp_cel = nullptr;    // elements meeting each chunk (ascending)
+    int4* cp_ebox = nullptr;      // [elements] box corner (grid-relative) and group
+    int4* cp_gdim = nullptr;      // [groups] box dims and offset of the group's template row pointers
+    int32_t* cp_tptr = nullptr;   // concatenated template row pointers (absolute)
+    int32_t* cp_tl = nullptr;     // template entry: local row of the element
+    double* cp_tw = nullptr;      // template entry: [4] weights (x, y, z, phi)
+    int32_t* cp_xfirst = nullptr; // [elements] first RWG (contiguous elements) or el_rptr
+    int32_t* cp_wrow = nullptr;   // [N] RWG whose weight row the interpolation reads
     // block-Jacobi preconditioner (aim_precond_build): one dense inverse per
     // translate group
     int prec_on = 0;
@@ -416,6 +431,7 @@ void free_precond(aim_plan* p);
 void build_compressed(aim_plan* p, cudaStream_t s);
 void free_compressed(aim_plan* p);
 void launch_near_cmp(aim_plan* p, const void* x, void* y, int R, cudaStream_t s);
+void launch_project_cmp(const aim_plan* p, const void* x, void* Q, cudaStream_t s);   // cp_on, R = 1
 // ---- reduced (macromodel) system (k_reduced.cu)
 void reduced_set(aim_plan* p, int ntypes, const int32_t* nhat, const int32_t* nint, const double2* D,
                  const double2* T, const double2* A, const double2* B, const int32_t* elem_type, int nelem);

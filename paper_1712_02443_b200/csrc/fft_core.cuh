@@ -36,16 +36,17 @@ __device__ __forceinline__ constexpr double os(int m) {
 
 // Twiddles of the composite in-register radices: c_rtw[rtw_off(R) + j] =
 // exp(-2 pi i j / R) (filled once per device by init_radix_twiddles()).
-constexpr int kRtwTotal = 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16;
+constexpr int kRtwTotal = 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 28;
 __host__ __device__ constexpr int rtw_off(int R) {
-    return R == 6 ? 0 : R == 8 ? 6 : R == 9 ? 14 : R == 10 ? 23 : R == 12 ? 33 : R == 14 ? 45 : R == 15 ? 59 : 74;
+    return R == 6 ? 0 : R == 8 ? 6 : R == 9 ? 14 : R == 10 ? 23 : R == 12 ? 33 : R == 14 ? 45 : R == 15 ? 59
+         : R == 16 ? 74 : 90;
 }
 __constant__ double2 c_rtw[kRtwTotal];
 
 // composite R = A * B, A the first (prime-power) factor
 template <int R>
 struct Split {
-    static constexpr int A = R == 16 ? 4 : R == 12 ? 4 : R == 8 ? 2 : (R % 2 == 0) ? 2 : 3;
+    static constexpr int A = R == 16 ? 4 : R == 12 ? 4 : R == 28 ? 4 : R == 8 ? 2 : (R % 2 == 0) ? 2 : 3;
     static constexpr int B = R / A;
 };
 

@@ -227,6 +227,249 @@ __global__ void __launch_bounds__(256) near_spmm_kernel(const int64_t* __restric
     }
 }
 
+// ------------------------------------------------ projection / interpolation
+// The weights of RWG m depend only on the positions of its quadrature points
+// relative to its stencil base (D2, D3), so a translate of an element by an
+// integer multiple of h has the weights of its group representative, with the
+// stencils shifted by the translation.  Projection from the group templates:
+//   Q^c[g] = sum_{e : g in box(e)} sum_{t in T_d(e)[g - b_e]} w^c_t x[rwg(e, l_t)]
+// (elements in ascending order, template entries in their fixed order);
+// T_d lists, per node p of the representative's stencil box, the pairs
+// (local row l, stencil node u) with base(l) - b + off(u) = p and their four
+// weights.  One CTA per chunk of 256/G consecutive grid nodes walks the
+// chunk's element list; G lanes per node stride over the template row.
+template <int G>
+__global__ void __launch_bounds__(256) project_cmp_kernel(
+    const int64_t* __restrict__ cptr, const int32_t* __restrict__ cel, const int4* __restrict__ ebox,
+    const int4* __restrict__ gdim, const int32_t* __restrict__ tptr, const int32_t* __restrict__ tl,
+    const double* __restrict__ tw, const int32_t* __restrict__ xfirst, const int32_t* __restrict__ el_rows,
+    int contig, const double2* __restrict__ x, int Ny, int Nz, long long Ng, double2* __restrict__ Q) {
+    const long long g = (long long)blockIdx.x * (256 / G) + threadIdx.x / G;
+    const int sub = threadIdx.x % G;
+    const bool live = g < Ng;
+    const int iz = (int)(g % Nz);
+    const long long gy = g / Nz;
+    const int iy = (int)(gy % Ny), ix = (int)(gy / Ny);
+    double2 a[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[c] = make_double2(0, 0);
+    const long long c1 = cptr[blockIdx.x + 1];
+    for (long long c = cptr[blockIdx.x]; c < c1; ++c) {
+        const int e = cel[c];
+        const int4 eb = ebox[e];
+        const int4 gd = gdim[eb.w];
+        const int px = ix - eb.x, py = iy - eb.y, pz = iz - eb.z;
+        if (!live || px < 0 || py < 0 || pz < 0 || px >= gd.x || py >= gd.y || pz >= gd.z) continue;
+        const int pl = (px * gd.y + py) * gd.z + pz;
+        const int t0 = tptr[gd.w + pl], t1 = tptr[gd.w + pl + 1];
+        const int xb = xfirst[e];
+#pragma unroll 4
+        for (int t = t0 + sub; t < t1; t += G) {
+            const int l = __ldg(&tl[t]);
+            double w0, w1, w2, w3;
+            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                : "=d"(w0), "=d"(w1), "=d"(w2), "=d"(w3)
+                : "l"(tw + 4 * (long long)t));
+            const double2 xv = __ldg(&x[contig ? xb + l : __ldg(&el_rows[xb + l])]);
+            a[0].x = fma(w0, xv.x, a[0].x); a[0].y = fma(w0, xv.y, a[0].y);
+            a[1].x = fma(w1, xv.x, a[1].x); a[1].y = fma(w1, xv.y, a[1].y);
+            a[2].x = fma(w2, xv.x, a[2].x); a[2].y = fma(w2, xv.y, a[2].y);
+            a[3].x = fma(w3, xv.x, a[3].x); a[3].y = fma(w3, xv.y, a[3].y);
+        }
+    }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double2 t = shfl_xor2(a[c], off);
+            a[c].x += t.x; a[c].y += t.y;
+        }
+    if (live && sub == 0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) __stcs(&Q[(long long)c * Ng + g], a[c]);
+}
+
+// rows of a row-major table (width in double2) gathered into a compact copy
+__global__ void cz_gather_rows_kernel(const double2* __restrict__ src, const int32_t* __restrict__ rows, int nrows,
+                                      int width, double2* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)nrows * width) return;
+    const int r = (int)(i / width), k = (int)(i - (long long)r * width);
+    dst[i] = src[(long long)rows[r] * width + k];
+}
+
+void launch_project_cmp(const aim_plan* p, const void* x, void* Q, cudaStream_t s) {
+    const unsigned grid = (unsigned)p->cp_chunks;
+#define PC(GG)                                                                                                   \
+    project_cmp_kernel<GG><<<grid, 256, 0, s>>>(p->cp_cptr, p->cp_cel, p->cp_ebox, p->cp_gdim, p->cp_tptr,     \
+                                                p->cp_tl, p->cp_tw, p->cp_xfirst, p->el_rows, p->cz_contig,    \
+                                                (const double2*)x, p->dims[1], p->dims[2], p->Ng, (double2*)Q)
+    switch (p->cp_G) {
+        case 32: PC(32); break;
+        case 16: PC(16); break;
+        case 8: PC(8); break;
+        default: PC(4); break;
+    }
+#undef PC
+    note_launch("project_cmp");
+}
+
+static void free_compressed_pi(aim_plan* p) {
+    for (void* q : {(void*)p->cp_cptr, (void*)p->cp_cel, (void*)p->cp_ebox, (void*)p->cp_gdim, (void*)p->cp_tptr,
+                    (void*)p->cp_tl, (void*)p->cp_tw, (void*)p->cp_xfirst, (void*)p->cp_wrow})
+        p->release(q);
+    p->cp_cptr = nullptr;
+    p->cp_cel = p->cp_tptr = p->cp_tl = p->cp_xfirst = p->cp_wrow = nullptr;
+    p->cp_ebox = p->cp_gdim = nullptr;
+    p->cp_tw = nullptr;
+    p->cp_on = 0;
+    p->cp_tpl_nnz = p->cp_chunks = 0;
+}
+
+// Templates, chunk lists and the interpolation's weight-row map for the
+// groups of build_compressed (grp: group of every element, rep: its
+// representative).  Skipped (cp_on = 0) unless the templates are at most
+// half the projection CSR (AIM_CMP_PI=0 / 1 in the environment: never / always).
+static void build_compressed_pi(aim_plan* p, const std::vector<int32_t>& grp, const std::vector<int32_t>& rep,
+                                const std::vector<int32_t>& base, cudaStream_t s) {
+    free_compressed_pi(p);
+    const char* env = getenv("AIM_CMP_PI");   // 0: never, 1: whenever compressible (tests)
+    if (env && env[0] == '0') return;
+    const bool force = env && env[0] == '1';
+    const int ne = p->el_count, ng = (int)rep.size();
+    const auto& rows = p->el_rows_h;
+    const auto& rptr = p->el_rptr_h;
+    const int M1 = p->M + 1, S = p->S;
+    int64_t tpl = 0;
+    for (int d = 0; d < ng; ++d) tpl += (rptr[rep[d] + 1] - rptr[rep[d]]) * (int64_t)S;
+    if ((!force && tpl * 2 > p->nnzP) || tpl >= (1LL << 31)) return;
+    const int* o = p->origin;
+    // element boxes: corner = smallest stencil base (grid-relative), group dims
+    std::vector<int4> ebox(ne), gdim(ng);
+    for (int e = 0; e < ne; ++e) {
+        int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+        for (int64_t q = rptr[e]; q < rptr[e + 1]; ++q)
+            for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], base[3 * rows[q] + c] - o[c]);
+        ebox[e] = make_int4(lo[0], lo[1], lo[2], grp[e]);
+    }
+    std::vector<int32_t> tptr, tl, wrow(p->N), reprows;
+    std::vector<int64_t> tsrc;   // template entry -> (row of reprows) * S + u
+    int64_t nrep = 0;
+    for (int d = 0; d < ng; ++d) {
+        const int r = rep[d];
+        const int nr = (int)(rptr[r + 1] - rptr[r]);
+        int hi[3] = {0, 0, 0};
+        for (int l = 0; l < nr; ++l)
+            for (int c = 0; c < 3; ++c) {
+                const int b = base[3 * rows[rptr[r] + l] + c] - o[c] - (&ebox[r].x)[c];
+                hi[c] = std::max(hi[c], b + M1);
+            }
+        const int B = hi[0] * hi[1] * hi[2];
+        gdim[d] = make_int4(hi[0], hi[1], hi[2], (int)tptr.size());
+        // counting sort of the representative's (l, u) pairs by box node
+        std::vector<int32_t> cnt(B + 1, 0), node((size_t)nr * S);
+        for (int l = 0; l < nr; ++l) {
+            const int m = rows[rptr[r] + l];
+            const int bx = base[3 * m] - o[0] - ebox[r].x, by = base[3 * m + 1] - o[1] - ebox[r].y,
+                      bz = base[3 * m + 2] - o[2] - ebox[r].z;
+            for (int u = 0; u < S; ++u) {
+                const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
+                const int pl = ((bx + ui) * hi[1] + (by + uj)) * hi[2] + bz + uk;
+                node[(size_t)l * S + u] = pl;
+                cnt[pl + 1]++;
+            }
+        }
+        for (int q = 0; q < B; ++q) cnt[q + 1] += cnt[q];
+        const int32_t t0 = (int32_t)tl.size();
+        for (int q = 0; q <= B; ++q) tptr.push_back(t0 + cnt[q]);
+        tl.resize(t0 + (size_t)nr * S);
+        tsrc.resize(t0 + (size_t)nr * S);
+        for (int l = 0; l < nr; ++l)
+            for (int u = 0; u < S; ++u) {
+                const int t = t0 + cnt[node[(size_t)l * S + u]]++;
+                tl[t] = l;
+                tsrc[t] = (nrep + l) * S + u;
+            }
+        for (int l = 0; l < nr; ++l) reprows.push_back(rows[rptr[r] + l]);
+        nrep += nr;
+    }
+    // every element's stencils are its representative's shifted by its box corner
+    for (int e = 0; e < ne; ++e) {
+        const int r = rep[grp[e]];
+        for (int64_t l = 0; l < rptr[e + 1] - rptr[e]; ++l) {
+            const int m = rows[rptr[e] + l], mr = rows[rptr[r] + l];
+            for (int c = 0; c < 3; ++c)
+                if (base[3 * m + c] - (&ebox[e].x)[c] != base[3 * mr + c] - (&ebox[r].x)[c])
+                    throw Error(AIM_E_ARG, "projection not repetition-compressible (element " + std::to_string(e) + ")");
+            wrow[m] = mr;
+        }
+    }
+    // chunks of 256/G consecutive grid nodes and the elements whose box meets them
+    const double per = p->Ng ? (double)p->nnzP / (double)p->Ng : 1.0;
+    const double pl = per / 8;
+    const int G = pl > 24 ? 32 : pl > 12 ? 16 : pl > 6 ? 8 : 4;
+    const int npc = 256 / G;
+    const int64_t nch = (p->Ng + npc - 1) / npc;
+    std::vector<std::vector<int32_t>> lists(nch);
+    const int Ny = p->dims[1], Nz = p->dims[2];
+    for (int e = 0; e < ne; ++e) {
+        const int4 b = ebox[e], d = gdim[grp[e]];
+        for (int ix = b.x; ix < b.x + d.x; ++ix)
+            for (int iy = b.y; iy < b.y + d.y; ++iy) {
+                const int64_t g0 = ((int64_t)ix * Ny + iy) * Nz + b.z, g1 = g0 + d.z - 1;
+                for (int64_t c = g0 / npc; c <= g1 / npc; ++c)
+                    if (lists[c].empty() || lists[c].back() != e) lists[c].push_back(e);
+            }
+    }
+    std::vector<int64_t> cptr(nch + 1, 0);
+    std::vector<int32_t> cel;
+    for (int64_t c = 0; c < nch; ++c) {
+        cel.insert(cel.end(), lists[c].begin(), lists[c].end());
+        cptr[c + 1] = (int64_t)cel.size();
+    }
+    std::vector<int32_t> xfirst(ne);
+    for (int e = 0; e < ne; ++e) xfirst[e] = p->cz_contig ? rows[rptr[e]] : (int32_t)rptr[e];
+    auto up32 = [&](const std::vector<int32_t>& v) {
+        int32_t* dp = p->alloc<int32_t>(std::max<size_t>(1, v.size()));
+        if (!v.empty()) h2d(dp, v.data(), sizeof(int32_t) * v.size(), s);
+        return dp;
+    };
+    p->cp_cptr = p->alloc<int64_t>(nch + 1);
+    h2d(p->cp_cptr, cptr.data(), sizeof(int64_t) * (nch + 1), s);
+    p->cp_cel = up32(cel);
+    p->cp_ebox = p->alloc<int4>(ne);
+    h2d(p->cp_ebox, ebox.data(), sizeof(int4) * ne, s);
+    p->cp_gdim = p->alloc<int4>(ng);
+    h2d(p->cp_gdim, gdim.data(), sizeof(int4) * ng, s);
+    p->cp_tptr = up32(tptr);
+    p->cp_tl = up32(tl);
+    p->cp_xfirst = up32(xfirst);
+    p->cp_wrow = up32(wrow);
+    // template weights: the representatives' weight rows gathered, then placed
+    // in template order on the host
+    {
+        int32_t* d_rows = up32(reprows);
+        double2* d_w = p->alloc<double2>((size_t)nrep * S * 2);
+        const long long tot = nrep * (long long)S * 2;
+        cz_gather_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const double2*)p->W, d_rows, (int)nrep,
+                                                                           2 * S, d_w);
+        note_launch("cz_gather_rows");
+        std::vector<double> wr((size_t)nrep * S * 4), tw(tl.size() * 4);
+        AIM_CUDA(cudaMemcpyAsync(wr.data(), d_w, sizeof(double) * wr.size(), cudaMemcpyDeviceToHost, s));
+        AIM_CUDA(cudaStreamSynchronize(s));
+        p->release(d_rows);
+        p->release(d_w);
+        for (size_t t = 0; t < tl.size(); ++t)
+            for (int c = 0; c < 4; ++c) tw[4 * t + c] = wr[4 * tsrc[t] + c];
+        p->cp_tw = p->alloc<double>(std::max<size_t>(4, tw.size()));
+        if (!tw.empty()) h2d(p->cp_tw, tw.data(), sizeof(double) * tw.size(), s);
+    }
+    p->cp_G = G;
+    p->cp_chunks = nch;
+    p->cp_tpl_nnz = (int64_t)tl.size();
+    p->cp_on = 1;
+}
+
 void free_compressed(aim_plan* p) {
     for (void* q : {(void*)p->cz_el_of, (void*)p->cz_loc, (void*)p->cz_slot_ptr, (void*)p->cz_slot_f,
                     (void*)p->cz_slot_b, (void*)p->cz_brow, (void*)p->cz_rowptr, (void*)p->cz_col,
@@ -240,6 +483,7 @@ void free_compressed(aim_plan* p) {
     p->cz_pe = p->cz_pf = p->cz_first = nullptr;
     p->cz_xt = p->cz_yt = nullptr;
     p->cz_pairs.clear();
+    free_compressed_pi(p);
     p->cmp_on = 0;
     p->cmp_nnz = p->cmp_blocks = 0;
 }
@@ -444,6 +688,10 @@ void build_compressed(aim_plan* p, cudaStream_t s) {
         p->cz_yt = p->alloc<double2>((size_t)p->cz_n * ne);
         p->cz_spmm = 1;
     }
+    std::vector<int32_t> rep(ng, -1);
+    for (int e = 0; e < ne; ++e)
+        if (rep[grp[e]] < 0) rep[grp[e]] = e;
+    build_compressed_pi(p, grp, rep, base, s);
     p->cmp_on = 1;
 }
 

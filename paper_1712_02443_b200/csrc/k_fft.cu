@@ -776,7 +776,7 @@ void init_radix_twiddles() {
     AIM_CUDA(cudaGetDevice(&dev));
     if (dev < 64 && done[dev]) return;
     std::vector<double2> h(kRtwTotal);
-    for (int R : {6, 8, 9, 10, 12, 14, 15, 16})
+    for (int R : {6, 8, 9, 10, 12, 14, 15, 16, 28})
         for (int j = 0; j < R; ++j) {
             long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)j / (long double)R;
             h[rtw_off(R) + j] = make_double2((double)cosl(a), (double)sinl(a));

@@ -248,11 +248,17 @@ __global__ void gm_reduce_kernel(const double2* __restrict__ partial, int nb, in
 }
 
 // dst = src / sqrt(nrm2->x)   (nrm2 on the device)
+// dst = src / sqrt(nrm2), and the same into dst2 when given (the fixed
+// product input of the unpreconditioned solve)
 __global__ void gm_scale_kernel(const double2* __restrict__ src, long long n, const double2* __restrict__ nrm2,
-                                double2* __restrict__ dst) {
+                                double2* __restrict__ dst, double2* __restrict__ dst2) {
     const double s = 1.0 / sqrt(nrm2->x);
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) dst[e] = make_double2(src[e].x * s, src[e].y * s);
+    if (e < n) {
+        const double2 v = make_double2(src[e].x * s, src[e].y * s);
+        dst[e] = v;
+        if (dst2) dst2[e] = v;
+    }
 }
 
 // out (+)= sum_i y[i] V_i
@@ -346,8 +352,8 @@ struct Vec {
     void norm2(const double2* w, double2* out) {
         dots(w, 1, w, out);
     }
-    void scale(const double2* src, const double2* nrm2, double2* dst) {
-        gm_scale_kernel<<<nb(), 256, 0, s>>>(src, n, nrm2, dst);
+    void scale(const double2* src, const double2* nrm2, double2* dst, double2* dst2 = nullptr) {
+        gm_scale_kernel<<<nb(), 256, 0, s>>>(src, n, nrm2, dst, dst2);
         note_launch("gmres_scale");
     }
     void combine(const double2* V, int nv, const double2* y, double2* out, bool acc) {
@@ -382,14 +388,14 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
     const long long n = ops.n;
     cudaStream_t s = p->stream;
     const bool pre = (bool)ops.precond;
-    if (p->gm_restart < restart || p->gm_n != n || (pre && !p->gm_z)) {
+    if (p->gm_restart < restart || p->gm_n != n || !p->gm_z) {
         p->release(p->gm_V);
         p->release(p->gm_w);
         p->release(p->gm_z);
         p->release(p->gm_part);
         p->gm_V = p->alloc<double2>((size_t)(restart + 1) * std::max(1LL, n));
         p->gm_w = p->alloc<double2>(std::max(1LL, n));
-        p->gm_z = pre ? p->alloc<double2>(std::max(1LL, n)) : nullptr;
+        p->gm_z = p->alloc<double2>(std::max(1LL, n));
         p->gm_part = p->alloc<double2>((size_t)kGmBlocks * kGmChunk + 3 * (kMaxBasis + 1));
         p->gm_restart = restart;
         p->gm_n = n;
@@ -424,8 +430,12 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
         return AIM_OK;
     }
     // r0 = b (x0 = 0)
+    // Unpreconditioned products read v_j from z, a copy written with it, so the
+    // product's CUDA graph (keyed on its input and output pointers) is captured
+    // once per solve instead of once per basis vector.
+    double2* zin = pre ? nullptr : z;
     double beta = bnorm;
-    g.scale(b, dmisc, V);
+    g.scale(b, dmisc, V, zin);
     int total = 0;
     double rel = 1.0;
     std::vector<cplx> H((size_t)(restart + 1) * restart), gv(restart + 1), sn(restart);
@@ -443,13 +453,13 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
                 ops.precond(vj, z, s);
                 ops.matvec(z, w, s);
             } else {
-                ops.matvec(vj, w, s);
+                ops.matvec(z, w, s);   // z == v_j
             }
             const int nv = j + 1;
             g.dots(V, nv, w, dh1);                 // pass 1
             g.axpy_dots(V, nv, dh1, w, dh2);       // pass 2
             g.axpy(V, nv, dh2, w, dmisc);          // pass 3 (+ ||w||^2)
-            g.scale(w, dmisc, V + (size_t)(j + 1) * n);
+            g.scale(w, dmisc, V + (size_t)(j + 1) * n, zin);
             fetch(dh1, nv, hbuf);
             fetch(dh2, nv, hbuf + (kMaxBasis + 1));
             fetch(dmisc, 1, hbuf + 2 * (kMaxBasis + 1));
@@ -523,7 +533,7 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
         if (!std::isfinite(beta)) throw Error(AIM_E_BREAKDOWN, "GMRES: non-finite residual");
         rel = beta / bnorm;
         if (stop || (fixed_iters <= 0 && rel <= tol) || beta == 0.0) break;
-        g.scale(V, dmisc, V);
+        g.scale(V, dmisc, V, zin);
     }
     sync();
     if (iters_out) *iters_out = total;

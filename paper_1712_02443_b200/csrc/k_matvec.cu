@@ -216,6 +216,10 @@ static void launch_project_t(const aim_plan* p, const C* x, C* Q, int R, cudaStr
 }
 
 void launch_project(const aim_plan* p, const void* x, void* Q, int R, cudaStream_t s) {
+    if (p->cp_on && R == 1) {   // repetition-compressed templates (NEXT-3, k_compress.cu)
+        launch_project_cmp(p, x, Q, s);
+        return;
+    }
     if (p->prec == AIM_C64) launch_project_t(p, (const float2*)x, (float2*)Q, R, s);
     else launch_project_t(p, (const double2*)x, (double2*)Q, R, s);
     note_launch("project");
@@ -310,7 +314,7 @@ template <int M, int RW, class C>
 __global__ void __launch_bounds__(256) interp1_kernel(const C* __restrict__ Phi, const Real<C>* __restrict__ W,
                                                       const int32_t* __restrict__ node0, long long Ng, int Ny, int Nz,
                                                       long long N, double keta, double ik2, int accumulate,
-                                                      C* __restrict__ y) {
+                                                      const int32_t* __restrict__ wrow, C* __restrict__ y) {
     // RW rows per warp: every row's weights and node index are requested
     // before any row's potential gathers, which are all in flight together
     constexpr int M1 = M + 1, S = M1 * M1 * M1, K = (S + 31) / 32;
@@ -323,7 +327,9 @@ __global__ void __launch_bounds__(256) interp1_kernel(const C* __restrict__ Phi,
     C w01[RW][K], w23[RW][K];
 #pragma unroll
     for (int q = 0; q < RW; ++q) {
-        const C* W2 = reinterpret_cast<const C*>(W) + 2 * (m0 + q) * S;
+        // wrow (repetition-compressed plans): the group representative's weight row
+        const long long wr = wrow && g0[q] >= 0 ? (long long)__ldg(&wrow[m0 + q]) : m0 + q;
+        const C* W2 = reinterpret_cast<const C*>(W) + 2 * wr * S;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int u = lane + 32 * k;
@@ -909,8 +915,9 @@ static void launch_interp_t(aim_plan* p, const C* Phi, C* y, int R, bool accumul
 #endif
         constexpr int RW = AIM_INTERP1_RW;   // rows per warp
         const unsigned grid1 = nblk((p->N + RW - 1) / RW * 32, 256);
+        const int32_t* wrow = p->cp_on ? p->cp_wrow : nullptr;
         switch (p->M) {
-#define I1(MM) case MM: interp1_kernel<MM, RW, C><<<grid1, 256, 0, s>>>(Phi, W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, keta, ik2, accumulate ? 1 : 0, y); break;
+#define I1(MM) case MM: interp1_kernel<MM, RW, C><<<grid1, 256, 0, s>>>(Phi, W, p->node0, p->Ng, p->dims[1], p->dims[2], p->N, keta, ik2, accumulate ? 1 : 0, wrow, y); break;
             I1(1) I1(2) I1(3) I1(4)
 #undef I1
         }

@@ -56,6 +56,7 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 //   DIT (inverse): a_t *= conj(w_{R ST}^{m t}), b = DFT_R(a) (sign +)
 template <int P, int R, int ST, int NZ, bool DIF>
 __device__ __forceinline__ void ym2_stage(double2* tile, const double2* tw) {
+    if constexpr (R == 1) return;        // two-stage plans (R3 = 1)
     constexpr int NB = P / R;            // butterflies per column
     constexpr int TWS = P / (R * ST);    // twiddle exponent scale
 #pragma unroll 1
@@ -122,6 +123,11 @@ __global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ 
         for (int e = Ny * NZ + threadIdx.x; e < P * NZ; e += blockDim.x) tile[e] = make_double2(0, 0);
         mbar_wait(&mbar, phase);
         phase ^= 1;
+        // the next plane of this CTA into L2 while this one is transformed
+        if (threadIdx.x == 0 && q + gridDim.x < planes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(W + (long long)(q + gridDim.x) * Ny * NZ),
+                         "r"(bytes)
+                         : "memory");
         __syncthreads();
         // 2. forward y FFT (DIF), digit-reversed output
         ym2_stage<P, R1, S1, NZ, true>(tile, tw);
@@ -422,6 +428,12 @@ bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, con
         note_launch("ymode2");                                                                                \
         return true;                                                                                          \
     }
+    // C4: 784 = 28 x 28 in two in-place stages (one 28-point butterfly per
+    // thread and column per stage, 392 threads) unless AIM_YM2_PLAN=3 selects
+    // the three-stage 16 x 7 x 7 plan
+    const char* envp = getenv("AIM_YM2_PLAN");
+    const bool three = envp && envp[0] == '3';
+    if (!three) YM2_CASE(784, 28, 28, 1, 14, 392, 1)
     YM2_CASE(784, 16, 7, 7, 14, 448, 1)
     YM2_CASE(486, 9, 9, 6, 13, 256, 2)
 #undef YM2_CASE

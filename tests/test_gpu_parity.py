@@ -171,15 +171,24 @@ def test_matvec_full_size_sampled_rows(name):
     mesh = make_mesh(cfg)
     x = make_vectors(mesh.n_rwg, 1, 0)
     G = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    xt = torch.from_numpy(x).cuda()
+    y = G.matvec(xt).cpu().numpy()
+    ys = [y]
+    if name in ("c4", "c5"):
+        # the repetition-compressed operators (NEXT-3: near dictionary,
+        # projection templates, representative weight rows) on the same rows
+        info = G.compress(1)
+        assert info["on"] == 1 and info["pi_on"] == 1 and info["tpl_nnz"] * 100 <= G.info["nnz_proj"]
+        ys.append(G.matvec(xt).cpu().numpy())
     G.close()
     from oracle.aim import OraclePlan
     O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
     rows = _stratified(O, cfg)
     assert rows.size >= 1000 and np.unique(O.bases[rows, 0]).size == np.unique(O.bases[:, 0]).size
     ref = O.matvec_rows(x, rows, method="fft")
-    assert rel(y[rows], ref) <= 1e-10
-    assert np.abs(y[rows] - ref).max() <= 1e-10 * np.abs(ref).max()
+    for yy in ys:
+        assert rel(yy[rows], ref) <= 1e-10
+        assert np.abs(yy[rows] - ref).max() <= 1e-10 * np.abs(ref).max()
 
 
 @pytest.mark.parametrize("name,nrhs", [("c1", 1), ("c1", 16), ("t_vol", 1), ("t_m3", 2), ("t_dissim", 5)])
@@ -452,6 +461,52 @@ def test_compressed_near_small(name, nrhs, blocks_max):
     assert rel(y1, O.matvec(x)) <= 1e-10
     G.compress(0)
     assert np.array_equal(G.matvec(xt).cpu().numpy(), y0)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_compressed_projection_interpolation_small(name, monkeypatch):
+    """NEXT-3 for the projection/interpolation weights (forced with
+    AIM_CMP_PI=1): the single-RHS projection through the group templates equals
+    the general CSR gather to 1e-13, the product equals the general path's to
+    1e-13 and the oracle's to 1e-10; multi-RHS products keep the general
+    tables; compress(0) restores the general product bit for bit."""
+    from paper_1712_02443_b200 import AimPlan
+    monkeypatch.setenv("AIM_CMP_PI", "1")
+    cfg = get_config(name)
+    G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    O = oracle_plan(name)
+    x = make_vectors(O.N, 2, 9)
+    x1 = torch.from_numpy(x[:, 0].copy()).cuda()
+    x2 = torch.from_numpy(x).cuda()
+    Q0 = G.project(x1).cpu().numpy()
+    y0 = G.matvec(x1).cpu().numpy()
+    y20 = G.matvec(x2).cpu().numpy()
+    info = G.compress(1)
+    assert info["on"] == 1 and info["pi_on"] == 1 and info["tpl_nnz"] >= 1
+    assert rel(G.project(x1).cpu().numpy(), Q0) <= 1e-13
+    y1 = G.matvec(x1).cpu().numpy()
+    assert np.array_equal(y1, G.matvec(x1).cpu().numpy())      # graph replay, deterministic
+    assert rel(y1, y0) <= 1e-13
+    assert rel(y1, O.matvec(x[:, 0])) <= 1e-10
+    assert rel(G.matvec(x2).cpu().numpy(), y20) <= 1e-13
+    G.compress(0)
+    assert np.array_equal(G.matvec(x1).cpu().numpy(), y0)
+    G.close()
+
+
+def test_compressed_pi_threshold():
+    """Without the override the templates are used only where they pay: on
+    for C1 (one group of four translates), off for the dissimilar grid."""
+    from paper_1712_02443_b200 import AimPlan
+    out = {}
+    for name in ("c1", "t_dissim"):
+        cfg = get_config(name)
+        G = AimPlan.from_mesh(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+        out[name] = G.compress(1)
+        out[name]["nnz_proj"] = G.info["nnz_proj"]
+        G.close()
+    assert out["c1"]["pi_on"] == 1 and out["c1"]["tpl_nnz"] * 4 == out["c1"]["nnz_proj"]
+    assert out["t_dissim"]["pi_on"] == 0
 
 
 @pytest.mark.parametrize("name", ["c2", "c4", "c5"])
