@@ -249,6 +249,7 @@ void destroy_plan(aim_plan* p) {
     if (p->ev_x) cudaEventDestroy(p->ev_x);
     if (p->ev_n) cudaEventDestroy(p->ev_n);
     if (p->gm_host) cudaFreeHost(p->gm_host);
+    if (p->gm_ev) cudaEventDestroy(p->gm_ev);
     if (p->hp_in) cudaStreamDestroy(p->hp_in);
     if (p->hp_out) cudaStreamDestroy(p->hp_out);
     for (int k = 0; k < 2; ++k) {

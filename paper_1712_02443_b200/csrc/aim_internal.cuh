@@ -252,6 +252,7 @@ struct aim_plan {
     double2* gm_z = nullptr;      // [n] preconditioned vector (right preconditioning)
     double2* gm_part = nullptr;   // block partials + device coefficients
     double2* gm_host = nullptr;   // pinned host mirror of the coefficients
+    cudaEvent_t gm_ev = nullptr;  // coefficients of the current iteration fetched
     std::vector<double> gm_hist;  // residual estimate |g_{j+1}|/||b|| of the last solve
     // array elements = connected surfaces of the mesh (built on first use by
     // ensure_elements): ordered by smallest RWG id, RWGs ascending within
@@ -284,7 +285,7 @@ struct aim_plan {
     // node-sorted template per group over the box of its representative's
     // stencil nodes, and per grid-node chunk (one CTA) the elements whose box
     // meets it; the interpolation reads the representative's weight row
-    int cp_on = 0, cp_G = 8;
+    int cp_on = 0;
     int64_t cp_tpl_nnz = 0, cp_chunks = 0;
     int64_t* cp_cptr = nullptr;   // [chunks+1]
     int32_t* cp_cel = nullptr;    // elements meeting each chunk (ascending)
@@ -295,6 +296,18 @@ struct aim_plan {
     double* cp_tw = nullptr;      // template entry: [4] weights (x, y, z, phi)
     int32_t* cp_xfirst = nullptr; // [elements] first RWG (contiguous elements) or el_rptr
     int32_t* cp_wrow = nullptr;   // [N] RWG whose weight row the interpolation reads
+    // element-batched projection: per group its elements, x transposed
+    // Xt_d [n][ne_d] and the per-element box contributions Qt_d [nodes][ne_d][4]
+    struct CpGroup {
+        int ne, n, nodes, toff, eoff;
+        int64_t xoff, qoff;
+    };
+    std::vector<CpGroup> cp_groups;
+    int32_t* cp_gel = nullptr;      // group element lists, concatenated
+    int64_t* cp_qbase = nullptr;    // [elements] offset of the element's Qt column (complex units)
+    int32_t* cp_qstride = nullptr;  // [elements] stride between box nodes (4 ne_d)
+    double2* cp_xt = nullptr;
+    double2* cp_qt = nullptr;
     // block-Jacobi preconditioner (aim_precond_build): one dense inverse per
     // translate group
     int prec_on = 0;

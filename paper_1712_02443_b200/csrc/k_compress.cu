@@ -176,9 +176,11 @@ __global__ void __launch_bounds__(256) near_cmp1_kernel(const int32_t* __restric
 // the element pairs (e_k, f_k) that use b, with x and y transposed to
 // [local row][element] so each nonzero of B multiplies a contiguous run of
 // elements (coalesced) instead of one scattered x value per stored entry.
-// Thread (row slot, pair): 64 consecutive pairs per CTA column tile; the
-// 4 row slots of a CTA walk rows l0 .. l0 + 15.
+// Thread (row slot, pair): 64 consecutive pairs per CTA column tile, the 4
+// row slots of a CTA walk 16 rows.  (64 rows x 8 pairs per CTA, for L1 reuse
+// of the Xt lines across rows, measured slower on C4: 1.06 vs 0.90 ms.)
 constexpr int kSpRows = 16;
+constexpr int kSpPairs = 64;
 __global__ void cz_transpose_kernel(const double2* __restrict__ x, int n, int ne, int first_stride,
                                     const int32_t* __restrict__ el_first, double2* __restrict__ xt, int to_t) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -194,9 +196,9 @@ __global__ void __launch_bounds__(256) near_spmm_kernel(const int64_t* __restric
                                                         const int32_t* __restrict__ pe,
                                                         const int32_t* __restrict__ pf, int m, int n, int ne,
                                                         const double2* __restrict__ xt, double2* __restrict__ yt) {
-    const int k = blockIdx.y * 64 + (threadIdx.x & 63);
+    const int k = blockIdx.y * kSpPairs + (threadIdx.x % kSpPairs);
     const int e = k < m ? pe[k] : -1, f = k < m ? pf[k] : 0;
-    for (int r = threadIdx.x >> 6; r < kSpRows; r += 4) {
+    for (int r = threadIdx.x / kSpPairs; r < kSpRows; r += 256 / kSpPairs) {
         const int l = blockIdx.x * kSpRows + r;
         if (l >= n) break;
         const long long t0 = rp[l], t1 = rp[l + 1];
@@ -231,21 +233,65 @@ __global__ void __launch_bounds__(256) near_spmm_kernel(const int64_t* __restric
 // The weights of RWG m depend only on the positions of its quadrature points
 // relative to its stencil base (D2, D3), so a translate of an element by an
 // integer multiple of h has the weights of its group representative, with the
-// stencils shifted by the translation.  Projection from the group templates:
-//   Q^c[g] = sum_{e : g in box(e)} sum_{t in T_d(e)[g - b_e]} w^c_t x[rwg(e, l_t)]
-// (elements in ascending order, template entries in their fixed order);
-// T_d lists, per node p of the representative's stencil box, the pairs
-// (local row l, stencil node u) with base(l) - b + off(u) = p and their four
-// weights.  One CTA per chunk of 256/G consecutive grid nodes walks the
-// chunk's element list; G lanes per node stride over the template row.
-template <int G>
-__global__ void __launch_bounds__(256) project_cmp_kernel(
+// stencils shifted by the translation.  Group d's template T_d lists, per node
+// p of the representative's stencil box, the pairs (local row l, stencil
+// node u) with base(l) - b + off(u) = p and their four weights.  Projection:
+//   1. Xt_d[l][k] = x[rwg(E_d[k], l)]         (x of the group's elements, transposed)
+//   2. Qt_d[p][k][c] = sum_{t in T_d[p]} w^c_t Xt_d[l_t][k]
+//      -- sparse (template) x dense (elements) product: a warp takes one box
+//      node and 32 elements, the template entries are warp-uniform loads and
+//      the Xt rows coalesced, so the template is read once per 64 elements;
+//   3. Q^c[g] = sum_{e : g in box(e)} Qt[g - b_e][e][c], elements ascending
+//      (fixed order: deterministic), one thread per grid node, the elements
+//      whose box meets the CTA's 256 nodes listed per chunk.
+__global__ void cp_xt_kernel(const double2* __restrict__ x, const int32_t* __restrict__ gel, int ne_d, int n_d,
+                             const int32_t* __restrict__ xfirst, const int32_t* __restrict__ el_rows, int contig,
+                             double2* __restrict__ xt) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)n_d * ne_d) return;
+    const int l = (int)(t / ne_d), k = (int)(t - (long long)l * ne_d);
+    const int e = gel[k];
+    xt[t] = __ldg(&x[contig ? xfirst[e] + l : __ldg(&el_rows[xfirst[e] + l])]);
+}
+
+constexpr int kCpK = 64;    // elements per CTA column
+constexpr int kCpP = 4;     // box nodes per CTA
+__global__ void __launch_bounds__(256) cp_spmm_kernel(const int32_t* __restrict__ tptr, const int32_t* __restrict__ tl,
+                                                      const double* __restrict__ tw, int nodes, int ne_d,
+                                                      const double2* __restrict__ xt, double2* __restrict__ qt) {
+    const int p = blockIdx.y * kCpP + (threadIdx.x / kCpK);
+    const int k = blockIdx.x * kCpK + (threadIdx.x % kCpK);
+    if (p >= nodes) return;
+    const bool live = k < ne_d;
+    const int t0 = tptr[p], t1 = tptr[p + 1];
+    double2 a[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[c] = make_double2(0, 0);
+#pragma unroll 4
+    for (int t = t0; t < t1; ++t) {
+        const int l = __ldg(&tl[t]);
+        double w0, w1, w2, w3;
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+            : "=d"(w0), "=d"(w1), "=d"(w2), "=d"(w3)
+            : "l"(tw + 4 * (long long)t));
+        const double2 xv = live ? __ldg(&xt[(long long)l * ne_d + k]) : make_double2(0, 0);
+        a[0].x = fma(w0, xv.x, a[0].x); a[0].y = fma(w0, xv.y, a[0].y);
+        a[1].x = fma(w1, xv.x, a[1].x); a[1].y = fma(w1, xv.y, a[1].y);
+        a[2].x = fma(w2, xv.x, a[2].x); a[2].y = fma(w2, xv.y, a[2].y);
+        a[3].x = fma(w3, xv.x, a[3].x); a[3].y = fma(w3, xv.y, a[3].y);
+    }
+    if (live) {
+        double2* o = qt + ((long long)p * ne_d + k) * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = a[c];
+    }
+}
+
+__global__ void __launch_bounds__(256) cp_gather_sum_kernel(
     const int64_t* __restrict__ cptr, const int32_t* __restrict__ cel, const int4* __restrict__ ebox,
-    const int4* __restrict__ gdim, const int32_t* __restrict__ tptr, const int32_t* __restrict__ tl,
-    const double* __restrict__ tw, const int32_t* __restrict__ xfirst, const int32_t* __restrict__ el_rows,
-    int contig, const double2* __restrict__ x, int Ny, int Nz, long long Ng, double2* __restrict__ Q) {
-    const long long g = (long long)blockIdx.x * (256 / G) + threadIdx.x / G;
-    const int sub = threadIdx.x % G;
+    const int4* __restrict__ gdim, const int64_t* __restrict__ qbase, const int32_t* __restrict__ qstride,
+    const double2* __restrict__ qt, int Ny, int Nz, long long Ng, double2* __restrict__ Q) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = g < Ng;
     const int iz = (int)(g % Nz);
     const long long gy = g / Nz;
@@ -260,33 +306,18 @@ __global__ void __launch_bounds__(256) project_cmp_kernel(
         const int4 gd = gdim[eb.w];
         const int px = ix - eb.x, py = iy - eb.y, pz = iz - eb.z;
         if (!live || px < 0 || py < 0 || pz < 0 || px >= gd.x || py >= gd.y || pz >= gd.z) continue;
-        const int pl = (px * gd.y + py) * gd.z + pz;
-        const int t0 = tptr[gd.w + pl], t1 = tptr[gd.w + pl + 1];
-        const int xb = xfirst[e];
-#pragma unroll 4
-        for (int t = t0 + sub; t < t1; t += G) {
-            const int l = __ldg(&tl[t]);
-            double w0, w1, w2, w3;
-            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
-                : "=d"(w0), "=d"(w1), "=d"(w2), "=d"(w3)
-                : "l"(tw + 4 * (long long)t));
-            const double2 xv = __ldg(&x[contig ? xb + l : __ldg(&el_rows[xb + l])]);
-            a[0].x = fma(w0, xv.x, a[0].x); a[0].y = fma(w0, xv.y, a[0].y);
-            a[1].x = fma(w1, xv.x, a[1].x); a[1].y = fma(w1, xv.y, a[1].y);
-            a[2].x = fma(w2, xv.x, a[2].x); a[2].y = fma(w2, xv.y, a[2].y);
-            a[3].x = fma(w3, xv.x, a[3].x); a[3].y = fma(w3, xv.y, a[3].y);
+        const long long pl = (px * gd.y + py) * gd.z + pz;
+        const double2* q = qt + qbase[e] + pl * qstride[e];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const double2 v = __ldcs(&q[cc]);
+            a[cc].x += v.x;
+            a[cc].y += v.y;
         }
     }
+    if (live)
 #pragma unroll
-    for (int off = 1; off < G; off <<= 1)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const double2 t = shfl_xor2(a[c], off);
-            a[c].x += t.x; a[c].y += t.y;
-        }
-    if (live && sub == 0)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) __stcs(&Q[(long long)c * Ng + g], a[c]);
+        for (int cc = 0; cc < 4; ++cc) __stcs(&Q[(long long)cc * Ng + g], a[cc]);
 }
 
 // rows of a row-major table (width in double2) gathered into a compact copy
@@ -299,27 +330,32 @@ __global__ void cz_gather_rows_kernel(const double2* __restrict__ src, const int
 }
 
 void launch_project_cmp(const aim_plan* p, const void* x, void* Q, cudaStream_t s) {
-    const unsigned grid = (unsigned)p->cp_chunks;
-#define PC(GG)                                                                                                   \
-    project_cmp_kernel<GG><<<grid, 256, 0, s>>>(p->cp_cptr, p->cp_cel, p->cp_ebox, p->cp_gdim, p->cp_tptr,     \
-                                                p->cp_tl, p->cp_tw, p->cp_xfirst, p->el_rows, p->cz_contig,    \
-                                                (const double2*)x, p->dims[1], p->dims[2], p->Ng, (double2*)Q)
-    switch (p->cp_G) {
-        case 32: PC(32); break;
-        case 16: PC(16); break;
-        case 8: PC(8); break;
-        default: PC(4); break;
+    for (const auto& G : p->cp_groups) {
+        const long long tot = (long long)G.n * G.ne;
+        cp_xt_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const double2*)x, p->cp_gel + G.eoff, G.ne, G.n,
+                                                                   p->cp_xfirst, p->el_rows, p->cz_contig,
+                                                                   p->cp_xt + G.xoff);
+        note_launch("cp_xt");
+        const dim3 g2((unsigned)((G.ne + kCpK - 1) / kCpK), (unsigned)((G.nodes + kCpP - 1) / kCpP));
+        cp_spmm_kernel<<<g2, 256, 0, s>>>(p->cp_tptr + G.toff, p->cp_tl, p->cp_tw, G.nodes, G.ne, p->cp_xt + G.xoff,
+                                          p->cp_qt + G.qoff);
+        note_launch("cp_spmm");
     }
-#undef PC
-    note_launch("project_cmp");
+    cp_gather_sum_kernel<<<(unsigned)p->cp_chunks, 256, 0, s>>>(p->cp_cptr, p->cp_cel, p->cp_ebox, p->cp_gdim,
+                                                                p->cp_qbase, p->cp_qstride, p->cp_qt, p->dims[1],
+                                                                p->dims[2], p->Ng, (double2*)Q);
+    note_launch("cp_gather_sum");
 }
 
 static void free_compressed_pi(aim_plan* p) {
     for (void* q : {(void*)p->cp_cptr, (void*)p->cp_cel, (void*)p->cp_ebox, (void*)p->cp_gdim, (void*)p->cp_tptr,
-                    (void*)p->cp_tl, (void*)p->cp_tw, (void*)p->cp_xfirst, (void*)p->cp_wrow})
+                    (void*)p->cp_tl, (void*)p->cp_tw, (void*)p->cp_xfirst, (void*)p->cp_wrow, (void*)p->cp_gel,
+                    (void*)p->cp_qbase, (void*)p->cp_qstride, (void*)p->cp_xt, (void*)p->cp_qt})
         p->release(q);
-    p->cp_cptr = nullptr;
-    p->cp_cel = p->cp_tptr = p->cp_tl = p->cp_xfirst = p->cp_wrow = nullptr;
+    p->cp_cptr = p->cp_qbase = nullptr;
+    p->cp_cel = p->cp_tptr = p->cp_tl = p->cp_xfirst = p->cp_wrow = p->cp_gel = p->cp_qstride = nullptr;
+    p->cp_xt = p->cp_qt = nullptr;
+    p->cp_groups.clear();
     p->cp_ebox = p->cp_gdim = nullptr;
     p->cp_tw = nullptr;
     p->cp_on = 0;
@@ -405,10 +441,7 @@ static void build_compressed_pi(aim_plan* p, const std::vector<int32_t>& grp, co
         }
     }
     // chunks of 256/G consecutive grid nodes and the elements whose box meets them
-    const double per = p->Ng ? (double)p->nnzP / (double)p->Ng : 1.0;
-    const double pl = per / 8;
-    const int G = pl > 24 ? 32 : pl > 12 ? 16 : pl > 6 ? 8 : 4;
-    const int npc = 256 / G;
+    const int npc = 256;
     const int64_t nch = (p->Ng + npc - 1) / npc;
     std::vector<std::vector<int32_t>> lists(nch);
     const int Ny = p->dims[1], Nz = p->dims[2];
@@ -464,7 +497,40 @@ static void build_compressed_pi(aim_plan* p, const std::vector<int32_t>& grp, co
         p->cp_tw = p->alloc<double>(std::max<size_t>(4, tw.size()));
         if (!tw.empty()) h2d(p->cp_tw, tw.data(), sizeof(double) * tw.size(), s);
     }
-    p->cp_G = G;
+    // per group: its elements (ascending), the offsets of its Xt and Qt blocks;
+    // per element: where its Qt column starts and the stride between box nodes
+    {
+        std::vector<std::vector<int32_t>> E(ng);
+        for (int e = 0; e < ne; ++e) E[grp[e]].push_back(e);
+        std::vector<int32_t> gel, qstride(ne);
+        std::vector<int64_t> qbase(ne);
+        int64_t xoff = 0, qoff = 0;
+        p->cp_groups.clear();
+        for (int d = 0; d < ng; ++d) {
+            aim_plan::CpGroup G;
+            G.ne = (int)E[d].size();
+            G.n = (int)(rptr[rep[d] + 1] - rptr[rep[d]]);
+            G.nodes = gdim[d].x * gdim[d].y * gdim[d].z;
+            G.toff = gdim[d].w;
+            G.eoff = (int)gel.size();
+            G.xoff = xoff;
+            G.qoff = qoff;
+            for (int k = 0; k < G.ne; ++k) {
+                qbase[E[d][k]] = qoff + 4LL * k;
+                qstride[E[d][k]] = 4 * G.ne;
+            }
+            gel.insert(gel.end(), E[d].begin(), E[d].end());
+            xoff += (int64_t)G.n * G.ne;
+            qoff += 4LL * G.nodes * G.ne;
+            p->cp_groups.push_back(G);
+        }
+        p->cp_gel = up32(gel);
+        p->cp_qstride = up32(qstride);
+        p->cp_qbase = p->alloc<int64_t>(ne);
+        h2d(p->cp_qbase, qbase.data(), sizeof(int64_t) * ne, s);
+        p->cp_xt = p->alloc<double2>(std::max<int64_t>(1, xoff));
+        p->cp_qt = p->alloc<double2>(std::max<int64_t>(1, qoff));
+    }
     p->cp_chunks = nch;
     p->cp_tpl_nnz = (int64_t)tl.size();
     p->cp_on = 1;
@@ -708,7 +774,7 @@ void launch_near_cmp(aim_plan* p, const void* x, void* y, int R, cudaStream_t s)
             const int m = (int)p->cz_pairs[b].second;
             if (!m) continue;
             // block b's row pointers: brow is on the device; the host copy is kept
-            const dim3 g2((unsigned)((n + kSpRows - 1) / kSpRows), (unsigned)((m + 63) / 64));
+            const dim3 g2((unsigned)((n + kSpRows - 1) / kSpRows), (unsigned)((m + kSpPairs - 1) / kSpPairs));
             near_spmm_kernel<<<g2, 256, 0, s>>>(p->cz_rowptr + p->cz_brow_h[b], p->cz_col, p->cz_val,
                                                 p->cz_pe + p->cz_pairs[b].first, p->cz_pf + p->cz_pairs[b].first, m, n,
                                                 ne, p->cz_xt, p->cz_yt);

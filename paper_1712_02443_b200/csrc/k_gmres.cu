@@ -30,6 +30,9 @@ namespace aim {
 using cplx = std::complex<double>;
 
 static constexpr int kGmBlocks = 296;   // 2 x 148 SMs
+static constexpr int kAdBlocks = 296;   // axpy_dot_smem_kernel: 2 x 148 SMs (3 measured slower)
+static constexpr int kAnBlocks = 2368;  // axpy_norm_kernel: up to 16 x 148 blocks of 256 threads
+static constexpr int kPartBlocks = kAnBlocks;   // rows of the block-partials buffer
 static constexpr int kGmThreads = 512;  // 16 warps
 static constexpr int kGmWarps = kGmThreads / 32;
 static constexpr int kGmChunk = 64;     // basis vectors per pass
@@ -189,19 +192,19 @@ __global__ void __launch_bounds__(kAdThreads, 2) axpy_dot_smem_kernel(const doub
 }
 
 // w -= sum_i c[i] V_i, and partial[b] = sum |w|^2 over block b's elements
-// (thread per element, coefficients staged in shared memory).
-__global__ void __launch_bounds__(kGmThreads) axpy_norm_kernel(const double2* __restrict__ V, long long ld,
+// (thread per element -- 256-thread blocks, up to 16 per SM, grid-stride over
+// the elements -- coefficients staged in shared memory).
+constexpr int kAnThreads = 256;
+__global__ void __launch_bounds__(kAnThreads) axpy_norm_kernel(const double2* __restrict__ V, long long ld,
                                                                long long n, int nv, const double2* __restrict__ c,
                                                                double2* __restrict__ w,
                                                                double2* __restrict__ partial, int want_norm) {
     __shared__ double2 cs[kGmChunk];
-    __shared__ double red[kGmWarps];
+    __shared__ double red[kAnThreads / 32];
     if (threadIdx.x < nv) cs[threadIdx.x] = c[threadIdx.x];
     __syncthreads();
-    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
-    const long long a = blockIdx.x * chunk, b = min(n, a + chunk);
     double nrm = 0.0;
-    for (long long e = a + threadIdx.x; e < b; e += blockDim.x) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         double2 x = w[e];
 #pragma unroll 8
         for (int i = 0; i < nv; ++i) {
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kGmThreads) axpy_norm_kernel(const double2* __
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0;
-        for (int q = 0; q < kGmWarps; ++q) t += red[q];
+        for (int q = 0; q < kAnThreads / 32; ++q) t += red[q];
         partial[(long long)blockIdx.x * kGmChunk] = make_double2(t, 0.0);
     }
 }
@@ -292,13 +295,14 @@ struct Vec {
     aim_plan* p;
     cudaStream_t s;
     long long n;
-    double2* part;        // [kGmBlocks][kGmChunk]
+    double2* part;        // [kPartBlocks][kGmChunk]
     double2* dcoef;       // [3][kMaxBasis + 1] device coefficients: h1, h2, misc
     const GmresOps& ops;
 
     unsigned nb() const { return (unsigned)((n + 255) / 256); }
-    void reduce(int nv, double2* out, bool acc) {
-        gm_reduce_kernel<<<(nv + 7) / 8, 256, 0, s>>>(part, kGmBlocks, nv, out, acc ? 1 : 0);
+    int an_blocks() const { return (int)std::max(1LL, std::min<long long>(kAnBlocks, (n + kAnThreads - 1) / kAnThreads)); }
+    void reduce(int nv, double2* out, bool acc, int nb = kGmBlocks) {
+        gm_reduce_kernel<<<(nv + 7) / 8, 256, 0, s>>>(part, nb, nv, out, acc ? 1 : 0);
         note_launch("gmres_reduce");
     }
     void allreduce(double2* d, int nv) {
@@ -325,10 +329,10 @@ struct Vec {
                     attr_mask |= 1ULL << (p->device & 63);
                 }
                 const size_t smem = 2 * (size_t)(nv + 1) * kAdT * sizeof(double2);
-                axpy_dot_smem_kernel<<<kGmBlocks, kAdThreads, smem, s>>>(V, n, n, nv, c, w, part);
+                axpy_dot_smem_kernel<<<kAdBlocks, kAdThreads, smem, s>>>(V, n, n, nv, c, w, part);
             }
             note_launch("gmres_axpy_dot");
-            reduce(nv, out, false);
+            reduce(nv, out, false, kAdBlocks);
             allreduce(out, nv);
             return;
         }
@@ -340,12 +344,12 @@ struct Vec {
         for (int i0 = 0; i0 < nv; i0 += kGmChunk) {
             const int m = std::min(kGmChunk, nv - i0);
             const bool last = i0 + m >= nv;
-            axpy_norm_kernel<<<kGmBlocks, kGmThreads, 0, s>>>(V + (size_t)i0 * n, n, n, m, c + i0, w, part,
-                                                             (last && nrm2) ? 1 : 0);
+            axpy_norm_kernel<<<an_blocks(), kAnThreads, 0, s>>>(V + (size_t)i0 * n, n, n, m, c + i0, w, part,
+                                                                (last && nrm2) ? 1 : 0);
             note_launch("gmres_axpy_norm");
         }
         if (nrm2) {
-            reduce(1, nrm2, false);
+            reduce(1, nrm2, false, an_blocks());
             allreduce(nrm2, 1);
         }
     }
@@ -396,16 +400,19 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
         p->gm_V = p->alloc<double2>((size_t)(restart + 1) * std::max(1LL, n));
         p->gm_w = p->alloc<double2>(std::max(1LL, n));
         p->gm_z = p->alloc<double2>(std::max(1LL, n));
-        p->gm_part = p->alloc<double2>((size_t)kGmBlocks * kGmChunk + 3 * (kMaxBasis + 1));
+        p->gm_part = p->alloc<double2>((size_t)kPartBlocks * kGmChunk + 3 * (kMaxBasis + 1));
         p->gm_restart = restart;
         p->gm_n = n;
     }
     if (!p->gm_host) AIM_CUDA(cudaMallocHost(&p->gm_host, sizeof(double2) * 3 * (kMaxBasis + 1)));
     double2* hbuf = p->gm_host;
-    Vec g{p, s, n, p->gm_part, p->gm_part + (size_t)kGmBlocks * kGmChunk, ops};
+    Vec g{p, s, n, p->gm_part, p->gm_part + (size_t)kPartBlocks * kGmChunk, ops};
     double2* dh1 = g.dcoef;
-    double2* dh2 = g.dcoef + (kMaxBasis + 1);
-    double2* dmisc = g.dcoef + 2 * (kMaxBasis + 1);   // [0] ||.||^2, [1..] y coefficients
+    // h1, h2 and ||w||^2 of an iteration are adjacent (one fetch):
+    // [h1: cst][h2: cst][misc: [0] ||.||^2, [1..] y coefficients], cst = restart + 1
+    const int cst = restart + 1;
+    double2* dh2 = g.dcoef + cst;
+    double2* dmisc = g.dcoef + 2 * cst;
     double2* V = p->gm_V;
     double2* w = p->gm_w;
     double2* z = p->gm_z;
@@ -416,6 +423,17 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
         AIM_CUDA(cudaMemcpyAsync(h, d, sizeof(double2) * cnt, cudaMemcpyDeviceToHost, s));
     };
     auto sync = [&]() { AIM_CUDA(cudaStreamSynchronize(s)); };
+    if (!p->gm_ev) AIM_CUDA(cudaEventCreateWithFlags(&p->gm_ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    // the product of basis vector j (v_j in V[j]; for the unpreconditioned
+    // solve also in z, the product's fixed input)
+    auto product = [&](int j) {
+        if (pre) {
+            ops.precond(V + (size_t)j * n, z, s);
+            ops.matvec(z, w, s);
+        } else {
+            ops.matvec(z, w, s);
+        }
+    };
 
     AIM_CUDA(cudaMemsetAsync(x, 0, sizeof(double2) * n, s));
     g.norm2(b, dmisc);
@@ -447,28 +465,30 @@ int gmres_core(aim_plan* p, const GmresOps& ops, const double2* b, double2* x, i
         gv[0] = beta;
         int jd = 0;
         bool stop = false;
+        bool pending = false;   // the product of v_j is already enqueued
         for (int j = 0; j < restart; ++j) {
-            double2* vj = V + (size_t)j * n;
-            if (pre) {
-                ops.precond(vj, z, s);
-                ops.matvec(z, w, s);
-            } else {
-                ops.matvec(z, w, s);   // z == v_j
-            }
+            if (!pending) product(j);
+            pending = false;
             const int nv = j + 1;
             g.dots(V, nv, w, dh1);                 // pass 1
             g.axpy_dots(V, nv, dh1, w, dh2);       // pass 2
             g.axpy(V, nv, dh2, w, dmisc);          // pass 3 (+ ||w||^2)
             g.scale(w, dmisc, V + (size_t)(j + 1) * n, zin);
-            fetch(dh1, nv, hbuf);
-            fetch(dh2, nv, hbuf + (kMaxBasis + 1));
-            fetch(dmisc, 1, hbuf + 2 * (kMaxBasis + 1));
-            sync();
+            fetch(dh1, 2 * cst + 1, hbuf);
+            AIM_CUDA(cudaEventRecord(p->gm_ev, s));
+            // v_{j+1} is complete on the device: enqueue its product before the
+            // host works on the coefficients, so the GPU does not idle during
+            // the Givens update (wasted once per solve if this iteration converges)
+            if (j + 1 < restart && total + 1 < limit) {
+                product(j + 1);
+                pending = true;
+            }
+            AIM_CUDA(cudaEventSynchronize(p->gm_ev));
             for (int i = 0; i <= j; ++i) {
-                Hij(i, j) = cplx(hbuf[i].x, hbuf[i].y) + cplx(hbuf[kMaxBasis + 1 + i].x, hbuf[kMaxBasis + 1 + i].y);
+                Hij(i, j) = cplx(hbuf[i].x, hbuf[i].y) + cplx(hbuf[cst + i].x, hbuf[cst + i].y);
                 if (!finite(Hij(i, j))) throw Error(AIM_E_BREAKDOWN, "GMRES: non-finite Arnoldi coefficient");
             }
-            const double hn2 = hbuf[2 * (kMaxBasis + 1)].x;
+            const double hn2 = hbuf[2 * cst].x;
             const double hn = std::isfinite(hn2) ? std::sqrt(std::max(0.0, hn2)) : hn2;
             if (!std::isfinite(hn)) throw Error(AIM_E_BREAKDOWN, "GMRES: non-finite Arnoldi norm");
             Hij(j + 1, j) = hn;

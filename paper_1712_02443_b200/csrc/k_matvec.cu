@@ -872,6 +872,110 @@ __global__ void __launch_bounds__(32 * kNmWarps) interp_mma_kernel(const int32_t
 // R >= 8, accumulating onto the near rows): measured on C2 it is slower than
 // the gather kernel (0.253 vs 0.233 ms; chunk fill 0.26 at 16 rows), so the
 // gather kernel is the default.
+// Single right-hand side, component-interleaved potentials: Phi_i[g][4]
+// (one 64-byte record per grid node, written by phi_interleave_kernel).  A
+// lane pair shares a stencil node: the even lane loads its x, y potentials
+// and weights, the odd lane its z, phi ones, so one warp instruction reads 16
+// nodes' complete 64-byte records -- four runs of 256 contiguous bytes
+// (4 consecutive z nodes) instead of eight 64-byte runs per component -- and
+// the weights of 16 nodes as 512 contiguous bytes.  About 40 L1 wavefronts
+// per row instead of about 110 for the component-major gather
+// (interp1_kernel); fixed shuffle order => deterministic.
+__global__ void __launch_bounds__(256) phi_interleave_kernel(const double2* __restrict__ Phi, long long Ng,
+                                                             double2* __restrict__ Pi) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Ng) return;
+    double2 v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __ldcs(&Phi[c * Ng + g]);
+    double2* o = Pi + 4 * g;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[c] = v[c];
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) interp1i_kernel(const double2* __restrict__ Pi, const double* __restrict__ W,
+                                                       const int32_t* __restrict__ node0, int Ny, int Nz, long long N,
+                                                       double keta, double ik2, int accumulate,
+                                                       const int32_t* __restrict__ wrow, double2* __restrict__ y) {
+    constexpr int M1 = M + 1, S = M1 * M1 * M1, KI = (S + 15) / 16;   // node rounds of 16
+    const long long m = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (m >= N) return;
+    const int lane = threadIdx.x & 31, half = lane & 1, v = lane >> 1;
+    const long long g0 = node0[m];
+    const long long wr = wrow ? (long long)__ldg(&wrow[m]) : m;
+    const double* W2 = W + 4 * wr * S;
+    double2 w[KI], f[KI][2];
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+        const int u = v + 16 * k;
+        double b0 = 0, b1 = 0;
+        // volatile: every load of the row is issued before the first FMA
+        if (u < S)
+            asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];\n" : "=d"(b0), "=d"(b1) : "l"(W2 + 4 * u + 2 * half));
+        w[k] = make_double2(b0, b1);
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+        const int u = v + 16 * k;
+        f[k][0] = f[k][1] = make_double2(0, 0);
+        if (u < S) {
+            const int ui = u / (M1 * M1), uj = (u / M1) % M1, uk = u % M1;
+            const double* src = reinterpret_cast<const double*>(Pi + 4 * (g0 + ((long long)ui * Ny + uj) * Nz + uk) + 2 * half);
+            double a0, a1, a2, a3;
+            asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                         : "=d"(a0), "=d"(a1), "=d"(a2), "=d"(a3)
+                         : "l"(src));
+            f[k][0] = make_double2(a0, a1);
+            f[k][1] = make_double2(a2, a3);
+        }
+    }
+    // even lane: w_x Phi_x + w_y Phi_y; odd lane: w_z Phi_z - k^-2 w_phi Phi_phi
+    const double s1 = half ? -ik2 : 1.0;
+    double2 a = make_double2(0, 0);
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+        a.x = fma(w[k].x, f[k][0].x, a.x); a.y = fma(w[k].x, f[k][0].y, a.y);
+        a.x = fma(s1 * w[k].y, f[k][1].x, a.x); a.y = fma(s1 * w[k].y, f[k][1].y, a.y);
+    }
+    double2 tot = make_double2(-keta * a.y, keta * a.x);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        tot.x += __shfl_xor_sync(0xffffffffu, tot.x, off);
+        tot.y += __shfl_xor_sync(0xffffffffu, tot.y, off);
+    }
+    if (lane == 0) {
+        if (accumulate) {
+            const double2 o = y[m];
+            tot.x += o.x;
+            tot.y += o.y;
+        }
+        y[m] = tot;
+    }
+}
+
+// Interleaved interpolation (R = 1, complex128, M <= 4): Phi -> Phi_i in the
+// scratch buffer, then interp1i_kernel.  AIM_INTERP_IL=0 keeps interp1_kernel.
+static bool interp_interleaved(const aim_plan* p, int R) {
+    const char* e = getenv("AIM_INTERP_IL");
+    if (e && e[0] == '0') return false;
+    return R == 1 && p->prec == AIM_C128 && p->M <= 4 && p->W1 != nullptr;
+}
+
+static void launch_interp_il(aim_plan* p, const double2* Phi, double2* y, bool accumulate, cudaStream_t s) {
+    double2* Pi = p->W1;   // free after the x inverse pass; 4 Px Ny Nz >= 4 Ng elements
+    phi_interleave_kernel<<<nblk(p->Ng, 256), 256, 0, s>>>(Phi, p->Ng, Pi);
+    note_launch("phi_interleave");
+    const double keta = p->k * eta0(), ik2 = 1.0 / (p->k * p->k);
+    const int32_t* wrow = p->cp_on ? p->cp_wrow : nullptr;
+    const unsigned grid = nblk(p->N * 32, 256);
+    switch (p->M) {
+#define II(MM) case MM: interp1i_kernel<MM><<<grid, 256, 0, s>>>(Pi, p->W, p->node0, p->dims[1], p->dims[2], p->N, keta, ik2, accumulate ? 1 : 0, wrow, y); break;
+        II(1) II(2) II(3) II(4)
+#undef II
+    }
+}
+
 constexpr int kInterpMmaRhs = 8;
 
 template <class C>
@@ -939,7 +1043,8 @@ static void launch_interp_t(aim_plan* p, const C* Phi, C* y, int R, bool accumul
 }
 
 void launch_interp(aim_plan* p, const void* Phi, void* y, int R, bool accumulate, cudaStream_t s) {
-    if (p->prec == AIM_C64) launch_interp_t(p, (const float2*)Phi, (float2*)y, R, accumulate, s);
+    if (interp_interleaved(p, R)) launch_interp_il(p, (const double2*)Phi, (double2*)y, accumulate, s);
+    else if (p->prec == AIM_C64) launch_interp_t(p, (const float2*)Phi, (float2*)y, R, accumulate, s);
     else launch_interp_t(p, (const double2*)Phi, (double2*)y, R, accumulate, s);
     note_launch("interp");
 }
@@ -1160,6 +1265,29 @@ void convolve(aim_plan* p, const void* Q, void* Phi, int R, cudaStream_t s) {
 static void matvec_body(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
     Prof pr(p);
     pr.mark(0, s);
+    // Repetition-compressed single-RHS products: the near field (a sparse x
+    // dense product over L2-resident dictionary blocks, not HBM-bound) runs on
+    // the side stream beside the projection and the FFT passes (shared-memory /
+    // FP64 bound) and joins before the interpolation accumulates into y.
+    // AIM_CMP_SIDE=0 runs it in order (A/B); profiled products (aim_profile,
+    // per-stage events) run in order so the stage times stay separable.
+    const char* es = getenv("AIM_CMP_SIDE");
+    if (p->cmp_on && R == 1 && !p->prof && !(es && es[0] == '0')) {
+        AIM_CUDA(cudaEventRecord(p->ev_x, s));
+        AIM_CUDA(cudaStreamWaitEvent(p->side, p->ev_x, 0));
+        pr.mark(7, s);
+        launch_near(p, x, y, R, p->side);
+        AIM_CUDA(cudaEventRecord(p->ev_n, p->side));
+        pr.mark(8, s);
+        launch_project(p, x, p->Q, R, s);
+        pr.mark(1, s);
+        convolve_impl(p, p->Q, p->Q, R, s, &pr);
+        pr.mark(5, s);
+        AIM_CUDA(cudaStreamWaitEvent(s, p->ev_n, 0));
+        launch_interp(p, p->Q, y, R, true, s);
+        pr.mark(6, s);
+        return;
+    }
     pr.mark(7, s);
     launch_near(p, x, y, R, s);
     pr.mark(8, s);

@@ -32,6 +32,12 @@ out["rel_vs_general"] = float((y1 - y0).norm() / y0.norm())
 t, _ = timed_steps(lambda: plan.matvec(x, y), 30, 3)
 out["compressed_ms"] = 1e3 * t / 30
 out["compressed_stages"] = profile_stages(plan, x, y, 5)
+os.environ["AIM_CMP_SIDE"] = "0"        # near in order (the graphs are rebuilt by compress)
+plan.compress(1)
+t, _ = timed_steps(lambda: plan.matvec(x, y), 30, 3)
+out["compressed_in_order_ms"] = 1e3 * t / 30
+del os.environ["AIM_CMP_SIDE"]
+plan.compress(1)
 if gm_iters:
     for mode in (0, 1):
         plan.compress(mode)

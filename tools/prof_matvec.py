@@ -1,5 +1,5 @@
 """Run a few matvecs of one config (for ncu / compute-sanitizer captures).
-    python tools/prof_matvec.py [config] [nmatvec]"""
+    python tools/prof_matvec.py [config] [nmatvec] [cmp]"""
 import os
 import sys
 
@@ -16,6 +16,9 @@ cfg = get_config(name)
 mesh = make_mesh(cfg)
 plan = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
 x = torch.from_numpy(make_vectors(mesh.n_rwg, cfg.nrhs, 0)).cuda()
+if "cmp" in sys.argv[3:]:          # the repetition-compressed operators, single RHS
+    plan.compress(1)
+    x = x[:, 0].contiguous()
 for _ in range(nmv):
     y = plan.matvec(x)
 torch.cuda.synchronize()
