@@ -362,8 +362,11 @@ int aim_nccl_unique_id(void* id, int64_t bytes);
 
 /*
  * aim_slab_create -- build the slab-decomposed operator (complex128).
- * Mesh and scalars as aim_plan_create.  Every rank passes the full mesh; the
- * whole operator is built once per rank and each rank keeps its own rows.
+ * Mesh and scalars as aim_plan_create.  Every rank passes the full mesh and
+ * builds the grid, weights, projection and spectrum of the whole operator,
+ * but near-field rows (the dominant plan time and memory) only for the RWGs
+ * it owns; each rank keeps its own rows.  (With rank < 0 one base plan holds
+ * every rank's near rows.)
  * rank in [0, world) with nccl_id (host, 128 bytes, the same on every rank):
  *   one process per GPU, exchanges over NCCL (grouped send/recv; halos to
  *   the neighbouring ranks, two all-to-all FFT transposes, a broadcast

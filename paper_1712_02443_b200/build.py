@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libaim_b200.so")
 SOURCES = ["aim_api.cu", "k_plan.cu", "k_fft.cu", "k_matvec.cu", "k_gmres.cu", "k_slab.cu", "k_precond.cu",
-           "k_reduced.cu", "k_compress.cu"]
+           "k_reduced.cu", "k_compress.cu", "k_near_stream.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]

@@ -70,7 +70,7 @@ __global__ void round_f32_kernel(const double* __restrict__ a, long long n, floa
 }
 
 static float* rounded_copy(aim_plan* p, const double* a, long long n, cudaStream_t s) {
-    float* b = p->alloc<float>(n);
+    float* b = p->alloc<float>(n + 4);  // + bulk-copy slack (k_near_stream.cu)
     round_f32_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(a, n, b);
     note_launch("round_f32");
     return b;

@@ -195,6 +195,16 @@ struct aim_plan {
     int64_t* nrow = nullptr;      // [N+1]
     int32_t* ncol = nullptr;      // [nnzN]
     double2* nval = nullptr;      // [nnzN]
+    // near rows to build (slab ranks: the owned RWGs); empty = every row
+    std::vector<uint8_t> near_keep;
+    int ncol_padded = 0;          // ncol/nval/nval32 padded >= 16 bytes past nnzN (bulk copies)
+    // near rows in chunks of <= 1024 entries for the TMA-staged SpMV that runs
+    // beside the FFT (k_near_stream.cu; built on first use)
+    int ns_state = 0;             // 0 = not built, 1 = ready, -1 = not applicable
+    int ns_count = 0;             // chunks
+    int32_t* ns_crow = nullptr;   // [ns_count+1] first row of each chunk
+    int64_t* ns_cent = nullptr;   // [ns_count+1] first entry of each chunk
+    unsigned* ns_ctr = nullptr;   // chunk counter shared by the two launches
     // complex64 plans (reading D16): the fp64 tables rounded once
     int prec = AIM_C128;
     float* W32 = nullptr;         // [N][S][4]
@@ -394,6 +404,12 @@ void build_near_list(aim_plan* p, cudaStream_t s);
 void build_near_values(aim_plan* p, cudaStream_t s);
 void build_green_spectrum(aim_plan* p, cudaStream_t s);
 void build_near_blocks(aim_plan* p, cudaStream_t s);
+// TMA-staged near SpMV overlapped with the FFT (k_near_stream.cu)
+int near_overlap_mode();
+int near_overlap_ctas_per_sm();
+bool near_stream_ready(aim_plan* p, cudaStream_t s);
+void near_stream_reset(aim_plan* p, cudaStream_t s);
+void launch_near_stream(aim_plan* p, const void* x, void* y, int ctas_per_sm, cudaStream_t s);
 void build_near_mma(aim_plan* p, cudaStream_t s);
 void build_interp_mma(aim_plan* p, cudaStream_t s);
 void make_c64_blocks(aim_plan* p, cudaStream_t s);   // rounded nb_val for AIM_C64 plans

@@ -1288,6 +1288,27 @@ static void matvec_body(aim_plan* p, const void* x, void* y, int R, cudaStream_t
         pr.mark(6, s);
         return;
     }
+    // AIM_NEAR_OVL=1 (measured slower, kept opt-in): the near SpMV streams its
+    // matrix through shared memory beside the FFT passes (k_near_stream.cu):
+    // CTAs on the side stream from the end of the projection take a share of
+    // the row chunks, the rest is taken at full occupancy on s after the FFT;
+    // both join before the interpolation accumulates into y.
+    if (!p->cmp_on && R == 1 && !p->prof && near_overlap_mode() && near_stream_ready(p, s)) {
+        near_stream_reset(p, s);
+        launch_project(p, x, p->Q, R, s);
+        const int a = near_overlap_ctas_per_sm();   // 0: no side launch (A/B of the streamed kernel alone)
+        if (a > 0) {
+            AIM_CUDA(cudaEventRecord(p->ev_x, s));
+            AIM_CUDA(cudaStreamWaitEvent(p->side, p->ev_x, 0));
+            launch_near_stream(p, x, y, a, p->side);
+            AIM_CUDA(cudaEventRecord(p->ev_n, p->side));
+        }
+        convolve_impl(p, p->Q, p->Q, R, s, &pr);
+        launch_near_stream(p, x, y, 0, s);
+        if (a > 0) AIM_CUDA(cudaStreamWaitEvent(s, p->ev_n, 0));
+        launch_interp(p, p->Q, y, R, true, s);
+        return;
+    }
     pr.mark(7, s);
     launch_near(p, x, y, R, s);
     pr.mark(8, s);

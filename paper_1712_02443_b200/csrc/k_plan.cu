@@ -215,6 +215,7 @@ __global__ void near_scan_kernel(const double* __restrict__ cen, long long N, Ce
     int cx = cell_of(cen[3 * m], cg.lo[0], cg.csz, cg.nc[0]);
     int cy = cell_of(cen[3 * m + 1], cg.lo[1], cg.csz, cg.nc[1]);
     int cz = cell_of(cen[3 * m + 2], cg.lo[2], cg.csz, cg.nc[2]);
+    if (FILL && rowp[m + 1] == rowp[m]) return;   // a row dropped by near_keep (every kept row holds m itself)
     long long pos = FILL ? rowp[m] : 0;
     int cnt = 0;
     for (int ax = max(cx - 1, 0); ax <= min(cx + 1, cg.nc[0] - 1); ++ax)
@@ -295,13 +296,17 @@ void build_near_list(aim_plan* p, cudaStream_t s) {
     std::vector<int32_t> cnt(N);
     AIM_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
     AIM_CUDA(cudaStreamSynchronize(s));
+    // rows a slab rank does not own get no near entries (aim_plan::near_keep)
+    if (!p->near_keep.empty())
+        for (long long m = 0; m < N; ++m)
+            if (!p->near_keep[m]) cnt[m] = 0;
     std::vector<int64_t> rowp(N + 1, 0);
     for (long long m = 0; m < N; ++m) rowp[m + 1] = rowp[m] + cnt[m];
     const long long nnz = rowp[N];
     if (nnz > 2147483647LL) throw Error(AIM_E_GRID, "near-field nnz exceeds 2^31-1");
     p->nnzN = nnz;
-    p->nrow = p->alloc<int64_t>(N + 1);
-    p->ncol = p->alloc<int32_t>(nnz);
+    p->nrow = p->alloc<int64_t>(N + 3);   // + bulk-copy slack
+    p->ncol = p->alloc<int32_t>(nnz + 4);  // + bulk-copy slack (k_near_stream.cu)
     AIM_CUDA(cudaMemcpyAsync(p->nrow, rowp.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, s));
     int32_t* tmp = nullptr;
     AIM_CUDA(cudaMalloc(&tmp, sizeof(int32_t) * std::max<long long>(1, nnz)));
@@ -866,7 +871,8 @@ __global__ void htab_kernel(double2* tab, int D, double h, double k) {
 }
 
 void build_near_values(aim_plan* p, cudaStream_t s) {
-    p->nval = p->alloc<double2>(p->nnzN);
+    p->nval = p->alloc<double2>(p->nnzN + 1);
+    p->ncol_padded = 1;
     const double lim = p->r * (1.0 + 1e-9);
     // table of G(h|d|) over |d_a| <= D in shared memory; offsets beyond the
     // table (huge near radii) fall back to direct evaluation in the kernel

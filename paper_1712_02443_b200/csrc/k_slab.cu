@@ -335,8 +335,18 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     AIM_CUDA(cudaEventCreateWithFlags(&S->ev_x, cudaEventDisableTiming));
     AIM_CUDA(cudaEventCreateWithFlags(&S->ev_n, cudaEventDisableTiming));
     cudaStream_t s = S->stream;
-    // full plan: every rank builds the whole operator once and keeps its rows
+    // partition (host formula, checked below against the plan's own stencil bases)
+    std::vector<int> bx;
+    int Nx = 0;
+    slab_partition(V, T, E, nv, nt, N, h, M, world, S->X, bx, Nx);
+    // base plan: the grid, weights, projection and spectrum of the whole
+    // operator; with one rank per process the near rows (the dominant plan
+    // time and memory) only for the RWGs this rank owns
     S->base = new aim_plan();
+    if (!S->virt) {
+        S->base->near_keep.resize(N);
+        for (int64_t n = 0; n < N; ++n) S->base->near_keep[n] = owner_of(S->X, bx[n]) == rank;
+    }
     create_plan(V, nv, T, nt, E, N, k, h, M, r, AIM_C128, S->base);
     aim_plan* B = S->base;
     S->planar = B->planar;
@@ -345,10 +355,6 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     S->Nx = B->dims[0]; S->Ny = B->dims[1]; S->Nz = B->dims[2];
     S->Px = B->pads[0]; S->Py = B->pads[1]; S->Pz = B->pads[2];
     S->Zc = S->planar ? S->Nz : S->Pz;
-    // partition (host formula, checked against the plan's own stencil bases)
-    std::vector<int> bx;
-    int Nx = 0;
-    slab_partition(V, T, E, nv, nt, N, h, M, world, S->X, bx, Nx);
     if (Nx != S->Nx) throw Error(AIM_E_GRID, "slab partition disagrees with the plan's grid");
     std::vector<int32_t> pb(3 * N);
     AIM_CUDA(cudaMemcpy(pb.data(), B->base, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToHost));
@@ -441,16 +447,39 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
             lrowp[i + 1] = lrowp[i] + (growp[g + 1] - growp[g]);
         }
         q->nnzN = lrowp[nl];
-        q->nrow = q->alloc<int64_t>(nl + 1);
-        q->ncol = q->alloc<int32_t>(q->nnzN);
-        q->nval = q->alloc<double2>(q->nnzN);
+        q->nrow = q->alloc<int64_t>(nl + 3);
+        q->ncol = q->alloc<int32_t>(q->nnzN + 4);
+        q->nval = q->alloc<double2>(q->nnzN + 1);
+        q->ncol_padded = 1;
         h2d(q->nrow, lrowp.data(), sizeof(int64_t) * (nl + 1), s);
+        // AIM_SLAB_RANK_NEAR=1 (tests): with all slabs in one process, take each
+        // rank's near rows from its own base plan built with that rank's
+        // near_keep, as a one-rank-per-process rank does (the owned rows'
+        // lists are the same; the others are empty)
+        aim_plan* NB = B;
+        const char* rn = getenv("AIM_SLAB_RANK_NEAR");
+        if (S->virt && rn && rn[0] == '1') {
+            NB = new aim_plan();
+            NB->near_keep.resize(N);
+            for (int64_t n = 0; n < N; ++n) NB->near_keep[n] = owner[n] == w;
+            try {
+                create_plan(V, nv, T, nt, E, N, k, h, M, r, AIM_C128, NB);
+            } catch (...) {
+                destroy_plan(NB);
+                throw;
+            }
+        }
+        struct NbGuard {
+            aim_plan* nb; aim_plan* b;
+            ~NbGuard() { if (nb != b) destroy_plan(nb); }
+        } nb_guard{NB, B};
         if (nl) {
             long long* d_err = nullptr;
             AIM_CUDA(cudaMalloc(&d_err, sizeof(long long)));
             AIM_CUDA(cudaMemsetAsync(d_err, 0, sizeof(long long), s));
-            slab_near_rows_kernel<<<nblk(nl, 128), 128, 0, s>>>(S->perm, R.n0, nl, B->nrow, B->ncol, B->nval, d_iperm,
-                                                                d_owner, q->nrow, q->ncol, q->nval, N, B->nnzN, d_err);
+            slab_near_rows_kernel<<<nblk(nl, 128), 128, 0, s>>>(S->perm, R.n0, nl, NB->nrow, NB->ncol, NB->nval,
+                                                                d_iperm, d_owner, q->nrow, q->ncol, q->nval, N,
+                                                                NB->nnzN, d_err);
             note_launch("slab_near_rows");
             long long herr = 0;
             AIM_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(long long), cudaMemcpyDeviceToHost, s));
@@ -459,7 +488,7 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
             if (herr)
                 throw Error(AIM_E_GRID, "slab near rows: bad index code " + std::to_string(herr) + " rank " +
                                             std::to_string(w) + " nl " + std::to_string(nl) + " nnz " +
-                                            std::to_string(q->nnzN) + " gnnz " + std::to_string(B->nnzN));
+                                            std::to_string(q->nnzN) + " gnnz " + std::to_string(NB->nnzN));
         }
         AIM_CUDA(cudaStreamSynchronize(s));
         S->ranks.push_back(R);

@@ -421,6 +421,9 @@ bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, con
         if (!(mask >> (dev & 63) & 1ULL)) {                                                                   \
             AIM_CUDA(cudaFuncSetAttribute(ymode2_kernel<PP, A, B, C, NZ, NT, MINB>,                           \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+            if (near_overlap_mode())                                                                          \
+                AIM_CUDA(cudaFuncSetAttribute(ymode2_kernel<PP, A, B, C, NZ, NT, MINB>,                       \
+                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));          \
             mask |= 1ULL << (dev & 63);                                                                       \
         }                                                                                                     \
         ymode2_kernel<PP, A, B, C, NZ, NT, MINB><<<148 * MINB, NT, smem, s>>>(                                \

@@ -542,3 +542,30 @@ def test_fused_mode2_cluster_variant_c3(monkeypatch):
     b = G.convolve(Q)
     assert rel(b.cpu().numpy(), a.cpu().numpy()) <= 1e-13
     G.close()
+
+
+@pytest.mark.parametrize("name", SMALL + ["c2", "c3", "c4"])
+def test_near_stream_overlap(name, monkeypatch):
+    """H6 beside the FFT (AIM_NEAR_OVL=1, k_near_stream.cu; opt-in, measured
+    slower): the single-RHS product whose near SpMV streams its rows through
+    shared memory (TMA bulk copies, CTAs beside the FFT taking a share of the
+    row chunks, the rest after it, chunks from one counter) equals the
+    in-order near1 product bit for bit (same per-row summation order), eager
+    and as a replayed graph, for several splits."""
+    from paper_1712_02443_b200 import AimPlan
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    x = torch.from_numpy(make_vectors(mesh.n_rwg, 1, 11)[:, 0].copy()).cuda()
+    monkeypatch.setenv("AIM_NEAR_OVL", "0")
+    A = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    y0 = A.matvec(x)
+    assert torch.equal(A.matvec(x), y0)
+    A.close()
+    monkeypatch.setenv("AIM_NEAR_OVL", "1")
+    for a, f in (("1", "0.25"), ("2", "1.0"), ("0", "0")):
+        monkeypatch.setenv("AIM_NEAR_OVL_A", a)
+        monkeypatch.setenv("AIM_NEAR_OVL_F", f)
+        B = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+        for _ in range(3):                     # eager, capture, replay
+            assert torch.equal(B.matvec(x), y0)
+        B.close()

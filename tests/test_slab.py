@@ -139,6 +139,31 @@ def test_slab_matvec_vs_single_and_oracle(name, world, nrhs, mode, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name,world", [("c1", 2), ("c1", 3), ("t_dissim", 3), ("t_vol", 2), ("c2", 4)])
+def test_slab_rank_local_near_rows(name, world, monkeypatch):
+    """Rank-local plan build: a one-rank-per-process rank builds near rows only
+    for the RWGs it owns (aim_plan::near_keep).  AIM_SLAB_RANK_NEAR=1 makes the
+    in-process slabs take each rank's rows from a base plan built that way;
+    the product equals the single plan's to 1e-13 and the near rows add up to
+    the full near matrix."""
+    import torch
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    monkeypatch.setenv("AIM_SLAB_RANK_NEAR", "1")
+    slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
+    q = [slab.query(r) for r in range(world)]
+    assert sum(d["nnz_near"] for d in q) == single.info["nnz_near"]
+    xt = torch.from_numpy(make_vectors(mesh.n_rwg, 2, 5)).cuda()
+    y1 = single.matvec(xt)
+    yg = slab.matvec(xt)
+    assert float((yg - y1).norm() / y1.norm()) <= 1e-13
+    slab.close()
+    single.close()
+
+
+@pytest.mark.gpu
 def test_slab_matvec_c2_full_size():
     """C2 at full size over 4 and 8 slabs (device-copy exchanges): equal to the
     single-GPU plan to 1e-13 on all 16 RHS."""
