@@ -233,7 +233,7 @@ void destroy_plan(aim_plan* p) {
     cudaSetDevice(p->device);
     // the plan's own work is on its streams; the caller orders (or has
     // finished) the products it queued on its streams before destroying
-    for (cudaStream_t st : {p->stream, p->side, p->hp_in, p->hp_out})
+    for (cudaStream_t st : {p->stream, p->side, p->hi, p->hp_in, p->hp_out})
         if (st) cudaStreamSynchronize(st);
     for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
     if (p->gx_fork) cudaEventDestroy(p->gx_fork);
@@ -246,6 +246,8 @@ void destroy_plan(aim_plan* p) {
     for (auto e : p->ev_pool) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->side) cudaStreamDestroy(p->side);
+    if (p->hi) cudaStreamDestroy(p->hi);
+    if (p->ev_h) cudaEventDestroy(p->ev_h);
     if (p->ev_x) cudaEventDestroy(p->ev_x);
     if (p->ev_n) cudaEventDestroy(p->ev_n);
     if (p->gm_host) cudaFreeHost(p->gm_host);

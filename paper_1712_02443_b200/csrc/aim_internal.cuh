@@ -354,6 +354,9 @@ struct aim_plan {
     // side stream for the near-field SpMV (overlaps the FFT passes)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_x = nullptr, ev_n = nullptr;
+    // high-priority stream for the FFT passes beside the near SpMV (AIM_NEAR_PRIO=1)
+    cudaStream_t hi = nullptr;
+    cudaEvent_t ev_h = nullptr;
     // live stage timing (aim_profile): kProfEvents events per profiled matvec
     int prof = 0;
     std::vector<cudaEvent_t> ev_pool;
@@ -406,6 +409,8 @@ void build_green_spectrum(aim_plan* p, cudaStream_t s);
 void build_near_blocks(aim_plan* p, cudaStream_t s);
 // TMA-staged near SpMV overlapped with the FFT (k_near_stream.cu)
 int near_overlap_mode();
+int near_prio_mode();
+int smem_carveout_max();
 int near_overlap_ctas_per_sm();
 bool near_stream_ready(aim_plan* p, cudaStream_t s);
 void near_stream_reset(aim_plan* p, cudaStream_t s);

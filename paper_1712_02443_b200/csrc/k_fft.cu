@@ -839,7 +839,7 @@ static void ensure_smem_attr(K kernel) {
     AIM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     // with the near SpMV beside the FFT (k_near_stream.cu) every SM stays in
     // its largest shared-memory configuration, so both CTAs fit at once
-    if (near_overlap_mode())
+    if (smem_carveout_max())
         AIM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     done.emplace_back(key, dev);
 }

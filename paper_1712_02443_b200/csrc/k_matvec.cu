@@ -1309,6 +1309,40 @@ static void matvec_body(aim_plan* p, const void* x, void* y, int R, cudaStream_t
         launch_interp(p, p->Q, y, R, true, s);
         return;
     }
+    // AIM_NEAR_PRIO=1: the FFT passes on a high-priority stream, near1 in
+    // 128-thread CTAs on the side stream from the end of the projection, so
+    // the block scheduler places the persistent FFT CTAs first and fills the
+    // rest of every SM with near rows; both join before the interpolation.
+    if (!p->cmp_on && R == 1 && !p->prof && near_prio_mode() && p->prec == AIM_C128) {
+        if (!p->hi) {
+            int lo = 0, hi = 0;
+            AIM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            AIM_CUDA(cudaStreamCreateWithPriority(&p->hi, cudaStreamNonBlocking, hi));
+            AIM_CUDA(cudaEventCreateWithFlags(&p->ev_h, cudaEventDisableTiming));
+            static unsigned long long attr = 0;  // per device
+            const char* en = getenv("AIM_NEAR1_CARVE");   // A/B: 0 = near1 keeps its default carveout
+            if (!(attr >> (p->device & 63) & 1ULL) && !(en && en[0] == '0')) {
+                AIM_CUDA(cudaFuncSetAttribute(near1_kernel<double2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                attr |= 1ULL << (p->device & 63);
+            }
+        }
+        launch_project(p, x, p->Q, R, s);
+        AIM_CUDA(cudaEventRecord(p->ev_x, s));
+        AIM_CUDA(cudaStreamWaitEvent(p->side, p->ev_x, 0));
+        AIM_CUDA(cudaStreamWaitEvent(p->hi, p->ev_x, 0));
+        const char* et = getenv("AIM_NEAR_PRIO_T");
+        const int nt = et ? atoi(et) : 128;
+        near1_kernel<double2><<<nblk(p->N * 32, nt), nt, 0, p->side>>>(p->nrow, p->ncol, p->nval, (const double2*)x,
+                                                                       p->N, (double2*)y);
+        note_launch("near");
+        AIM_CUDA(cudaEventRecord(p->ev_n, p->side));
+        convolve_impl(p, p->Q, p->Q, R, p->hi, &pr);
+        AIM_CUDA(cudaEventRecord(p->ev_h, p->hi));
+        AIM_CUDA(cudaStreamWaitEvent(s, p->ev_h, 0));
+        AIM_CUDA(cudaStreamWaitEvent(s, p->ev_n, 0));
+        launch_interp(p, p->Q, y, R, true, s);
+        return;
+    }
     pr.mark(7, s);
     launch_near(p, x, y, R, s);
     pr.mark(8, s);
@@ -1357,7 +1391,8 @@ void matvec(aim_plan* p, const void* x, void* y, int R, cudaStream_t s) {
         }
         AIM_CUDA(cudaStreamEndCapture(p->stream, &graph));
         cudaGraphExec_t exec;
-        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        const cudaError_t e =
+            cudaGraphInstantiate(&exec, graph, near_prio_mode() ? cudaGraphInstantiateFlagUseNodePriority : 0);
         cudaGraphDestroy(graph);
         AIM_CUDA(e);
         const long long nk = launch_counter() - before;

@@ -249,6 +249,20 @@ int near_overlap_mode() {
     return (e && e[0] == '1') ? 1 : 0;
 }
 
+// AIM_NEAR_PRIO=1: near1 (128-thread CTAs) on the side stream beside the FFT
+// passes, which run on a high-priority stream (k_matvec.cu matvec_body).
+int near_prio_mode() {
+    const char* e = getenv("AIM_NEAR_PRIO");
+    return (e && e[0] == '1') ? 1 : 0;
+}
+
+// keep every SM in its largest shared-memory configuration (both overlap modes)
+int smem_carveout_max() {
+    const char* e = getenv("AIM_NEAR_CARVE");   // A/B: 0 = leave the FFT kernels' carveout alone
+    if (e && e[0] == '0') return 0;
+    return near_overlap_mode() || near_prio_mode();
+}
+
 static int near_overlap_ctas() {
     const char* e = getenv("AIM_NEAR_OVL_A");
     const int a = e ? atoi(e) : 1;

@@ -421,7 +421,7 @@ bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, con
         if (!(mask >> (dev & 63) & 1ULL)) {                                                                   \
             AIM_CUDA(cudaFuncSetAttribute(ymode2_kernel<PP, A, B, C, NZ, NT, MINB>,                           \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-            if (near_overlap_mode())                                                                          \
+            if (smem_carveout_max())                                                                          \
                 AIM_CUDA(cudaFuncSetAttribute(ymode2_kernel<PP, A, B, C, NZ, NT, MINB>,                       \
                                               cudaFuncAttributePreferredSharedMemoryCarveout, 100));          \
             mask |= 1ULL << (dev & 63);                                                                       \

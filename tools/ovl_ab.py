@@ -19,13 +19,18 @@ mesh = make_mesh(cfg)
 x = torch.from_numpy(make_vectors(mesh.n_rwg, 1, 0)[:, 0].copy()).cuda()
 out = {"config": name}
 ref = None
-variants = [("off", {"AIM_NEAR_OVL": "0"}), ("a0", {"AIM_NEAR_OVL": "1", "AIM_NEAR_OVL_A": "0"}),
-            ("a1f25", {"AIM_NEAR_OVL": "1", "AIM_NEAR_OVL_A": "1"}), ("a1f10", {"AIM_NEAR_OVL": "1", "AIM_NEAR_OVL_A": "1", "AIM_NEAR_OVL_F": "0.1"}),
-            ("a1f50", {"AIM_NEAR_OVL": "1", "AIM_NEAR_OVL_A": "1", "AIM_NEAR_OVL_F": "0.5"}), ("a2f25", {"AIM_NEAR_OVL": "1", "AIM_NEAR_OVL_A": "2"}),
-            ("off2", {"AIM_NEAR_OVL": "0"})]
+ALL = {"off": {}, "prio128": {"AIM_NEAR_PRIO": "1"}, "prio256": {"AIM_NEAR_PRIO": "1", "AIM_NEAR_PRIO_T": "256"},
+       "prio256_nc": {"AIM_NEAR_PRIO": "1", "AIM_NEAR_PRIO_T": "256", "AIM_NEAR_CARVE": "0", "AIM_NEAR1_CARVE": "0"},
+       "prio256_fc": {"AIM_NEAR_PRIO": "1", "AIM_NEAR_PRIO_T": "256", "AIM_NEAR1_CARVE": "0"},
+       "prio128_nc": {"AIM_NEAR_PRIO": "1", "AIM_NEAR_CARVE": "0", "AIM_NEAR1_CARVE": "0"},
+       "prio128_fc": {"AIM_NEAR_PRIO": "1", "AIM_NEAR1_CARVE": "0"},
+       "ovl_a1f10": {"AIM_NEAR_OVL": "1", "AIM_NEAR_OVL_A": "1", "AIM_NEAR_OVL_F": "0.1"}}
+names = sys.argv[3].split(",") if len(sys.argv) > 3 else ["off", "prio128", "prio256", "ovl_a1f10", "off"]
+variants = [(n, ALL[n]) for n in names]
 plan = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
 for tag, env in variants:
-    for k in ("AIM_NEAR_OVL", "AIM_NEAR_OVL_A", "AIM_NEAR_OVL_F"):
+    for k in ("AIM_NEAR_OVL", "AIM_NEAR_OVL_A", "AIM_NEAR_OVL_F", "AIM_NEAR_PRIO", "AIM_NEAR_PRIO_T", "AIM_NEAR_CARVE",
+              "AIM_NEAR1_CARVE"):
         os.environ.pop(k, None)
     os.environ.update(env)
     plan.compress(0)                   # drops the captured graphs
@@ -33,7 +38,7 @@ for tag, env in variants:
     if ref is None:
         ref = y.clone()
     t, _ = timed_steps(lambda: plan.matvec(x, y), steps, 3)
-    out[tag] = {"ms": 1e3 * t / steps, "bitwise_equal_to_off": bool(torch.equal(y, ref))}
+    out[tag + ("" if tag not in out else "_2")] = {"ms": 1e3 * t / steps, "bitwise_equal_to_off": bool(torch.equal(y, ref))}
     print(tag, out[tag], flush=True)
 print(json.dumps(out), flush=True)
 plan.close()
