@@ -75,3 +75,89 @@ def test_gmres_golden_full_size(name):
     r_gpu = Vh[sub] - ZJ[sub]
     r_ora = Vh[sub] - O.matvec_rows(Jh, sub, method="fft")
     assert np.linalg.norm(r_gpu - r_ora) <= 1e-8 * np.linalg.norm(Vh[sub])
+
+
+def _arnoldi_lstsq(matvec, V, k):
+    """Plain PyTorch GMRES reference of the same operation (one cycle of k
+    steps, no restart): Arnoldi with modified Gram-Schmidt applied twice, then
+    the (j+1) x j Hessenberg least-squares problems solved densely on the host
+    (numpy lstsq) -- no Givens recurrences, nothing shared with k_gmres.cu.
+    Returns J_k and |beta e1 - H_j y_j| / beta for j = 1..k."""
+    beta = torch.linalg.vector_norm(V)
+    Q = torch.empty((k + 1, V.numel()), dtype=V.dtype, device=V.device)
+    H = np.zeros((k + 1, k), dtype=np.complex128)
+    Q[0] = V / beta
+    for j in range(k):
+        w = matvec(Q[j]).clone()
+        for _ in range(2):
+            for i in range(j + 1):
+                h = torch.vdot(Q[i], w)
+                w -= h * Q[i]
+                H[i, j] += complex(h)
+        hn = torch.linalg.vector_norm(w)
+        H[j + 1, j] = float(hn)
+        Q[j + 1] = w / hn
+    b = float(beta)
+    hist = []
+    y = None
+    for j in range(1, k + 1):
+        e1 = np.zeros(j + 1, dtype=np.complex128)
+        e1[0] = b
+        y, *_ = np.linalg.lstsq(H[:j + 1, :j], e1, rcond=None)
+        hist.append(np.linalg.norm(e1 - H[:j + 1, :j] @ y) / b)
+    J = (torch.as_tensor(y, device=V.device)[:, None] * Q[:k]).sum(0)
+    return J, np.asarray(hist)
+
+
+def test_gmres_c4_one_cycle():
+    """C4 (BASELINE.json configs[3], the GMRES(50) workload) at D15's k = 50.
+    The oracle's full C4 solve is out of reach (its near matrix alone is about
+    13 core-hours, each product about 80 s), so no golden file exists for C4
+    and the golden test above skips it.  Here the device solver is held to
+      * a plain PyTorch Arnoldi + dense least-squares GMRES of the same k on
+        the same operator: J_k <= 1e-5, the residual history <= 1e-6 relative;
+      * GMRES's defining property at any size: r_k = V - Z J_k is orthogonal to
+        Z K_k (checked against Z V and Z J_k, both in Z K_k);
+      * the oracle: V on the stratified rows, and the residual of the GPU's J_k
+        on sampled rows recomputed with the oracle's row-sampled product
+        (matvec_rows, pinned in tests/test_oracle_aim.py), <= 1e-8 ||V||.
+    The operator itself is compared with the oracle on >= 1,000 stratified
+    rows in tests/test_gpu_parity.py."""
+    from paper_1712_02443_b200 import AimPlan
+    from workloads.sketch import stratified_rows
+    cfg = get_config("c4")
+    mesh = make_mesh(cfg)
+    G = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    V = G.planewave_rhs()
+    k = 50
+    J, it, rr, _ = G.gmres(V, restart=50, tol=1e-4, fixed_iters=k)
+    assert it == k
+    hist = G.gmres_history()
+    assert hist.size == k
+    Jref, href = _arnoldi_lstsq(G.matvec, V, k)
+    assert float(torch.linalg.vector_norm(J - Jref)) <= 1e-5 * float(torch.linalg.vector_norm(Jref))
+    assert np.abs(hist - href).max() <= 1e-6 * href.min()
+    del Jref
+    ZJ = G.matvec(J)
+    r = V - ZJ
+    bn = float(torch.linalg.vector_norm(V))
+    rn = float(torch.linalg.vector_norm(r))
+    assert abs(rn / bn - rr) <= 1e-6 * rr
+    assert abs(rn / bn - hist[-1]) <= 1e-6 * rr
+    ZV = G.matvec(V)
+    for Zv in (ZV, ZJ):
+        assert abs(complex(torch.vdot(Zv, r))) <= 1e-8 * float(torch.linalg.vector_norm(Zv)) * rn
+    Vh, Jh, ZJh = V.cpu().numpy(), J.cpu().numpy(), ZJ.cpu().numpy()
+    G.close()
+    del J, V, ZJ, ZV, r
+    torch.cuda.empty_cache()
+    from oracle.aim import OraclePlan
+    from oracle.excitation import plane_wave_rhs
+    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    rows = stratified_rows(O.bases, n_random=1024, seed=7)
+    Vo = plane_wave_rhs(O.ctx)
+    assert np.abs(Vh[rows] - Vo[rows]).max() <= 1e-13 * np.abs(Vo).max()
+    sub = rows[np.linspace(0, rows.size - 1, 192).astype(np.int64)]
+    r_gpu = Vh[sub] - ZJh[sub]
+    r_ora = Vo[sub] - O.matvec_rows(Jh, sub, method="fft")
+    assert np.linalg.norm(r_gpu - r_ora) <= 1e-8 * np.linalg.norm(Vh[sub])
