@@ -118,8 +118,9 @@ def test_gmres_c4_one_cycle():
         the same operator: J_k <= 1e-5, the residual history <= 1e-6 relative;
       * GMRES's defining property at any size: r_k = V - Z J_k is orthogonal to
         Z K_k (checked against Z V and Z J_k, both in Z K_k);
-      * the oracle: V on the stratified rows, and the residual of the GPU's J_k
-        on sampled rows recomputed with the oracle's row-sampled product
+      * the oracle: V on the stratified rows (<= 1e-13), and, with
+        AIM_TEST_SLOW=1 (about 6 CPU-minutes), the residual of the GPU's J_k on
+        sampled rows recomputed with the oracle's row-sampled product
         (matvec_rows, pinned in tests/test_oracle_aim.py), <= 1e-8 ||V||.
     The operator itself is compared with the oracle on >= 1,000 stratified
     rows in tests/test_gpu_parity.py."""
@@ -151,12 +152,17 @@ def test_gmres_c4_one_cycle():
     G.close()
     del J, V, ZJ, ZV, r
     torch.cuda.empty_cache()
-    from oracle.aim import OraclePlan
+    from oracle.efie import EfieContext
     from oracle.excitation import plane_wave_rhs
-    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    rows = stratified_rows(O.bases, n_random=1024, seed=7)
-    Vo = plane_wave_rhs(O.ctx)
+    from oracle.aim import stencil_bases
+    ctx = EfieContext(mesh.vertices, mesh.triangles, mesh.rwg, cfg.k)
+    rows = stratified_rows(stencil_bases(ctx.geo["centre"], cfg.h, cfg.M), n_random=1024, seed=7)
+    Vo = plane_wave_rhs(ctx)
     assert np.abs(Vh[rows] - Vo[rows]).max() <= 1e-13 * np.abs(Vo).max()
+    if os.environ.get("AIM_TEST_SLOW") != "1":
+        return      # the oracle's C4 plan + one FFT product of J_k take about 6 CPU-minutes
+    from oracle.aim import OraclePlan
+    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
     sub = rows[np.linspace(0, rows.size - 1, 192).astype(np.int64)]
     r_gpu = Vh[sub] - ZJh[sub]
     r_ora = Vo[sub] - O.matvec_rows(Jh, sub, method="fft")
