@@ -374,6 +374,9 @@ int aim_nccl_unique_id(void* id, int64_t bytes);
  * rank < 0 (nccl_id ignored): all `world` slabs on the current GPU in this
  *   process, exchanges as device copies with the same packing (checks the
  *   decomposition on one device).
+ * Planar layouts whose y length has a compile-time plan (210, 784) store the y
+ * pass's lines straight into the all-to-all blocks and load them back from
+ * there (AIM_SLAB_FUSE_PACK=0: separate pack/unpack kernels, same bits).
  * Errors: as aim_plan_create; AIM_E_ARG also for world * M > Nx;
  * AIM_E_NCCL.  Synchronous.
  */
@@ -389,9 +392,12 @@ int aim_slab_create(const double* vertices, int64_t nv, const int32_t* triangles
 int aim_slab_matvec(aim_slab* slab, const void* x, void* y, int32_t nrhs, void* stream);
 
 /* aim_gmres on the slab-decomposed operator (D15).  V, J:
- * device complex128 [N], replicated: every rank runs the identical iteration
- * (the Krylov vectors are replicated; only the products are distributed).
- * Collective with NCCL.  Synchronous.  Returns as aim_gmres. */
+ * device complex128 [N], replicated on entry and exit.  Inside, every rank
+ * keeps only its own rows [n0, n1) of the Krylov vectors; a product gathers
+ * the input rows to every rank, and every dot product is a local partial sum
+ * followed by an NCCL all-reduce of the (j+1) coefficients, so the iteration
+ * is identical on every rank.  (rank < 0: the vectors span all rows, no
+ * reduction.)  Collective with NCCL.  Synchronous.  Returns as aim_gmres. */
 int aim_slab_gmres(aim_slab* slab, const void* V, void* J, int32_t restart, double tol,
                    int32_t max_iters, int32_t fixed_iters, int32_t* iters, double* rel_res);
 

@@ -103,6 +103,13 @@ struct FftPass {
     int spec_mode = 0;
     int Pz = 0, PxH = 0;
     int off = 0, nky = 1, Rin = 1;
+    // Table-addressed lines (slab path: the all-to-all pack fused into the y-pass
+    // store, the unpack into its load; compile-time plans only, modes 0/1,
+    // complex128): element (oo, j, ii) of the output lives at
+    // out + jout[j] + oo * inner + ii instead of out + (oo * Lout + j) * inner + ii,
+    // the input likewise with jin.  Device tables of P entries, or null.
+    const long long* jin = nullptr;
+    const long long* jout = nullptr;
 };
 
 // Fused planar y/z pass (planar arrays): y fwd, direct z convolution with the
@@ -122,6 +129,8 @@ struct PlanarPass {
 };
 
 void launch_fft_pass(const FftPass& p, cudaStream_t s);
+// Pass with jin/jout tables: false (nothing launched) if no compile-time plan takes it.
+bool try_launch_fft_pass_tab(const FftPass& p, cudaStream_t s);
 void launch_planar_yz(const PlanarPass& p, cudaStream_t s);
 // z Toeplitz x G2 in place on lines [4][A][B][Nz][R]: (kx, ky) = (a, b) if kx_is_a
 // else (b + 0, a + off) -- the second form serves the slab path's ky pencils

@@ -228,7 +228,7 @@ __device__ __forceinline__ void planar_toeplitz(C* buf, const C* g2, int Py, int
 // Persistent CTAs, three tile buffers: X holds the tile being transformed, Y
 // is the ping-pong scratch, Z receives the next tile by cp.async; X and Z
 // swap after every tile.  All sizes compile-time (F::P, F::NL, F::T).
-template <class F, int MODE, int MINB, class C>
+template <class F, int MODE, int MINB, class C, bool TAB = false>
 __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles) {
     constexpr int P = F::P, NL = F::NL, T = F::T, JS = T / NL;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -252,11 +252,14 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
         if (!act) return;
         const int oo = ot * (NL / TI) + o, ii = itl * TI + i;
         const bool live = oo < outer && ii < inner;
-        const C* src = ((const C*)p.in) + (live ? (long long)oo * p.Lin * inner + ii : 0);
+        const bool tin = TAB && p.jin != nullptr;   // lines addressed through the jin table (fused unpack)
+        const C* src = ((const C*)p.in) + (live ? (long long)oo * (tin ? 1 : p.Lin) * inner + ii : 0);
 #pragma unroll 2
         for (int j = js; j < P; j += JS) {
             const bool v = live && j < p.Lin;
-            cp_async_c(&buf[j * NL + l], v ? src + (long long)j * inner : (const C*)p.in, v);
+            long long jo = (long long)j * inner;
+            if constexpr (TAB) { if (tin && v) jo = __ldg(&p.jin[j]); }
+            cp_async_c(&buf[j * NL + l], v ? src + jo : (const C*)p.in, v);
         }
     };
     auto advance = [&]() {
@@ -288,9 +291,21 @@ __global__ void __launch_bounds__(F::T, MINB) fft_ct_kernel(FftPass p, int tiles
         }
         const int oo = cur_o * (NL / TI) + o, ii = cur_i * TI + i;
         if (act && oo < outer && ii < inner) {
-            C* dst = ((C*)p.out) + (long long)oo * p.Lout * inner + ii;
+            if constexpr (TAB) {
+                if (p.jout != nullptr) {      // fused pack: line j goes to its owner's block
+                    C* dst = ((C*)p.out) + (long long)oo * inner + ii;
 #pragma unroll 2
-            for (int j = js; j < p.Lout; j += JS) __stcs(dst + (long long)j * inner, res[j * NL + l]);
+                    for (int j = js; j < p.Lout; j += JS) __stcs(dst + __ldg(&p.jout[j]), res[j * NL + l]);
+                } else {
+                    C* dst = ((C*)p.out) + (long long)oo * p.Lout * inner + ii;
+#pragma unroll 2
+                    for (int j = js; j < p.Lout; j += JS) __stcs(dst + (long long)j * inner, res[j * NL + l]);
+                }
+            } else {
+                C* dst = ((C*)p.out) + (long long)oo * p.Lout * inner + ii;
+#pragma unroll 2
+                for (int j = js; j < p.Lout; j += JS) __stcs(dst + (long long)j * inner, res[j * NL + l]);
+            }
         }
         cur_o = ot;
         cur_i = itl;
@@ -898,6 +913,17 @@ static bool try_ct_pass(FftPass p, cudaStream_t s) {
         if (e != cudaSuccess)
             throw Error(AIM_E_CUDA, "fft_ct_kernel P=" + std::to_string(F::P) + ": " + cudaGetErrorString(e));
     };
+    if (p.jin || p.jout) {
+        // table-addressed lines: complex128, forward/inverse, the planar configs' lengths
+        if constexpr (sizeof(C) == 16 && (F::P == 210 || F::P == 784)) {
+            if (p.mode == 0) go(fft_ct_kernel<F, 0, MINB, C, true>);
+            else if (p.mode == 1) go(fft_ct_kernel<F, 1, MINB, C, true>);
+            else return false;
+            return true;
+        } else {
+            return false;
+        }
+    }
     if (p.mode == 0) go(fft_ct_kernel<F, 0, MINB, C>);
     else if (p.mode == 1) go(fft_ct_kernel<F, 1, MINB, C>);
     else go(fft_ct_kernel<F, 2, MINB, C>);
@@ -941,8 +967,18 @@ static void launch_fft_pass_t(FftPass p, cudaStream_t s) {
     }
 }
 
+bool try_launch_fft_pass_tab(const FftPass& p, cudaStream_t s) {
+    if (p.outer <= 0 || p.inner <= 0) return true;
+    const char* ce = getenv("AIM_FFT_NOCT");
+    if (p.prec == 1 || p.TI > 0 || (ce && ce[0] == '1')) return false;
+    const bool ok = try_ct_pass<double2, Ct210, 2>(p, s) || try_ct_pass<double2, Ct784, (AIM_CT784_NL > 2 ? 1 : 2)>(p, s);
+    if (ok) note_launch("fft_pass");
+    return ok;
+}
+
 void launch_fft_pass(const FftPass& p, cudaStream_t s) {
     if (p.outer <= 0 || p.inner <= 0) return;
+    if (p.jin || p.jout) throw Error(AIM_E_GRID, "launch_fft_pass: table-addressed passes go through try_launch_fft_pass_tab");
     if (p.prec == 1) launch_fft_pass_t<float2>(p, s);
     else launch_fft_pass_t<double2>(p, s);
     note_launch("fft_pass");

@@ -252,6 +252,8 @@ struct aim_slab_rank {
     double2* rb = nullptr;    // receive blocks
     double2* hb = nullptr;    // halo staging [4][M][Ny][Nz][R]
     long long* d_off1 = nullptr;   // pack offsets of all-to-all #1, per destination
+    long long* d_jtab = nullptr;   // [4][Py] planar: element offset of line (c, ky) in the packed blocks
+                                   // (the pack fused into the y-pass store, the unpack into its load)
 };
 
 struct aim_slab {
@@ -272,6 +274,7 @@ struct aim_slab {
     double2* xp = nullptr;                // [N][R] permuted x
     double2* yp = nullptr;                // [N][R] permuted y
     int ws_nrhs = 0;
+    int tab_nrhs = 0;                      // nrhs the offset tables (d_off1, d_jtab) were written for
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;          // near-field rows, overlapping the FFT and its all-to-alls
@@ -516,8 +519,35 @@ static void slab_create(const double* V, int64_t nv, const int32_t* T, int64_t n
     S->bytes_halo = 2LL * 4 * M * S->Ny * S->Nz * 16 * (world > 1 ? 2 : 0);
 }
 
+// Offsets of the all-to-all #1 blocks for exactly R right-hand sides (they scale
+// with R, so a product with fewer RHS than the workspace was sized for needs its own).
+static void slab_tables(aim_slab* S, int R) {
+    if (S->tab_nrhs == R) return;
+    // products of the previous nrhs may still be reading the tables on the caller's stream
+    AIM_CUDA(cudaDeviceSynchronize());
+    const long long ZR = (long long)S->Zc * R;
+    for (auto& Rk : S->ranks) {
+        std::vector<long long> off(S->world + 1, 0);
+        for (int w = 0; w < S->world; ++w) off[w + 1] = off[w] + 4LL * (S->KY[w + 1] - S->KY[w]) * Rk.Xl * ZR;
+        h2d(Rk.d_off1, off.data(), sizeof(long long) * (S->world + 1), S->stream);
+        // line (c, ky) of the y-transformed slab starts at off[s] + ((c kys + ky - KY_s) Xl) ZR, s = owner of ky
+        std::vector<long long> jt(4 * (size_t)S->Py);
+        for (int c = 0; c < 4; ++c)
+            for (int w = 0; w < S->world; ++w) {
+                const long long kys = S->KY[w + 1] - S->KY[w];
+                for (int ky = S->KY[w]; ky < S->KY[w + 1]; ++ky)
+                    jt[(size_t)c * S->Py + ky] = off[w] + ((c * kys + (ky - S->KY[w])) * Rk.Xl) * ZR;
+            }
+        h2d(Rk.d_jtab, jt.data(), sizeof(long long) * jt.size(), S->stream);
+    }
+    S->tab_nrhs = R;
+}
+
 static void slab_workspace(aim_slab* S, int R) {
-    if (S->ws_nrhs >= R) return;
+    if (S->ws_nrhs >= R) {
+        slab_tables(S, R);
+        return;
+    }
     AIM_CUDA(cudaDeviceSynchronize());
     S->release(S->xp);
     S->release(S->yp);
@@ -526,7 +556,7 @@ static void slab_workspace(aim_slab* S, int R) {
     const long long NzR = (long long)S->Nz * R, ZR = (long long)S->Zc * R;
     for (auto& Rk : S->ranks) {
         for (void* ptr : {(void*)Rk.Qh, (void*)Rk.Wy, (void*)Rk.Wy1, (void*)Rk.T, (void*)Rk.Tp, (void*)Rk.sb,
-                          (void*)Rk.rb, (void*)Rk.hb, (void*)Rk.d_off1})
+                          (void*)Rk.rb, (void*)Rk.hb, (void*)Rk.d_off1, (void*)Rk.d_jtab})
             S->release(ptr);
         Rk.Wy1 = nullptr;
         Rk.Tp = nullptr;
@@ -540,12 +570,12 @@ static void slab_workspace(aim_slab* S, int R) {
         Rk.sb = S->alloc<double2>(blk);
         Rk.rb = S->alloc<double2>(blk);
         Rk.hb = S->alloc<double2>(4LL * S->M * S->Ny * NzR);
-        std::vector<long long> off(S->world + 1, 0);
-        for (int w = 0; w < S->world; ++w) off[w + 1] = off[w] + 4LL * (S->KY[w + 1] - S->KY[w]) * Rk.Xl * ZR;
         Rk.d_off1 = S->alloc<long long>(S->world + 1);
-        h2d(Rk.d_off1, off.data(), sizeof(long long) * (S->world + 1), S->stream);
+        Rk.d_jtab = S->alloc<long long>(4 * (size_t)S->Py);
     }
     S->ws_nrhs = R;
+    S->tab_nrhs = 0;
+    slab_tables(S, R);
 }
 
 static aim_slab_rank* rank_of(aim_slab* S, int w) {
@@ -554,9 +584,21 @@ static aim_slab_rank* rank_of(aim_slab* S, int w) {
     return nullptr;
 }
 
+// The all-to-all pack fused into the y-pass store (and the unpack into the
+// inverse pass's load): planar layouts only (the y pass is the last before the
+// exchange), AIM_SLAB_FUSE_PACK=0 keeps the separate pack kernel.
+static bool slab_fuse_pack(const aim_slab* S) {
+    const char* e = getenv("AIM_SLAB_FUSE_PACK");
+    return S->planar && !(e && e[0] == '0');
+}
+
 // one y pass per component: [Xl][Ny -> Py][NzR] forward (Qh -> Y) or
-// [Xl][Py -> Ny][NzR] inverse (Y -> Qh); Y = Wy (planar) or Wy1 (3-D)
-static void slab_ypass(aim_slab* S, aim_slab_rank& Rk, int R, bool inverse, cudaStream_t s) {
+// [Xl][Py -> Ny][NzR] inverse (Y -> Qh); Y = Wy (planar) or Wy1 (3-D).
+// With `xbuf` (planar, fused exchange layout) the forward pass writes its lines
+// straight into the all-to-all #1 blocks of xbuf and the inverse pass reads them
+// from there (d_jtab); returns false if no table-addressed kernel takes the
+// pass (nothing launched: the caller runs the plain pass and the pack kernel).
+static bool slab_ypass(aim_slab* S, aim_slab_rank& Rk, int R, bool inverse, cudaStream_t s, double2* xbuf = nullptr) {
     const long long NzR = (long long)S->Nz * R;
     double2* Y = S->planar ? Rk.Wy : Rk.Wy1;
     for (int c = 0; c < 4; ++c) {
@@ -570,13 +612,23 @@ static void slab_ypass(aim_slab* S, aim_slab_rank& Rk, int R, bool inverse, cuda
             f.in = Rk.Qh + c * (long long)Rk.Xh * S->Ny * NzR;
             f.out = Y + c * (long long)Rk.Xl * S->Py * NzR;
             f.Lin = S->Ny; f.Lout = S->Py; f.mode = 0;
+            if (xbuf) { f.out = xbuf; f.jout = Rk.d_jtab + (size_t)c * S->Py; }
         } else {
             f.in = Y + c * (long long)Rk.Xl * S->Py * NzR;
             f.out = Rk.Qh + c * (long long)Rk.Xh * S->Ny * NzR;
             f.Lin = S->Py; f.Lout = S->Ny; f.mode = 1;
+            if (xbuf) { f.in = xbuf; f.jin = Rk.d_jtab + (size_t)c * S->Py; }
         }
-        launch_fft_pass(f, s);
+        if (xbuf) {
+            if (!try_launch_fft_pass_tab(f, s)) {
+                if (c) throw Error(AIM_E_GRID, "slab y pass: table-addressed kernel refused component " + std::to_string(c));
+                return false;
+            }
+        } else {
+            launch_fft_pass(f, s);
+        }
     }
+    return true;
 }
 
 // 3-D only: z pass over [4 Xl Py][Nz -> Pz][R] (Wy1 -> Wy) or back (Wy -> Wy1)
@@ -713,6 +765,7 @@ static void slab_core(aim_slab* S, int R, cudaStream_t s) {
     }
     // y (3-D: and z) forward on the owned planes, pack for all-to-all #1
     for (auto& Rk : S->ranks) {
+        if (slab_fuse_pack(S) && slab_ypass(S, Rk, R, false, s, Rk.sb)) continue;   // lines stored into the blocks
         slab_ypass(S, Rk, R, false, s);
         if (!S->planar) slab_zpass(S, Rk, R, false, s);
         const long long tot = 4LL * Rk.Xl * S->Py * ZR;
@@ -819,6 +872,7 @@ static void slab_core(aim_slab* S, int R, cudaStream_t s) {
     }
     T.run();
     for (auto& Rk : S->ranks) {
+        if (slab_fuse_pack(S) && slab_ypass(S, Rk, R, true, s, Rk.rb)) continue;    // lines loaded from the blocks
         const long long tot = 4LL * Rk.Xl * S->Py * ZR;
         slab_pack_kernel<true><<<nblk(tot, 256), 256, 0, s>>>(Rk.Wy, Rk.rb, Rk.Xl, S->Py, ZR, S->kyown, S->d_KY,
                                                                Rk.d_off1);

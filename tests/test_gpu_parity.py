@@ -129,43 +129,54 @@ def test_conv_modes_used():
     assert gpu_plan("t_vol").info["conv_mode"] in (0, 1)
 
 
+def _golden_matvec_rows(name, x):
+    """(rows, oracle y[rows]) of the full-size product for the seeded x.  The
+    values were written by tools/make_matvec_goldens.py, which calls only
+    oracle/ (OraclePlan.matvec_rows on stratified rows: every grid x-plane, D3
+    tie classes, 8-slab cuts, uniform rows); AIM_TEST_SLOW=1 (or a missing
+    file) recomputes them live with the oracle, as the writer does."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"matvec_{name}.npz")
+    if os.environ.get("AIM_TEST_SLOW") != "1" and os.path.exists(path):
+        d = np.load(path)
+        meta = json.loads(str(d["meta"]))
+        assert meta["N"] == x.shape[0] and meta["nrhs"] == x.shape[1] and meta["x_seed"] == 0
+        assert meta["x_planes_covered"] == meta["x_planes"]
+        return d["rows"], d["ref"]
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from make_matvec_goldens import golden_rows
+    from oracle.aim import OraclePlan
+    cfg = get_config(name)
+    O = OraclePlan(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    one = x.shape[1] == 1
+    rows = golden_rows(O, cfg, 640 if one else 400, 1000 if one else 500)
+    assert np.unique(O.bases[rows, 0]).size == np.unique(O.bases[:, 0]).size
+    return rows, O.matvec_rows(x, rows, method="fft" if one else "auto")
+
+
 def test_matvec_c2_full_size_sampled_rows():
     """configs[1] at full size (N=115,200, 16 RHS, bench launch config):
     sampled rows against the oracle computed row by row."""
-    G, O = gpu_plan("c2"), oracle_plan("c2")
-    x = make_vectors(O.N, 16, 0)
+    G = gpu_plan("c2")
+    x = make_vectors(G.N, 16, 0)
     y = G.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
-    rows = _stratified(O, get_config("c2"), n_random=400, min_rows=500)
+    rows, ref = _golden_matvec_rows("c2", x)
     assert rows.size >= 500
-    ref = O.matvec_rows(x, rows)
     assert rel(y[rows], ref) <= 1e-10
     assert np.abs(y[rows] - ref).max() <= 1e-10 * np.abs(ref).max()
-
-
-def _stratified(O, cfg, n_random=640, min_rows=1000):
-    """>= 1,000 rows: one RWG per grid x-plane, 32 of each D3 tie class (a
-    centre coordinate exactly on a stencil-placement tie), two on either side
-    of every boundary of an 8-slab partition, the first and last, uniform rows."""
-    from paper_1712_02443_b200 import slab_partition
-    from workloads.sketch import stratified_rows
-    t = O.centres / cfg.h - (cfg.M - 1) / 2.0
-    tie = np.abs(t - np.round(t)) <= 1e-6
-    X, _, _ = slab_partition(make_mesh(cfg), cfg.h, cfg.M, 8)
-    while True:
-        rows = stratified_rows(O.bases, n_random=n_random, seed=3, slab_bounds=X[1:-1], tie_mask=tie)
-        if rows.size >= min_rows:
-            return rows
-        n_random += min_rows - rows.size + 16
 
 
 @pytest.mark.parametrize("name", ["c3", "c5", "c4"])
 def test_matvec_full_size_sampled_rows(name):
     """configs[2], [4], [3] at full size (N = 526,068 / 1,119,744 / 1,843,200;
     one RHS, the launch configuration of their matvec) on >= 1,000 stratified
-    rows (every grid x-plane, tie classes, slab boundaries) against the oracle
-    (full projection + its own radix-2 FFT convolution, interpolation and exact
-    near rows for the sampled rows only): relative L2 <= 1e-10 and every row
-    within 1e-10 of the largest.  The GPU plan is released before the oracle runs."""
+    rows (every grid x-plane, tie classes, slab boundaries) against the oracle's
+    values (tests/golden/matvec_<config>.npz, written by the oracle-only
+    tools/make_matvec_goldens.py: full projection + its own radix-2 FFT
+    convolution, interpolation and exact near rows for the sampled rows):
+    relative L2 <= 1e-10 and every row within 1e-10 of the largest."""
     from paper_1712_02443_b200 import AimPlan
     cfg = get_config(name)
     mesh = make_mesh(cfg)
@@ -181,11 +192,8 @@ def test_matvec_full_size_sampled_rows(name):
         assert info["on"] == 1 and info["pi_on"] == 1 and info["tpl_nnz"] * 100 <= G.info["nnz_proj"]
         ys.append(G.matvec(xt).cpu().numpy())
     G.close()
-    from oracle.aim import OraclePlan
-    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    rows = _stratified(O, cfg)
-    assert rows.size >= 1000 and np.unique(O.bases[rows, 0]).size == np.unique(O.bases[:, 0]).size
-    ref = O.matvec_rows(x, rows, method="fft")
+    rows, ref = _golden_matvec_rows(name, x)
+    assert rows.size >= 1000
     for yy in ys:
         assert rel(yy[rows], ref) <= 1e-10
         assert np.abs(yy[rows] - ref).max() <= 1e-10 * np.abs(ref).max()
@@ -215,16 +223,14 @@ def test_matvec_c5_c64_full_size_sampled_rows():
     against the complex128 oracle, <= 1e-4 (BASELINE.json configs[4])."""
     from paper_1712_02443_b200 import AimPlan
     from paper_1712_02443_b200.api import C64
-    from oracle.aim import OraclePlan
     cfg = get_config("c5")
     mesh = make_mesh(cfg)
     x = make_vectors(mesh.n_rwg, 1, 0)
     G = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, precision=C64)
     y = G.matvec(torch.from_numpy(x.astype(np.complex64)).cuda()).cpu().numpy()
     G.close()
-    O = OraclePlan(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
-    rows = np.unique(np.concatenate([[0, O.N - 1], np.random.default_rng(2).integers(0, O.N, 32)]))
-    ref = O.matvec_rows(x, rows, method="fft")
+    rows, ref = _golden_matvec_rows("c5", x)
+    assert rows.size >= 1000
     assert rel(y[rows], ref) <= 1e-4
 
 

@@ -346,3 +346,30 @@ def test_near_pairs_equal_brute_force(name):
         Q = OraclePlan(make_mesh("t_one"), 2 * np.pi, 0.1, 2, r)
         rp, cols = Q.near_pairs()
         assert rp[-1] == (Q.N if r == 0 else Q.N ** 2)
+
+
+def test_matvec_golden_files_are_the_oracles():
+    """tests/golden/matvec_c*.npz (tools/make_matvec_goldens.py, oracle only):
+    metadata, row coverage (every grid x-plane), and -- on C2 -- a few stored
+    rows recomputed live with the oracle's row-sampled product."""
+    import json
+    import os
+    from workloads import get_config, make_mesh, make_vectors
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    sizes = {"c2": (115200, 16, 500), "c3": (526068, 1, 1000), "c4": (1843200, 1, 1000), "c5": (1119744, 1, 1000)}
+    for name, (N, R, nmin) in sizes.items():
+        d = np.load(os.path.join(gold, f"matvec_{name}.npz"))
+        meta = json.loads(str(d["meta"]))
+        assert (meta["N"], meta["nrhs"], meta["x_seed"]) == (N, R, 0)
+        assert meta["writer"].startswith("tools/make_matvec_goldens.py")
+        assert meta["x_planes_covered"] == meta["x_planes"]
+        rows, ref = d["rows"], d["ref"]
+        assert rows.size >= nmin and ref.shape == (rows.size, R) and np.all(np.diff(rows) > 0)
+        assert rows[0] == 0 and rows[-1] == N - 1 and np.isfinite(ref.view(np.float64)).all()
+    cfg = get_config("c2")
+    O = OraclePlan(make_mesh(cfg), cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    d = np.load(os.path.join(gold, "matvec_c2.npz"))
+    pick = np.linspace(0, d["rows"].size - 1, 5).astype(np.int64)
+    x = make_vectors(O.N, 16, 0)[:, 5:6].copy()          # one of the 16 columns (they are independent)
+    live = O.matvec_rows(x, d["rows"][pick])
+    assert np.abs(live - d["ref"][pick][:, 5:6]).max() <= 1e-12 * np.abs(d["ref"]).max()

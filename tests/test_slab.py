@@ -301,3 +301,39 @@ def test_slab_gmres_virtual_worlds_c2(world):
     assert float((Jg - J1).norm() / J1.norm()) <= 1e-10
     assert abs(rrg - rr1) <= 1e-8 * rr1
     slab.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,world,seq", [("c2", 4, (16, 1, 3)), ("c2", 3, (1,)), ("c4", 2, (1,))])
+def test_slab_fused_pack_equals_pack_kernel(name, world, seq, monkeypatch):
+    """Planar layouts with a compile-time y plan (C2: 210, C4: 784): the forward
+    y pass stores its lines straight into the all-to-all #1 blocks and the
+    inverse pass loads them from the received blocks (FftPass::jout / jin).
+    Bit-identical to the separate pack / unpack kernels (AIM_SLAB_FUSE_PACK=0),
+    2 launches per slab fewer, equal to the single plan to 1e-13; the nrhs
+    sequence shrinks below the workspace's nrhs (block offsets scale with nrhs)."""
+    import torch
+    from paper_1712_02443_b200 import AimPlan, AimSlabPlan, launch_count
+    cfg = get_config(name)
+    mesh = make_mesh(cfg)
+    single = AimPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius)
+    xs = [torch.from_numpy(make_vectors(mesh.n_rwg, r, 11 + r)).cuda() for r in seq]
+    y1 = [single.matvec(x) for x in xs]
+    single.close()
+    slab = AimSlabPlan.from_mesh(mesh, cfg.k, cfg.h, cfg.M, cfg.near_radius, world)
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("AIM_SLAB_FUSE_PACK", fuse)
+        ys, n = [], []
+        for x in xs:
+            slab.matvec(x)                      # workspace, tables
+            c0 = launch_count()
+            ys.append(slab.matvec(x))
+            n.append(launch_count() - c0)
+        out[fuse] = (ys, n)
+    for i in range(len(xs)):
+        for fuse in ("1", "0"):
+            assert float((out[fuse][0][i] - y1[i]).norm() / y1[i].norm()) <= 1e-13, (fuse, i)
+        assert torch.equal(out["1"][0][i], out["0"][0][i])
+        assert out["0"][1][i] - out["1"][1][i] == 2 * world
+    slab.close()
