@@ -16,6 +16,10 @@
 // One HBM round trip of the plane instead of the three passes (y forward to
 // the y-padded W2, z Toeplitz on W2, y inverse back) of the unfused mode 2.
 
+#ifndef AIM_YM2_PRUNE
+#define AIM_YM2_PRUNE 1   // skip the zero-padding rows in the first forward / last inverse stage
+#endif
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
@@ -54,7 +58,11 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // offset m = j % ST) on positions base + t ST, base = (j / ST) R ST + m.
 //   DIF (forward): b = DFT_R(a) (sign -), b_k *= w_{R ST}^{m k}
 //   DIT (inverse): a_t *= conj(w_{R ST}^{m t}), b = DFT_R(a) (sign +)
-template <int P, int R, int ST, int NZ, bool DIF>
+// TLD < R: only inputs t < TLD are read, the others are zero (first forward
+// stage: rows >= P/2 are y padding); TST < R: only outputs t < TST are stored
+// (last inverse stage: rows >= P/2 are pruned), the rest of the butterfly's
+// outputs is dead code.
+template <int P, int R, int ST, int NZ, bool DIF, int TLD = R, int TST = R>
 __device__ __forceinline__ void ym2_stage(double2* tile, const double2* tw) {
     if constexpr (R == 1) return;        // two-stage plans (R3 = 1)
     constexpr int NB = P / R;            // butterflies per column
@@ -66,7 +74,7 @@ __device__ __forceinline__ void ym2_stage(double2* tile, const double2* tw) {
         const int base = (j / ST) * R * ST + m;
         double2 a[R];
 #pragma unroll
-        for (int t = 0; t < R; ++t) a[t] = tile[(base + t * ST) * NZ + l];
+        for (int t = 0; t < R; ++t) a[t] = t < TLD ? tile[(base + t * ST) * NZ + l] : make_double2(0, 0);
         if constexpr (DIF) {
             dft<R>(a, -1.0);
 #pragma unroll
@@ -86,7 +94,8 @@ __device__ __forceinline__ void ym2_stage(double2* tile, const double2* tw) {
             dft<R>(a, 1.0);
         }
 #pragma unroll
-        for (int t = 0; t < R; ++t) tile[(base + t * ST) * NZ + l] = a[t];
+        for (int t = 0; t < R; ++t)
+            if (t < TST) tile[(base + t * ST) * NZ + l] = a[t];
     }
 }
 
@@ -96,6 +105,10 @@ __global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ 
                                                            const double2* __restrict__ twg, int planes) {
     static_assert(R1 * R2 * R3 == P, "radices");
     constexpr int S1 = R2 * R3;
+    // rows >= P/2 are zero padding on input and pruned on output (Ny <= (P + 1) / 2):
+    // the first forward stage reads, and the last inverse stage writes, only t < TH
+    constexpr int TH = AIM_YM2_PRUNE ? (R1 + 1) / 2 : R1;
+    constexpr int ZEND = (TH * S1 < P ? TH * S1 : P) * NZ;
     extern __shared__ __align__(128) unsigned char ym2_raw[];
     double2* tile = reinterpret_cast<double2*>(ym2_raw);     // [P][NZ]
     double2* tw = tile + P * NZ;                             // [P]
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ 
             mbar_expect_tx(&mbar, bytes);
             bulk_g2s(tile, plane, bytes, &mbar);
         }
-        for (int e = Ny * NZ + threadIdx.x; e < P * NZ; e += blockDim.x) tile[e] = make_double2(0, 0);
+        for (int e = Ny * NZ + threadIdx.x; e < ZEND; e += blockDim.x) tile[e] = make_double2(0, 0);
         mbar_wait(&mbar, phase);
         phase ^= 1;
         // the next plane of this CTA into L2 while this one is transformed
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ 
                          : "memory");
         __syncthreads();
         // 2. forward y FFT (DIF), digit-reversed output
-        ym2_stage<P, R1, S1, NZ, true>(tile, tw);
+        ym2_stage<P, R1, S1, NZ, true, TH, R1>(tile, tw);
         __syncthreads();
         ym2_stage<P, R2, R3, NZ, true>(tile, tw);
         __syncthreads();
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(NT, MINB) ymode2_kernel(double2* __restrict__ 
         __syncthreads();
         ym2_stage<P, R2, R3, NZ, false>(tile, tw);
         __syncthreads();
-        ym2_stage<P, R1, S1, NZ, false>(tile, tw);
+        ym2_stage<P, R1, S1, NZ, false, R1, TH>(tile, tw);
         // 5. store rows 0 .. Ny-1
         fence_async_smem();
         __syncthreads();
@@ -376,6 +389,7 @@ bool launch_ymode2(void* W, int prec, int Px, int Ny, int Nz, int Py, int R, con
     const char* env = getenv("AIM_YZ_FUSED");
     const bool off = env && env[0] == '0';
     if (off || prec != 0 || R != 1) return false;
+    if (2 * Ny > Py + 1) return false;   // the pruned first/last stages assume rows >= ceil(Py/2) are padding
     int dev = 0;
     AIM_CUDA(cudaGetDevice(&dev));
     const int planes = 4 * Px;
